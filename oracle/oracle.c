@@ -1,0 +1,323 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct fp64 CPU oracle for the CogDL
+ * (arXiv 2103.00959) sparse-operator hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2103_00959_b200/csrc, include/gsp.h) and includes neither.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
+ *        (IEEE double on x86-64 SSE2, no FMA contraction).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section / equation in
+ * brackets); "S:n" = SPEC.md line n; "A<k>" = DESIGN.md ambiguity reading k.
+ *
+ * Every function works on caller-owned host arrays and returns 0 on success
+ * or a negative code on invalid input.  Row-range entry points ([r0, r1))
+ * write output row u at (u - r0) so huge graphs can be checked in pieces.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_ERR_ARG (-1)
+#define ORC_ERR_RANGE (-2)
+#define ORC_ERR_NEGATIVE (-3)
+#define ORC_ERR_NONFINITE (-4)
+#define ORC_ERR_CAPACITY (-5)
+#define ORC_ERR_NOMEM (-6)
+
+int orc_version(void) { return 1; }
+
+/* ---------------------------------------------------------------------------
+ * 1. COO -> canonical CSR of A~ = A + fill*I.
+ *    P:625-632 [§4 Graph Notations: A binary or weighted, A_ij >= 0, directed
+ *    or undirected; undirected => e_ij = e_ji, A_ij = A_ji];
+ *    P:244 [Eq. gcn_layer: A~ = A + I_n]; P:646 [§4.1: CSR-format design];
+ *    A2 (fill is ADDED to an existing (u,u)), A4 (duplicates summed in input
+ *    order), A5 (undirected: (v,u) added for u != v), A6 (reject w < 0 and
+ *    non-finite w; keep explicit zeros).
+ *
+ *    Entry i of the input (u_i, v_i, w_i) produces (u_i, v_i, w_i, pos=2i) and,
+ *    when undirected and u_i != v_i, (v_i, u_i, w_i, pos=2i+1).  Node u's
+ *    self-loop (fill != 0) is (u, u, fill, pos=2m+u).  Entries are sorted by
+ *    (row, col, pos); equal (row, col) are summed in pos order in fp64 and
+ *    rounded once to fp32.  row_ptr[u] = number of distinct entries in rows < u.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t row, col, pos;
+  double w;
+} orc_entry;
+
+static int cmp_entry(const void *pa, const void *pb) {
+  const orc_entry *a = (const orc_entry *)pa, *b = (const orc_entry *)pb;
+  if (a->row != b->row) return a->row < b->row ? -1 : 1;
+  if (a->col != b->col) return a->col < b->col ? -1 : 1;
+  if (a->pos != b->pos) return a->pos < b->pos ? -1 : 1;
+  return 0;
+}
+
+int orc_build_csr(int64_t n, int64_t m, const int64_t *src, const int64_t *dst,
+                  const float *w /* nullable: all 1.0 */, int undirected, float fill,
+                  int64_t *row_ptr /* [n+1] */, int32_t *col /* [cap] */,
+                  float *val /* [cap] */, int64_t cap, int64_t *nnz_out) {
+  if (n < 0 || m < 0 || !row_ptr || !nnz_out || (m > 0 && (!src || !dst))) return ORC_ERR_ARG;
+  int64_t total = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    if (src[i] < 0 || src[i] >= n || dst[i] < 0 || dst[i] >= n) return ORC_ERR_RANGE;
+    if (w) {
+      if (!isfinite(w[i])) return ORC_ERR_NONFINITE;
+      if (w[i] < 0.0f) return ORC_ERR_NEGATIVE;
+    }
+    total += (undirected && src[i] != dst[i]) ? 2 : 1;
+  }
+  if (!isfinite(fill)) return ORC_ERR_NONFINITE;
+  if (fill < 0.0f) return ORC_ERR_NEGATIVE;
+  if (fill != 0.0f) total += n;
+
+  orc_entry *e = (orc_entry *)malloc(sizeof(orc_entry) * (size_t)(total > 0 ? total : 1));
+  if (!e) return ORC_ERR_NOMEM;
+  int64_t k = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    double wi = w ? (double)w[i] : 1.0;
+    e[k].row = src[i]; e[k].col = dst[i]; e[k].pos = 2 * i; e[k].w = wi; ++k;
+    if (undirected && src[i] != dst[i]) {
+      e[k].row = dst[i]; e[k].col = src[i]; e[k].pos = 2 * i + 1; e[k].w = wi; ++k;
+    }
+  }
+  if (fill != 0.0f)
+    for (int64_t u = 0; u < n; ++u) {
+      e[k].row = u; e[k].col = u; e[k].pos = 2 * m + u; e[k].w = (double)fill; ++k;
+    }
+  qsort(e, (size_t)total, sizeof(orc_entry), cmp_entry);
+
+  /* coalesce equal (row, col): fp64 sum in pos order, then one rounding */
+  int64_t nnz = 0;
+  for (int64_t u = 0; u <= n; ++u) row_ptr[u] = 0;
+  for (int64_t a = 0; a < total;) {
+    int64_t b = a;
+    double s = 0.0;
+    while (b < total && e[b].row == e[a].row && e[b].col == e[a].col) { s += e[b].w; ++b; }
+    if (nnz >= cap) { free(e); return ORC_ERR_CAPACITY; }
+    if (col) col[nnz] = (int32_t)e[a].col;
+    if (val) val[nnz] = (float)s;
+    row_ptr[e[a].row + 1] += 1;
+    ++nnz;
+    a = b;
+  }
+  for (int64_t u = 0; u < n; ++u) row_ptr[u + 1] += row_ptr[u];
+  *nnz_out = nnz;
+  free(e);
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 2. Degree and symmetric normalisation.
+ *    P:244 [Eq. gcn_layer: A^ = D~^-1/2 A~ D~^-1/2, D~_ii = sum_j A~_ij];
+ *    A3 (row sums on both sides), A7 (a^ = 0 when d_u*d_v = 0), A8 (formula
+ *    a^_uv = w_uv / sqrt(d_u * d_v), IEEE double, then one rounding to fp32).
+ *    d_u is summed sequentially in column order.
+ *    Outputs: deg [n] (nullable), a64 [nnz] (nullable, unrounded),
+ *    a32 [nnz] (nullable, fp32-rounded a64).
+ * ------------------------------------------------------------------------- */
+int orc_sym_norm(int64_t n, const int64_t *row_ptr, const int32_t *col, const float *w,
+                 double *deg, double *a64, float *a32) {
+  if (n < 0 || !row_ptr || !col || !w) return ORC_ERR_ARG;
+  double *d = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  if (!d) return ORC_ERR_NOMEM;
+  for (int64_t u = 0; u < n; ++u) {
+    double s = 0.0;
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) s += (double)w[e];
+    d[u] = s;
+    if (deg) deg[u] = s;
+  }
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      double p = d[u] * d[col[e]];
+      double r = 0.0;
+      if (p != 0.0) {
+        double q = sqrt(p);
+        r = (double)w[e] / q;
+      }
+      if (a64) a64[e] = r;
+      if (a32) a32[e] = (float)r;
+    }
+  free(d);
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 3. SpMM  Y = A X  (GSpMM with phi = sum, psi = multiply).
+ *    P:640-645 [§4.1 Eq. formula:1: h_u = phi(psi(h_v, h_e)), v in N(u),
+ *    e = (u,v); "SpMM operator H^(l+1) <- A H^(l)"]; A1 (pair (u,v) is stored
+ *    at row u, col v).  a == NULL means unit weights (psi = copy).
+ *    y[u,k] = sum_e a_e * x[col_e, k] in fp64; cond[u,k] = sum_e |a_e x[col_e,k]|
+ *    (the condition sum used by the parity bound).  Rows [r0, r1).
+ * ------------------------------------------------------------------------- */
+int orc_spmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col,
+             const double *a, const float *x, int64_t f, int64_t ldx,
+             double *y, double *cond, int64_t ldy) {
+  if (r0 < 0 || r1 < r0 || f < 0 || ldx < f || ldy < f || !row_ptr || (!col && r1 > r0) || !x || !y)
+    return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u) {
+    double *yu = y + (u - r0) * ldy;
+    double *cu = cond ? cond + (u - r0) * ldy : NULL;
+    for (int64_t k = 0; k < f; ++k) { yu[k] = 0.0; if (cu) cu[k] = 0.0; }
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      double ae = a ? a[e] : 1.0;
+      const float *xv = x + (int64_t)col[e] * ldx;
+      for (int64_t k = 0; k < f; ++k) {
+        double t = ae * (double)xv[k];
+        yu[k] += t;
+        if (cu) cu[k] += fabs(t);
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 4. Edge-wise softmax, per head.
+ *    P:653-656 [§4.1: alpha'_uv = exp(alpha_uv) / sum_{w in N(u)} exp(alpha_uw);
+ *    "first apply the scan to find the max value ... subtract this maximum ...
+ *    apply the exponent function and reduce ... to acquire the sum"];
+ *    A9 (denominator over the whole row), A10 (max is a reduction),
+ *    A12 (empty rows emit nothing).  logits/alpha are [nnz][heads].
+ * ------------------------------------------------------------------------- */
+int orc_edge_softmax(int64_t r0, int64_t r1, const int64_t *row_ptr, int64_t heads,
+                     const double *logits, double *alpha) {
+  if (r0 < 0 || r1 < r0 || heads <= 0 || !row_ptr || !logits || !alpha) return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u) {
+    int64_t b = row_ptr[u], e1 = row_ptr[u + 1];
+    if (b == e1) continue;
+    for (int64_t h = 0; h < heads; ++h) {
+      double mx = -INFINITY;
+      for (int64_t e = b; e < e1; ++e) if (logits[e * heads + h] > mx) mx = logits[e * heads + h];
+      double s = 0.0;
+      for (int64_t e = b; e < e1; ++e) s += exp(logits[e * heads + h] - mx);
+      for (int64_t e = b; e < e1; ++e) alpha[e * heads + h] = exp(logits[e * heads + h] - mx) / s;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 5. GAT per-edge attention score ("masked self-attentional layers";
+ *    the formula is not printed in the paper -> A13 / S:503, S:544 split form):
+ *    s[e,h] = LeakyReLU(el[u,h] + er[v,h]; slope), e = (u,v) in row u.
+ *    el is [n_rows][heads] (aggregating row), er is [n_cols][heads] (neighbour).
+ * ------------------------------------------------------------------------- */
+int orc_gat_scores(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col,
+                   int64_t heads, const float *el, const float *er, double slope, double *s) {
+  if (r0 < 0 || r1 < r0 || heads <= 0 || !row_ptr || !el || !er || !s) return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u)
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e)
+      for (int64_t h = 0; h < heads; ++h) {
+        double t = (double)el[u * heads + h] + (double)er[(int64_t)col[e] * heads + h];
+        s[e * heads + h] = t >= 0.0 ? t : slope * t;
+      }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 6. Multi-head SpMM.  P:648-649 [§4.1 multi-head SpMM: heads share the
+ *    sparsity pattern]; A14 (Z, Y are [n][H][D], alpha [nnz][H]).
+ *    y[u,h,d] = sum_e alpha[e,h] * z[col_e,h,d]; cond likewise with |.|.
+ * ------------------------------------------------------------------------- */
+int orc_multihead_spmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col,
+                       int64_t heads, const double *alpha, const float *z, int64_t d,
+                       int64_t ldz, double *y, double *cond, int64_t ldy) {
+  if (r0 < 0 || r1 < r0 || heads <= 0 || d < 0 || ldz < heads * d || ldy < heads * d ||
+      !row_ptr || !alpha || !z || !y)
+    return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u) {
+    double *yu = y + (u - r0) * ldy;
+    double *cu = cond ? cond + (u - r0) * ldy : NULL;
+    for (int64_t k = 0; k < heads * d; ++k) { yu[k] = 0.0; if (cu) cu[k] = 0.0; }
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      const float *zv = z + (int64_t)col[e] * ldz;
+      for (int64_t h = 0; h < heads; ++h) {
+        double ah = alpha[e * heads + h];
+        for (int64_t k = 0; k < d; ++k) {
+          double t = ah * (double)zv[h * d + k];
+          yu[h * d + k] += t;
+          if (cu) cu[h * d + k] += fabs(t);
+        }
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 7. Attention projection (A13; S:503, S:544 split form of a^T [z_u || z_v]):
+ *    el[u,h] = sum_d a_l[h,d] z[u,h,d];  er[u,h] = sum_d a_r[h,d] z[u,h,d].
+ *    *_cond = sum_d |a z| (dot-product tolerance).  Rows [r0, r1).
+ * ------------------------------------------------------------------------- */
+int orc_attn_project(int64_t r0, int64_t r1, int64_t heads, int64_t d, const float *z, int64_t ldz,
+                     const float *a_l, const float *a_r, double *el, double *er,
+                     double *el_cond, double *er_cond) {
+  if (r0 < 0 || r1 < r0 || heads <= 0 || d < 0 || ldz < heads * d || !z || !a_l || !a_r || !el || !er)
+    return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u)
+    for (int64_t h = 0; h < heads; ++h) {
+      double sl = 0.0, sr = 0.0, cl = 0.0, cr = 0.0;
+      for (int64_t k = 0; k < d; ++k) {
+        double zv = (double)z[u * ldz + h * d + k];
+        double tl = (double)a_l[h * d + k] * zv, tr = (double)a_r[h * d + k] * zv;
+        sl += tl; sr += tr; cl += fabs(tl); cr += fabs(tr);
+      }
+      int64_t o = (u - r0) * heads + h;
+      el[o] = sl; er[o] = sr;
+      if (el_cond) el_cond[o] = cl;
+      if (er_cond) er_cond[o] = cr;
+    }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 8. Row partition balanced by nnz (DESIGN.md multi-GPU):
+ *    bound_p = lower_bound(row_ptr[0..n], ceil(p * nnz / P)) for 0 < p < P,
+ *    bound_0 = 0, bound_P = n.  lower_bound = first r with row_ptr[r] >= t.
+ *    Plain linear scan.
+ * ------------------------------------------------------------------------- */
+int orc_partition_rows(int64_t n, const int64_t *row_ptr, int64_t parts, int64_t *bounds) {
+  if (n < 0 || parts <= 0 || !row_ptr || !bounds) return ORC_ERR_ARG;
+  int64_t nnz = row_ptr[n];
+  bounds[0] = 0;
+  for (int64_t p = 1; p < parts; ++p) {
+    int64_t t = (p * nnz + parts - 1) / parts;
+    int64_t r = 0;
+    while (r < n && row_ptr[r] < t) ++r;
+    bounds[p] = r;
+  }
+  bounds[parts] = n;
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * 9. CSR slice for rank `rank` with columns remapped into the padded
+ *    all-gather layout: rows [b_rank, b_rank+1); a column c
+ *    owned by rank q (b_q <= c < b_q+1) becomes q * rows_padded + (c - b_q).
+ *    row_ptr_out [rows+1] starts at 0; values are copied unchanged.
+ * ------------------------------------------------------------------------- */
+int orc_csr_slice(int64_t n, const int64_t *row_ptr, const int32_t *col, const float *val,
+                  const int64_t *bounds, int64_t parts, int64_t rank, int64_t rows_padded,
+                  int64_t *row_ptr_out, int32_t *col_out, float *val_out) {
+  if (n < 0 || parts <= 0 || rank < 0 || rank >= parts || !row_ptr || !bounds || !row_ptr_out)
+    return ORC_ERR_ARG;
+  int64_t r0 = bounds[rank], r1 = bounds[rank + 1];
+  int64_t base = row_ptr[r0];
+  for (int64_t u = r0; u <= r1; ++u) row_ptr_out[u - r0] = row_ptr[u] - base;
+  for (int64_t e = row_ptr[r0]; e < row_ptr[r1]; ++e) {
+    int64_t c = col[e];
+    int64_t q = 0;
+    while (!(bounds[q] <= c && c < bounds[q + 1])) ++q;
+    if (col_out) col_out[e - base] = (int32_t)(q * rows_padded + (c - bounds[q]));
+    if (val_out && val) val_out[e - base] = val[e];
+  }
+  return ORC_OK;
+}
