@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py -- SpMM GE/s and achieved HBM GB/s on the Reddit-shaped graph.
+
+Workload (BASELINE.json metric): C4, a Chung-Lu power-law
+graph with Reddit's node / edge counts (232,965 nodes, 11,606,919 undirected
+pairs -> nnz(A^) = 23,446,803), 602 fp32 features (ld 604).  One STEP is
+Y = A^ X through gsp_spmm (one kernel launch); A^ is built (gsp_coo_to_csr)
+and normalised (gsp_sym_normalize) once before timing -- both are reported as
+components.  The GAT path (C3, Flickr-shaped, 8 heads x 64) is reported as a
+secondary object.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (row partition + NCCL all-gather)
+
+Timing: W untimed warm-ups, then K steps each bracketed by CUDA events on the
+launching stream, with an L2 flush (256 MB memset, untimed) before every step;
+barrier + synchronize around the timed loop; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_PATH))["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def spmm_alg_bytes(n, nnz, f):
+    """Gather-model algorithmic bytes of one Y = A X (DESIGN.md
+    §Roofline): one X row-slab per nonzero + Y write + col/val + row_ptr."""
+    return 4 * nnz * f + 4 * n * f + 8 * nnz + 8 * (n + 1)
+
+
+def gat_alg_bytes(n, nnz, H, D):
+    """GAT aggregate: Z gathers + Y write + col + row_ptr + gathered er + el."""
+    return 4 * nnz * H * D + 4 * n * H * D + 4 * nnz + 8 * (n + 1) + 4 * nnz * H + 4 * n * H
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.1)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/*ncu_full*.json), or None."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json"))):
+        try:
+            d = json.load(open(p))
+        except Exception:
+            continue
+        if d.get("workload") == workload and d.get("dram_bytes_per_launch"):
+            best = d["dram_bytes_per_launch"]
+    return best
+
+
+# ---------------------------------------------------------------------------
+# oracle timing (reference arm and cpu_baseline): the oracle as it stands
+# ---------------------------------------------------------------------------
+
+def oracle_sample_rate(row_ptr, col, a64, x, f, budget_ge, start_row=0):
+    """Time the fp64 oracle SpMM (single thread) on a contiguous row sample of
+    about budget_ge edge x feature units; returns (GE/s, seconds, rows, ge)."""
+    import oracle as orc
+    nnz_target = max(1, int(budget_ge // f))
+    r0 = start_row % (row_ptr.size - 1)
+    r1 = int(np.searchsorted(row_ptr, row_ptr[r0] + nnz_target, side="left"))
+    r1 = max(r0 + 1, min(r1, row_ptr.size - 1))
+    ge = int(row_ptr[r1] - row_ptr[r0]) * f
+    t0 = time.perf_counter()
+    orc.spmm(row_ptr, col, a64, x, f=f, r0=r0, r1=r1, want_cond=False)
+    dt = time.perf_counter() - t0
+    return ge / dt, dt, (r0, r1), ge
+
+
+def host_graph(cfg, seed=1):
+    """Host CSR of A^ for the oracle (built by the oracle itself)."""
+    import oracle as orc
+    from synth import graph_for
+    s, d = graph_for(cfg, seed=seed)
+    g = orc.build_csr(cfg.n, s, d, None, True, 1.0)
+    _, a64, _ = orc.sym_norm(g)
+    return g, a64
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on host cores, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from synth import CONFIGS, features
+    cfg = CONFIGS[args.config]
+    g, a64 = host_graph(cfg)
+    x = features(cfg.n, cfg.f, cfg.ld, seed=2)
+    budget = args.ref_budget_ge
+    times, ges = [], []
+    for i in range(args.warmup + args.steps):
+        rate, dt, rows, ge = oracle_sample_rate(g.row_ptr, g.col, a64, x, cfg.f, budget, start_row=i * 7919)
+        if i >= args.warmup:
+            times.append(dt)
+            ges.append(ge)
+    value = float(sum(ges) / sum(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GE/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "nnz": cfg.nnz, "f": cfg.f, "graph": "chung-lu gamma=2.5 seed=1",
+                   "sample": f"each step: contiguous row range with ~{budget / 1e9:.2f} G edge x feature units"},
+        "cpu_baseline": {"value": value, "unit": "GE/s", "cores": 1, "kind": "oracle",
+                         "sample": f"~{budget / 1e9:.2f} G GE contiguous rows per step, fp64 single thread"},
+        "e2e": {"value": value, "unit": "GE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--slab-cols", type=int, default=0)
+    ap.add_argument("--block-nnz", type=int, default=0)
+    ap.add_argument("--chunks", type=int, default=4, help="feature chunks for comm/compute overlap (N>1)")
+    ap.add_argument("--no-gat", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-ge", type=float, default=1.5e9)
+    ap.add_argument("--ref-budget-ge", type=float, default=0.25e9)
+    ap.add_argument("--sweep", default="", help="comma list of slab widths to time (diagnostic)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_00959_b200 as G
+    from synth import CONFIGS, features, graph_for, uniform
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    G.lib()  # fail loudly if the extension is missing
+
+    cfg = CONFIGS[args.config]
+    src, dst = graph_for(cfg, seed=1)
+    s_t = torch.from_numpy(src).to(dev)
+    d_t = torch.from_numpy(dst).to(dev)
+    # --- a1 + a2: one-off build + normalisation (components) ---
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    torch.cuda.synchronize()
+    e0.record()
+    g = G.gsp_coo_to_csr(cfg.n, s_t, d_t, None, True, 1.0)
+    e1.record()
+    gn = G.gsp_sym_normalize(g, in_place=False)
+    e2.record()
+    torch.cuda.synchronize()
+    build_ms, norm_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
+    del s_t, d_t
+    n, nnz, f = cfg.n, gn.nnz, cfg.f
+    x_host = features(n, f, cfg.ld, seed=2)
+    x = torch.from_numpy(x_host).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    if world > 1:
+        from paper_2103_00959_b200.dist import RowPartitionedSpMM
+        op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev)
+        op.load_shard(x[op.r0:op.r1, :f])
+        del x
+        y = torch.empty((op.rows, f), dtype=torch.float32, device=dev)
+
+        def step():
+            op(y)
+        launches_per_step = len(op.cols) - 1
+    else:
+        y = torch.empty((n, f), dtype=torch.float32, device=dev)
+
+        def step():
+            G.gsp_spmm(gn, x, f=f, y=y, slab_cols=args.slab_cols, block_nnz=args.block_nnz)
+        launches_per_step = 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush (untimed: outside the events)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ge = nnz * f
+    value = ge / (t_ms * 1e-3)
+
+    peak, peak_kind = hbm_peak()
+    alg = spmm_alg_bytes(n, nnz, f) / world
+    achieved = alg / (t_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "GE/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "ms_per_step_median": float(np.median(times)),
+        "ms_per_step_min": float(np.min(times)), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ld": cfg.ld,
+                   "graph": "chung-lu gamma=2.5 seed=1 (Reddit node/edge counts, P:25)",
+                   "l2": "flushed before every step (256 MB memset, untimed); X (562 MB) > L2 as well",
+                   "parallelism": f"row-partition x{world}" + (f" + NCCL all-gather ({args.chunks} chunks)" if world > 1 else ""),
+                   "slab_cols": args.slab_cols or "auto", "block_nnz": args.block_nnz or "auto"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(cfg.name) if world == 1 else None,
+                     "kernel": "engine_kernel<4,*,WeightVal> (gsp_spmm)",
+                     "alg_bytes_per_launch": alg, "peak_kind": f"{peak_kind} hbm_gbs (copy, MEASURED_PEAKS.json)",
+                     "model": "gather model: 4*nnz*F + 4*n*F + 8*nnz + 8*(n+1) bytes per launch"},
+        "components": {"build_ms": build_ms, "normalize_ms": norm_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+    }
+
+    if world == 1 and args.sweep:
+        sw = {}
+        for sc in [int(v) for v in args.sweep.split(",")]:
+            ts = []
+            for i in range(args.warmup + 10):
+                flush.zero_()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                G.gsp_spmm(gn, x, f=f, y=y, slab_cols=sc)
+                a1.record()
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    ts.append(a0.elapsed_time(a1))
+            sw[str(sc)] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3),
+                           "alg_GB/s": spmm_alg_bytes(n, nnz, f) / (np.mean(ts) * 1e-3) / 1e9}
+        out["sweep_slab_cols"] = sw
+
+    # --- e2e: host buffers, H2D + kernel + D2H inside the timed region ---
+    if world == 1 and not args.no_e2e:
+        xh = torch.from_numpy(x_host).pin_memory()
+        yh = torch.empty((n, f), dtype=torch.float32).pin_memory()
+        ts = []
+        for i in range(args.warmup + max(3, args.steps // 3)):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            x.copy_(xh, non_blocking=True)
+            G.gsp_spmm(gn, x, f=f, y=y)
+            yh.copy_(y, non_blocking=True)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ts.append(a0.elapsed_time(a1))
+        te = float(np.mean(ts))
+        out["e2e"] = {"value": ge / (te * 1e-3), "unit": "GE/s", "ms_per_step": te,
+                      "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4),
+                      "api": "gsp_spmm via the Python binding of the C ABI, pinned host X -> device -> host Y"}
+    elif world > 1:
+        out["e2e"] = None
+
+    # --- secondary: fused GAT aggregate on the Flickr-shaped graph (C3) ---
+    if world == 1 and not args.no_gat:
+        c3 = CONFIGS["C3"]
+        H, D = c3.heads, c3.d
+        s3, d3 = graph_for(c3, seed=1)
+        g3 = G.gsp_coo_to_csr(c3.n, torch.from_numpy(s3).to(dev), torch.from_numpy(d3).to(dev), None, True, 1.0)
+        z = torch.from_numpy(uniform((c3.n, H * D), seed=3)).to(dev)
+        al = torch.from_numpy(uniform((H, D), seed=6).reshape(-1)).to(dev)
+        ar = torch.from_numpy(uniform((H, D), seed=7).reshape(-1)).to(dev)
+        el, er = G.gsp_attn_project(z, al, ar, H, D)
+        y3 = torch.empty((c3.n, H * D), dtype=torch.float32, device=dev)
+        ws = torch.empty(G.gsp_gat_workspace(g3, H), dtype=torch.uint8, device=dev)
+        tg, tp = [], []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a0.record()
+            G.gsp_attn_project(z, al, ar, H, D, el=el, er=er)
+            a1.record()
+            G.gsp_gat_aggregate(g3, el, er, z, H, D, 0.2, y=y3, ws=ws)
+            a2.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                tp.append(a0.elapsed_time(a1))
+                tg.append(a1.elapsed_time(a2))
+        tgm = float(np.mean(tg))
+        gb = gat_alg_bytes(c3.n, g3.nnz, H, D)
+        out["secondary"] = {"C3_gat": {
+            "workload": c3.name, "n": c3.n, "nnz": g3.nnz, "heads": H, "d": D,
+            "aggregate_ms": tgm, "attn_project_ms": float(np.mean(tp)),
+            "GE/s": g3.nnz * H * D / (tgm * 1e-3),
+            "alg_GB/s": gb / (tgm * 1e-3) / 1e9, "frac_of_hbm_peak": gb / (tgm * 1e-3) / 1e9 / peak,
+            "launches": "row_stats + engine_kernel<*,*,WeightGat> per aggregate"}}
+
+    # --- cpu_baseline: the oracle as it stands, bounded sample, rank 0 at N=1 ---
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            import oracle as orc
+            gh_rp = gn.row_ptr.cpu().numpy()
+            gh_col = gn.col.cpu().numpy()
+            a64 = orc.sym_norm(orc.CSR(n, gh_rp, gh_col, g.val.cpu().numpy()))[1]
+            rate, dt, rows, ge_s = oracle_sample_rate(gh_rp, gh_col, a64, x_host, f, args.cpu_budget_ge)
+            out["cpu_baseline"] = {"value": rate, "unit": "GE/s", "cores": 1, "kind": "oracle",
+                                   "sample": f"rows [{rows[0]}, {rows[1]}) of {cfg.name}: {ge_s / 1e9:.2f} G GE, "
+                                             f"fp64 single thread, {dt:.1f} s"}
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,247 @@
+/*
+ * gsp.h -- C ABI of libgsp: B200-native (sm_100a) sparse GNN operators after
+ * CogDL (arXiv 2103.00959), §4 "Efficiency of CogDL".
+ *
+ * Citations: "P:n" = PAPER.md line n, with the section / equation named;
+ * "S:n" = SPEC.md line n (interface source only); "A<k>" = reading k of the
+ * ambiguity register in DESIGN.md.
+ *
+ * CONVENTIONS (apply to every call)
+ *  - Memory.  Every array argument is caller-owned DEVICE memory unless the
+ *    parameter says "host".  The library never allocates device memory; calls
+ *    that need scratch take a caller workspace sized by a *_workspace query.
+ *  - Streams.  Every call enqueues its kernels on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream) and returns without synchronising, except
+ *    gsp_coo_to_csr and (with a host output) gsp_partition_rows, which
+ *    synchronise `stream`
+ *    (documented on each).
+ *  - Layout.  Dense matrices are row-major fp32 with an explicit row stride
+ *    `ld` in elements (ld >= width).  Multi-head matrices are [n][H][D]
+ *    (D fastest, A14); per-edge per-head arrays are [nnz][H] in canonical CSR
+ *    order (edge-major, head-minor).  Vectorised (16-byte) paths are
+ *    used when ld % 4 == 0 and base pointers are 16-byte aligned; otherwise a
+ *    narrower path runs.  Misalignment is never an error.
+ *  - Outputs are fully overwritten (beta = 0); empty rows give zeros.
+ *    Columns of an output beyond its logical width (the ld padding) are not
+ *    written.
+ *  - Errors.  Arguments are validated on the host BEFORE any launch; on a
+ *    host-detected error the call returns non-zero and touches nothing.
+ *    gsp_last_error_detail() returns a thread-local description of the last
+ *    error.  Launch failures return GSP_ERR_CUDA.
+ *  - Determinism.  Every call is bitwise reproducible run to run (no
+ *    floating-point atomics).  gsp_spmm / gsp_multihead_spmm /
+ *    gsp_gat_aggregate use a summation order that depends only on the row
+ *    (DESIGN.md §Summation order), so the result of a row does not depend on
+ *    which other rows are in the call: a row-partitioned multi-GPU run is
+ *    bitwise equal to the single-GPU run.
+ *  - Threads.  Re-entrant; no global mutable state except the thread-local
+ *    error string and a per-device cached SM count.
+ */
+#ifndef GSP_H_
+#define GSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSP_VERSION 1
+
+/* ABI-compatible with cudaStream_t / CUstream. */
+typedef struct CUstream_st *gsp_stream;
+
+typedef enum {
+  GSP_OK = 0,
+  GSP_ERR_INVALID_ARG = 1,     /* null pointer, negative size, ld < width, ... */
+  GSP_ERR_INDEX_RANGE = 2,     /* an edge endpoint outside [0, n)       */
+  GSP_ERR_NEGATIVE_WEIGHT = 3, /* A_ij >= 0 violated                   */
+  GSP_ERR_NONFINITE = 4,       /* NaN / Inf weight or (validate mode) logit    */
+  GSP_ERR_ALIAS = 5,           /* input and output ranges overlap              */
+  GSP_ERR_WORKSPACE = 6,       /* workspace missing or too small               */
+  GSP_ERR_UNSUPPORTED = 7,     /* size beyond the supported range              */
+  GSP_ERR_CUDA = 8             /* CUDA launch / runtime error                  */
+} gsp_status;
+
+typedef enum { GSP_I32 = 0, GSP_I64 = 1 } gsp_index_type;
+
+/* flags for gsp_coo_to_csr */
+enum { GSP_UNDIRECTED = 1u };
+
+/*
+ * Borrowed view of a CSR matrix in device memory ("CogDL utilizes
+ * CSR-format design").  Rows are sorted; within a row, columns are strictly
+ * increasing (canonical form produced by gsp_coo_to_csr).
+ *   n_rows   rows; n_cols columns (= n for a whole graph; for a slice made by
+ *            gsp_csr_slice, the padded all-gathered row count P * rows_padded)
+ *   nnz      stored entries; row_ptr[n_rows] == nnz
+ *   row_ptr  int64 [n_rows + 1], row_ptr[0] == 0, nondecreasing
+ *   col_idx  int32 [nnz], each < n_cols
+ *   val      fp32 [nnz], or NULL meaning every weight is 1.0 (psi = copy)
+ * n_rows, n_cols < 2^31.
+ */
+typedef struct {
+  int64_t n_rows, n_cols, nnz;
+  const int64_t *row_ptr;
+  const int32_t *col_idx;
+  const float *val;
+} gsp_csr;
+
+/* ---------------------------------------------------------------------------
+ * a1. COO -> canonical CSR of A~ = A + fill * I.
+ * P:625-632 (§4 Graph Notations: A binary or weighted, A_ij >= 0, directed or
+ * undirected), P:244 (Eq. gcn_layer, A~ = A + I_n), P:646 (CSR design),
+ * P:1707 (Graph(edge_index=...)).  Readings A2, A4, A5, A6.
+ *
+ * Input pair i is (src[i], dst[i]) with weight w[i] (w NULL => 1.0); it is
+ * stored at row src[i], column dst[i] (A1).  With GSP_UNDIRECTED, (dst, src)
+ * is also stored when src != dst.  If fill != 0, (u, u, fill) is added for
+ * every u.  Duplicates (including an input self-loop plus the fill) are
+ * coalesced by summing their weights in input order in fp64 and rounding once
+ * to fp32; explicit zero weights stay in the structure.
+ *
+ *   n, m          nodes, input pairs (m >= 0, n >= 0, n < 2^31,
+ *                 (2m + n) < 2^32)
+ *   src, dst      device int32 or int64 (per `it`) [m]
+ *   w             device fp32 [m] or NULL
+ *   row_ptr       out, device int64 [n + 1]
+ *   col_idx, val  out, device int32 / fp32 [nnz_max] (nnz_max from the query)
+ *   nnz_out       out, HOST int64: number of stored entries
+ *   ws, ws_bytes  device workspace, >= gsp_coo_to_csr_workspace()'s size
+ * Errors: GSP_ERR_INDEX_RANGE, GSP_ERR_NEGATIVE_WEIGHT, GSP_ERR_NONFINITE are
+ * detected on the device; the call synchronises `stream` once (to read
+ * nnz and the validation flags).  On a device-detected error the outputs are
+ * left unspecified (no out-of-bounds writes occur).
+ */
+gsp_status gsp_coo_to_csr_workspace(int64_t n, int64_t m, uint32_t flags, float fill,
+                                    size_t *ws_bytes, int64_t *nnz_max);
+gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, const void *dst,
+                          gsp_index_type it, const float *w, uint32_t flags, float fill,
+                          int64_t *row_ptr, int32_t *col_idx, float *val, int64_t *nnz_out,
+                          void *ws, size_t ws_bytes, gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * a2. Degree and GCN symmetric normalisation A^ = D~^-1/2 A~ D~^-1/2.
+ * P:244 (Eq. gcn_layer: D~_ii = sum_j A~_ij).  Readings A3, A7, A8.
+ *   d_u = sum of row u's weights, fp64, sequential in column order;
+ *   val_out[e] = fp32( w_e / sqrt(d_u * d_v) ) with IEEE round-to-nearest
+ *   double operations (bit-identical to the oracle), 0 when d_u * d_v == 0.
+ *   a->val must be non-NULL (the A~ weights).  val_out may equal a->val
+ *   (in place).  deg_out: device fp64 [n_rows].
+ *   Requires a square matrix (n_rows == n_cols).
+ */
+gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, gsp_stream stream);
+/* deg_out is REQUIRED (it is also the scratch holding d for the second pass). */
+
+/* ---------------------------------------------------------------------------
+ * a3. SpMM  Y = A X  (GSpMM, phi = sum, psi = multiply).
+ * P:640-645 (§4.1 Eq. formula:1; "SpMM operator H^(l+1) <- A H^(l)"),
+ * P:646-648 (kernel design: CSR, coalesced feature access, cached indices).
+ *   x  device fp32 [a->n_cols][ldx], columns [0, f) used
+ *   y  device fp32 [a->n_rows][ldy], columns [0, f) written
+ *   f >= 0, ldx >= f, ldy >= f.  x and y must not overlap (GSP_ERR_ALIAS).
+ * fp32 multiply-add; error bound per element in DESIGN.md §Summation order
+ * (|y - y_exact| <= ~100 u * sum_j |a_ij x_jk| for rows up to 1.5M entries).
+ */
+gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
+                    int64_t ldy, gsp_stream stream);
+
+/* Tuning knobs for gsp_spmm_ex (0 = automatic).  Results are bitwise
+ * identical for every setting (the summation order does not depend on them). */
+typedef struct {
+  int32_t slab_cols;   /* columns per slab: 0 = auto (L2-resident slab), else 16..512 */
+  int32_t block_nnz;   /* nonzeros per CTA row block: 0 = auto                          */
+  int32_t reserved[6];
+} gsp_spmm_opts;
+gsp_status gsp_spmm_ex(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
+                       int64_t ldy, const gsp_spmm_opts *opts, gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * a6. Edge-wise softmax per head, max-subtracted.
+ * P:653-656 (§4.1: alpha'_uv = exp(alpha_uv) / sum_{w in N(u)} exp(alpha_uw);
+ * "find the max value ... subtract ... exponent ... reduce ... the sum").
+ * Readings A9, A10, A12.
+ *   logits, alpha  device fp32 [nnz][heads]; alpha may equal logits (in place)
+ *   heads >= 1.  Empty rows emit nothing.  s - max is formed in fp64 before the
+ *   fp32 exponential; the row sum is accumulated in fp64.
+ */
+gsp_status gsp_edge_softmax(const gsp_csr *a, int32_t heads, const float *logits, float *alpha,
+                            gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * a7. Multi-head SpMM: Y[u,h,:] = sum_{e in row u} alpha[e,h] * Z[col_e,h,:].
+ * P:648-649 (§4.1 multi-head SpMM; heads share the sparsity pattern), A14.
+ *   alpha  device fp32 [nnz][heads]
+ *   z      device fp32 [a->n_cols][ldz], viewed as [H][D]; ldz >= heads*d
+ *   y      device fp32 [a->n_rows][ldy]; ldy >= heads*d; must not overlap z
+ */
+gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const float *alpha,
+                              const float *z, int64_t d, int64_t ldz, float *y, int64_t ldy,
+                              gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * a4. GAT attention projection (split form of a^T [z_u || z_v], A13):
+ *   el[u,h] = sum_d a_l[h,d] z[u,h,d],  er[u,h] = sum_d a_r[h,d] z[u,h,d].
+ *   z device fp32 [n][ldz]; a_l, a_r device fp32 [heads][d];
+ *   el, er device fp32 [n][heads].
+ */
+gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, const float *z, int64_t ldz,
+                            const float *a_l, const float *a_r, float *el, float *er,
+                            gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * a5 + a6 + a7 fused.  GAT aggregation (P:253 GAT):
+ *   s[e,h]  = LeakyReLU(el[u,h] + er[v,h]; negative_slope)     e = (u,v), A13
+ *   alpha   = edge softmax of s over row u, per head
+ *   Y[u,h,:] = sum_e alpha[e,h] Z[v,h,:]
+ * Two launches: a per-(row, head) statistics pass (max and sum of exp, kept in
+ * the workspace, never per-edge) and the fused score -> softmax -> aggregate
+ * pass.  Per-edge scores and alpha are never materialised unless alpha_out is
+ * non-NULL.
+ *   el  device fp32 [a->n_rows][heads];  er device fp32 [a->n_cols][heads]
+ *   z   device fp32 [a->n_cols][ldz] ([H][D]);  y device fp32 [a->n_rows][ldy]
+ *   alpha_out  device fp32 [nnz][heads] or NULL
+ *   ws  device workspace >= gsp_gat_workspace(a, heads) bytes
+ * The score is formed in fp64 (el + er, slope multiply, minus the row max) and
+ * rounded once before the fp32 exponential.
+ */
+gsp_status gsp_gat_workspace(const gsp_csr *a, int32_t heads, size_t *ws_bytes);
+gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const float *el, const float *er,
+                             double negative_slope, const float *z, int64_t d, int64_t ldz,
+                             float *y, int64_t ldy, float *alpha_out, void *ws, size_t ws_bytes,
+                             gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU row partition.
+ * gsp_partition_rows: row_bounds[p] = first row r with row_ptr[r] >=
+ *   ceil(p * nnz / parts) for 0 < p < parts; row_bounds[0] = 0,
+ *   row_bounds[parts] = n_rows; 1 <= parts <= 128.  Written to
+ *   row_bounds_dev (DEVICE int64 [parts + 1]) and, when row_bounds_host
+ *   (HOST int64 [parts + 1]) is non-NULL, copied there -- in that case the
+ *   call synchronises `stream`.
+ * gsp_csr_slice: the rows [row_bounds[rank], row_bounds[rank+1]) of `a`, with
+ *   column c (owned by rank q: row_bounds[q] <= c < row_bounds[q+1]) remapped
+ *   to q * rows_padded + (c - row_bounds[q]) -- its row in the buffer produced
+ *   by an equal-count all-gather of per-rank feature shards padded to
+ *   rows_padded rows.  row_bounds is HOST [parts + 1]; rows_padded >= the
+ *   largest part.  Outputs (device): row_ptr_out int64 [rows + 1] (starts at
+ *   0), col_out int32 [slice nnz], val_out fp32 [slice nnz] (NULL to skip;
+ *   ignored when a->val is NULL).
+ */
+gsp_status gsp_partition_rows(const gsp_csr *a, int32_t parts, int64_t *row_bounds_dev,
+                              int64_t *row_bounds_host, gsp_stream stream);
+gsp_status gsp_csr_slice(const gsp_csr *a, const int64_t *row_bounds, int32_t parts, int32_t rank,
+                         int64_t rows_padded, int64_t *row_ptr_out, int32_t *col_out,
+                         float *val_out, gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Misc. */
+const char *gsp_status_string(gsp_status st);
+const char *gsp_last_error_detail(void); /* thread-local; "" when none */
+int gsp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSP_H_ */

@@ -1,0 +1,330 @@
+"""paper_2103_00959_b200 -- B200-native (sm_100a) sparse GNN operators after
+CogDL (arXiv 2103.00959, §4 "Efficiency of CogDL").
+
+This module is the thin Python binding of the C ABI in include/gsp.h: every
+function below has the name of the C entry point it calls and does argument
+marshalling only (torch tensors -> device pointers + sizes + the current
+stream).  Every step of the path runs in libgsp.so's CUDA kernels; there is
+no CPU fallback -- if libgsp.so is missing the call raises.
+
+PyTorch is used for device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsp.so")
+
+GSP_OK = 0
+GSP_UNDIRECTED = 1
+GSP_I32, GSP_I64 = 0, 1
+STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "GSP_ERR_NEGATIVE_WEIGHT",
+          4: "GSP_ERR_NONFINITE", 5: "GSP_ERR_ALIAS", 6: "GSP_ERR_WORKSPACE", 7: "GSP_ERR_UNSUPPORTED",
+          8: "GSP_ERR_CUDA"}
+
+# every symbol include/gsp.h declares
+EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
+           "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
+           "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version")
+
+
+class GspError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+class gsp_csr(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("val", ctypes.c_void_p)]
+
+
+class gsp_spmm_opts(ctypes.Structure):
+    _fields_ = [("slab_cols", ctypes.c_int32), ("block_nnz", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libgsp.so (raises if it has not been built -- never falls back)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2103_00959_b200._build` "
+                               "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, I32, F, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_double
+        CP = ctypes.POINTER(gsp_csr)
+        sig = {
+            "gsp_coo_to_csr_workspace": [I, I, ctypes.c_uint32, F, ctypes.POINTER(ctypes.c_size_t),
+                                         ctypes.POINTER(ctypes.c_int64)],
+            "gsp_coo_to_csr": [I, I, P, P, ctypes.c_int, P, ctypes.c_uint32, F, P, P, P,
+                               ctypes.POINTER(ctypes.c_int64), P, ctypes.c_size_t, P],
+            "gsp_sym_normalize": [CP, P, P, P],
+            "gsp_spmm": [CP, P, I, I, P, I, P],
+            "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
+            "gsp_edge_softmax": [CP, I32, P, P, P],
+            "gsp_multihead_spmm": [CP, I32, P, P, I, I, P, I, P],
+            "gsp_attn_project": [I, I32, I, P, I, P, P, P, P, P],
+            "gsp_gat_workspace": [CP, I32, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_gat_aggregate": [CP, I32, P, P, D, P, I, I, P, I, P, P, ctypes.c_size_t, P],
+            "gsp_partition_rows": [CP, I32, P, P, P],
+            "gsp_csr_slice": [CP, P, I32, I32, I, P, P, P, P],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.gsp_status_string.argtypes = [ctypes.c_int]
+        L.gsp_status_string.restype = ctypes.c_char_p
+        L.gsp_last_error_detail.argtypes = []
+        L.gsp_last_error_detail.restype = ctypes.c_char_p
+        L.gsp_version.argtypes = []
+        L.gsp_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int, fn: str):
+    if st != GSP_OK:
+        raise GspError(st, fn, lib().gsp_last_error_detail().decode())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t: torch.Tensor, dtype, name: str):
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA {dtype} tensor")
+
+
+def _vec(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
+    _need(t, dtype, name)
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _mat(t: torch.Tensor, name: str):
+    """(tensor, ld) of a row-major fp32 matrix with unit column stride."""
+    _need(t, torch.float32, name)
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    ld = t.stride(0) if t.shape[0] > 1 else max(t.shape[1], t.stride(0))
+    return t, ld
+
+
+class CSR:
+    """Device CSR held in torch tensors; .view() is the borrowed gsp_csr."""
+
+    def __init__(self, row_ptr: torch.Tensor, col: torch.Tensor, val: Optional[torch.Tensor], n_cols: int,
+                 deg: Optional[torch.Tensor] = None):
+        self.row_ptr = _vec(row_ptr, torch.int64, "row_ptr")
+        self.col = _vec(col, torch.int32, "col")
+        self.val = None if val is None else _vec(val, torch.float32, "val")
+        self.n_rows = row_ptr.numel() - 1
+        self.n_cols = int(n_cols)
+        self.nnz = col.numel()
+        self.deg = deg
+
+    def view(self) -> gsp_csr:
+        return gsp_csr(self.n_rows, self.n_cols, self.nnz, self.row_ptr.data_ptr(),
+                       self.col.data_ptr() if self.nnz else None,
+                       self.val.data_ptr() if (self.val is not None and self.nnz) else None)
+
+    def with_val(self, val: Optional[torch.Tensor]) -> "CSR":
+        return CSR(self.row_ptr, self.col, val, self.n_cols, self.deg)
+
+
+# ---------------------------------------------------------------------------
+# a1 / a2
+# ---------------------------------------------------------------------------
+
+def gsp_coo_to_csr(n: int, src: torch.Tensor, dst: torch.Tensor, w: Optional[torch.Tensor] = None,
+                   undirected: bool = True, fill: float = 1.0, stream=None) -> CSR:
+    """COO edge list (device int32/int64) -> canonical CSR of A + fill*I (gsp.h a1)."""
+    if src.dtype != dst.dtype or src.dtype not in (torch.int32, torch.int64):
+        raise TypeError("src/dst must both be int32 or int64")
+    _vec(src, src.dtype, "src")
+    _vec(dst, dst.dtype, "dst")
+    if w is not None:
+        _vec(w, torch.float32, "w")
+    m = src.numel()
+    flags = GSP_UNDIRECTED if undirected else 0
+    wsb = ctypes.c_size_t(0)
+    nmax = ctypes.c_int64(0)
+    _check(lib().gsp_coo_to_csr_workspace(n, m, flags, fill, ctypes.byref(wsb), ctypes.byref(nmax)),
+           "gsp_coo_to_csr_workspace")
+    dev = src.device
+    ws = torch.empty(wsb.value + 256, dtype=torch.uint8, device=dev)
+    wsp = (ws.data_ptr() + 255) // 256 * 256
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(nmax.value, 1), dtype=torch.int32, device=dev)
+    val = torch.empty(max(nmax.value, 1), dtype=torch.float32, device=dev)
+    nnz = ctypes.c_int64(0)
+    _check(lib().gsp_coo_to_csr(n, m, _ptr(src), _ptr(dst), GSP_I64 if src.dtype == torch.int64 else GSP_I32,
+                                _ptr(w), flags, fill, _ptr(row_ptr), _ptr(col), _ptr(val), ctypes.byref(nnz),
+                                ctypes.c_void_p(wsp), wsb.value, _stream(stream)), "gsp_coo_to_csr")
+    k = nnz.value
+    del ws
+    return CSR(row_ptr, col[:k], val[:k], n)
+
+
+def gsp_sym_normalize(a: CSR, in_place: bool = False, stream=None) -> CSR:
+    """A^ = D~^-1/2 A~ D~^-1/2 (gsp.h a2).  Returns a CSR sharing the structure,
+    with the normalised values and the fp64 degrees in .deg."""
+    if a.val is None:
+        raise ValueError("gsp_sym_normalize needs A~ values")
+    out = a.val if in_place else torch.empty_like(a.val)
+    deg = torch.empty(max(a.n_rows, 1), dtype=torch.float64, device=a.row_ptr.device)
+    v = a.view()
+    _check(lib().gsp_sym_normalize(ctypes.byref(v), _ptr(out), _ptr(deg), _stream(stream)), "gsp_sym_normalize")
+    return CSR(a.row_ptr, a.col, out, a.n_cols, deg[:a.n_rows])
+
+
+# ---------------------------------------------------------------------------
+# a3
+# ---------------------------------------------------------------------------
+
+def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch.Tensor] = None, stream=None,
+             slab_cols: int = 0, block_nnz: int = 0) -> torch.Tensor:
+    """Y = A X (gsp.h a3).  x: [n_cols, >= f] fp32 (row stride = ld)."""
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    if y is None:
+        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    if slab_cols or block_nnz:
+        o = gsp_spmm_opts(slab_cols, block_nnz)
+        st = lib().gsp_spmm_ex(ctypes.byref(v), _ptr(x), f, ldx, _ptr(y), ldy, ctypes.byref(o), _stream(stream))
+        _check(st, "gsp_spmm_ex")
+    else:
+        _check(lib().gsp_spmm(ctypes.byref(v), _ptr(x), f, ldx, _ptr(y), ldy, _stream(stream)), "gsp_spmm")
+    return y
+
+
+gsp_spmm_ex = gsp_spmm
+
+
+# ---------------------------------------------------------------------------
+# a4 - a7
+# ---------------------------------------------------------------------------
+
+def gsp_edge_softmax(a: CSR, logits: torch.Tensor, heads: int, alpha: Optional[torch.Tensor] = None,
+                     stream=None) -> torch.Tensor:
+    """Row-wise edge softmax per head (gsp.h a6); logits [nnz, heads] (alpha may be logits)."""
+    _vec(logits, torch.float32, "logits")
+    if alpha is None:
+        alpha = torch.empty_like(logits)
+    _vec(alpha, torch.float32, "alpha")
+    v = a.view()
+    _check(lib().gsp_edge_softmax(ctypes.byref(v), heads, _ptr(logits), _ptr(alpha), _stream(stream)),
+           "gsp_edge_softmax")
+    return alpha
+
+
+def gsp_multihead_spmm(a: CSR, alpha: torch.Tensor, z: torch.Tensor, heads: int, d: int,
+                       y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Y[u,h,:] = sum_e alpha[e,h] Z[v,h,:] (gsp.h a7).  z: [n_cols, >= heads*d]."""
+    _vec(alpha, torch.float32, "alpha")
+    z, ldz = _mat(z, "z")
+    if y is None:
+        y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device)
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    _check(lib().gsp_multihead_spmm(ctypes.byref(v), heads, _ptr(alpha), _ptr(z), d, ldz, _ptr(y), ldy,
+                                    _stream(stream)), "gsp_multihead_spmm")
+    return y
+
+
+def gsp_attn_project(z: torch.Tensor, a_l: torch.Tensor, a_r: torch.Tensor, heads: int, d: int,
+                     el: Optional[torch.Tensor] = None, er: Optional[torch.Tensor] = None, stream=None):
+    """(el, er) [n, heads] with el[u,h] = a_l[h] . z[u,h,:] (gsp.h a4)."""
+    z, ldz = _mat(z, "z")
+    n = z.shape[0]
+    _vec(a_l, torch.float32, "a_l")
+    _vec(a_r, torch.float32, "a_r")
+    el = torch.empty((n, heads), dtype=torch.float32, device=z.device) if el is None else el
+    er = torch.empty((n, heads), dtype=torch.float32, device=z.device) if er is None else er
+    _check(lib().gsp_attn_project(n, heads, d, _ptr(z), ldz, _ptr(a_l), _ptr(a_r), _ptr(el), _ptr(er),
+                                  _stream(stream)), "gsp_attn_project")
+    return el, er
+
+
+def gsp_gat_workspace(a: CSR, heads: int) -> int:
+    n = ctypes.c_size_t(0)
+    v = a.view()
+    _check(lib().gsp_gat_workspace(ctypes.byref(v), heads, ctypes.byref(n)), "gsp_gat_workspace")
+    return n.value
+
+
+def gsp_gat_aggregate(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tensor, heads: int, d: int,
+                      negative_slope: float = 0.2, y: Optional[torch.Tensor] = None, alpha_out=None,
+                      ws: Optional[torch.Tensor] = None, stream=None):
+    """Fused LeakyReLU score -> edge softmax -> multi-head SpMM (gsp.h a5+a6+a7).
+    alpha_out: None, True (allocate) or a [nnz, heads] tensor.  Returns y or (y, alpha)."""
+    _vec(el, torch.float32, "el")
+    _vec(er, torch.float32, "er")
+    z, ldz = _mat(z, "z")
+    if y is None:
+        y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device)
+    y, ldy = _mat(y, "y")
+    want = alpha_out is not None
+    if alpha_out is True:
+        alpha_out = torch.empty((a.nnz, heads), dtype=torch.float32, device=z.device)
+    need = gsp_gat_workspace(a, heads)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=z.device)
+    v = a.view()
+    _check(lib().gsp_gat_aggregate(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope), _ptr(z), d,
+                                   ldz, _ptr(y), ldy, _ptr(alpha_out if want else None), _ptr(ws), ws.numel(),
+                                   _stream(stream)), "gsp_gat_aggregate")
+    return (y, alpha_out) if want else y
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU partition
+# ---------------------------------------------------------------------------
+
+def gsp_partition_rows(a: CSR, parts: int, stream=None):
+    """(host list of parts+1 row bounds, device int64 tensor of the same)."""
+    dev = torch.empty(parts + 1, dtype=torch.int64, device=a.row_ptr.device)
+    host = (ctypes.c_int64 * (parts + 1))()
+    v = a.view()
+    _check(lib().gsp_partition_rows(ctypes.byref(v), parts, _ptr(dev), host, _stream(stream)),
+           "gsp_partition_rows")
+    return list(host), dev
+
+
+def gsp_csr_slice(a: CSR, bounds, rank: int, rows_padded: int, stream=None) -> CSR:
+    """Rows of `rank` with columns remapped into the padded all-gather layout."""
+    parts = len(bounds) - 1
+    hb = (ctypes.c_int64 * (parts + 1))(*[int(b) for b in bounds])
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    rp_host = a.row_ptr[[r0, r1]].tolist()
+    k = rp_host[1] - rp_host[0]
+    dev = a.row_ptr.device
+    rp = torch.empty(r1 - r0 + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    val = torch.empty(max(k, 1), dtype=torch.float32, device=dev) if a.val is not None else None
+    v = a.view()
+    _check(lib().gsp_csr_slice(ctypes.byref(v), hb, parts, rank, rows_padded, _ptr(rp), _ptr(col), _ptr(val),
+                               _stream(stream)), "gsp_csr_slice")
+    return CSR(rp, col[:k], None if val is None else val[:k], parts * rows_padded)
+
+
+def version() -> int:
+    return lib().gsp_version()

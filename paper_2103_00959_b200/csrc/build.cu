@@ -1,0 +1,445 @@
+// build.cu -- a1 COO -> canonical CSR of A~ = A + fill*I and a2 degree +
+// symmetric normalisation (§4 Graph Notations, P:244
+// Eq. gcn_layer, P:646 CSR design; readings A1-A8).
+//
+// Build pipeline (all hand-written kernels, one host sync at the end):
+//   1. make_keys   slot t -> 64-bit key row*n + col (EMPTY = n*n for a missing
+//                  reverse of a self-pair / invalid input), value = t.  Slots
+//                  are laid out in the oracle's "pos" order (2i, 2i+1, loops),
+//                  validation flags are OR-ed into a device word.
+//   2. LSD radix   stable 8-bit passes over the bits of n*n: per-tile digit
+//                  histogram, exclusive scan (digit-major), stable scatter
+//                  (warp __match_any_sync ranking).  Stability keeps equal
+//                  (row, col) keys in pos order.
+//   3. coalesce    head flags -> exclusive scan -> per-head fp64 weight sum in
+//                  pos order, one rounding to fp32.
+//   4. row_ptr     gap-filling from the row changes of the sorted heads.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace gsp {
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 8;
+constexpr int64_t kRadixTile = kRadixThreads * kRadixItems;  // 2048 keys per tile
+constexpr int64_t kScanTile = 2048;
+
+enum : uint32_t { kErrRange = 1u, kErrNeg = 2u, kErrNonfinite = 4u };
+
+static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ----------------------------------------------------------------- scan
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan of 2048 uint32 (8 per thread, blocked layout).
+// If `sums` != NULL the tile total goes to sums[blockIdx.x]; if `offs` != NULL
+// offs[blockIdx.x] is added to every output; out == NULL skips the outputs
+// (reduce-only pass).  in may equal out (each thread reads before writing).
+__global__ void __launch_bounds__(256) scan_tile_kernel(const uint32_t *in, uint32_t *out, int64_t L, uint32_t *sums,
+                                                        const uint32_t *offs) {
+  __shared__ uint32_t warp_tot[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)tid * 8;
+  uint32_t v[8];
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = (base + i < L) ? in[base + i] : 0u;
+    tsum += v[i];
+  }
+  uint32_t x = tsum;  // inclusive warp scan of thread sums
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    if (w < warp) wpre += warp_tot[w];
+    total += warp_tot[w];
+  }
+  uint32_t run = wpre + x - tsum + (offs ? offs[blockIdx.x] : 0u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t t = v[i];
+    if (out && base + i < L) out[base + i] = run;
+    run += t;
+  }
+  if (sums && tid == 0) sums[blockIdx.x] = total;
+}
+
+static size_t scan_ws_bytes(int64_t L) {
+  size_t b = 0;
+  while (L > kScanTile) {
+    L = ceil_div(L, kScanTile);
+    b += align256((size_t)L * 4);
+  }
+  return b + 256;
+}
+
+// Exclusive scan of L uint32 (in may equal out); ws from scan_ws_bytes(L).
+static gsp_status scan_exclusive(const uint32_t *in, uint32_t *out, int64_t L, uint8_t *ws, cudaStream_t s) {
+  if (L <= 0) return GSP_OK;
+  const int64_t nt = ceil_div(L, kScanTile);
+  if (nt == 1) {
+    scan_tile_kernel<<<1, 256, 0, s>>>(in, out, L, nullptr, nullptr);
+    return check_launch("scan_tile");
+  }
+  uint32_t *sums = reinterpret_cast<uint32_t *>(ws);
+  uint8_t *rest = ws + align256((size_t)nt * 4);
+  // pass 1: tile totals only; pass 2: scan with the scanned totals as offsets
+  scan_tile_kernel<<<(unsigned)nt, 256, 0, s>>>(in, nullptr, L, sums, nullptr);
+  gsp_status st = check_launch("scan_tile(up)");
+  if (st) return st;
+  st = scan_exclusive(sums, sums, nt, rest, s);
+  if (st) return st;
+  scan_tile_kernel<<<(unsigned)nt, 256, 0, s>>>(in, out, L, nullptr, sums);
+  return check_launch("scan_tile(down)");
+}
+
+// ----------------------------------------------------------------- radix
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint64_t *__restrict__ keys, int64_t N,
+                                                                   int shift, uint32_t *__restrict__ counts,
+                                                                   int64_t ntiles) {
+  __shared__ uint32_t h[256];
+  const int tid = threadIdx.x;
+  h[tid] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    const int64_t k = base + (int64_t)i * kRadixThreads + tid;
+    if (k < N) atomicAdd(&h[(unsigned)(keys[k] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  counts[(int64_t)tid * ntiles + blockIdx.x] = h[tid];
+}
+
+__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
+    const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t N, int shift, const uint32_t *__restrict__ offsets, int64_t ntiles) {
+  __shared__ uint32_t wcnt[8][256];
+  __shared__ uint32_t gbase[256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) wcnt[w][tid] = 0;
+  gbase[tid] = offsets[(int64_t)tid * ntiles + blockIdx.x];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile + (int64_t)warp * (32 * kRadixItems);
+  uint64_t k[kRadixItems];
+  uint32_t v[kRadixItems], rank[kRadixItems];
+  int dig[kRadixItems];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    const bool valid = idx < N;
+    k[i] = valid ? kin[idx] : 0ull;
+    v[i] = valid ? vin[idx] : 0u;
+    const int d = valid ? (int)((k[i] >> shift) & 255u) : 256;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t before = 0;
+    if (valid) before = wcnt[warp][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] += __popc(peers);
+    __syncwarp();
+    rank[i] = before + __popc(peers & lt);
+    dig[i] = d;
+  }
+  __syncthreads();
+  {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t t = wcnt[w][tid];
+      wcnt[w][tid] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kRadixItems; ++i) {
+    if (dig[i] < 256) {
+      const uint32_t pos = gbase[dig[i]] + wcnt[warp][dig[i]] + rank[i];
+      kout[pos] = k[i];
+      vout[pos] = v[i];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- build
+template <typename IT>
+__global__ void make_keys_kernel(int64_t n, int64_t m, const IT *__restrict__ src, const IT *__restrict__ dst,
+                                 const float *__restrict__ w, int und, int with_loops, uint64_t *__restrict__ keys,
+                                 uint32_t *__restrict__ vals, uint32_t *__restrict__ err) {
+  const int64_t mm = und ? 2 * m : m;
+  const int64_t S = mm + (with_loops ? n : 0);
+  const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < S; t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key;
+    if (t < mm) {
+      const int64_t i = und ? (t >> 1) : t;
+      const bool rev = und && (t & 1);
+      const int64_t u = (int64_t)src[i], v = (int64_t)dst[i];
+      uint32_t e = 0;
+      if (u < 0 || u >= n || v < 0 || v >= n) e |= kErrRange;
+      if (w && !rev) {
+        const float wi = w[i];
+        if (!isfinite(wi)) e |= kErrNonfinite;
+        else if (wi < 0.0f) e |= kErrNeg;
+      }
+      if (e) atomicOr(err, e);
+      if (e || (rev && u == v)) key = EMPTY;
+      else key = rev ? (uint64_t)v * n + u : (uint64_t)u * n + v;
+    } else {
+      const uint64_t u = (uint64_t)(t - mm);
+      key = u * n + u;
+    }
+    keys[t] = key;
+    vals[t] = (uint32_t)t;
+  }
+}
+
+__global__ void head_flags_kernel(const uint64_t *__restrict__ keys, int64_t S, uint64_t EMPTY,
+                                  uint32_t *__restrict__ head) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[k];
+    head[k] = (key < EMPTY && (k == 0 || keys[k - 1] != key)) ? 1u : 0u;
+  }
+}
+
+// For every head: fp64 sum of the run's weights in pos order -> fp32; the
+// column; and the row_ptr entries of rows that start here (gap filling).
+__global__ void coalesce_kernel(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ pos, int64_t S,
+                                int64_t n, int64_t m, int und, const float *__restrict__ w, float fill,
+                                const uint32_t *__restrict__ head, const uint32_t *__restrict__ idx,
+                                int64_t *__restrict__ row_ptr, int32_t *__restrict__ col, float *__restrict__ val,
+                                int64_t *__restrict__ nnz_out) {
+  const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
+  const int64_t mm = und ? 2 * m : m;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[k];
+    if (key >= EMPTY) continue;
+    const bool last_valid = (k + 1 == S) || keys[k + 1] >= EMPTY;
+    const int64_t r = (int64_t)(key / (uint64_t)n);
+    if (head[k]) {
+      double s = 0.0;
+      for (int64_t j = k; j < S && keys[j] == key; ++j) {
+        const int64_t p = pos[j];
+        double wj;
+        if (p < mm) {
+          const int64_t i = und ? (p >> 1) : p;
+          wj = w ? (double)w[i] : 1.0;
+        } else {
+          wj = (double)fill;
+        }
+        s = __dadd_rn(s, wj);
+      }
+      const int64_t o = idx[k];
+      col[o] = (int32_t)(key - (uint64_t)r * n);
+      val[o] = __double2float_rn(s);
+      const int64_t prev_r = (k == 0) ? -1 : (int64_t)(keys[k - 1] / (uint64_t)n);
+      for (int64_t rr = prev_r + 1; rr <= r; ++rr) row_ptr[rr] = o;
+    }
+    if (last_valid) {
+      const int64_t total = (int64_t)idx[k] + head[k];
+      for (int64_t rr = r + 1; rr <= n; ++rr) row_ptr[rr] = total;
+      *nnz_out = total;
+    }
+  }
+}
+
+__global__ void fill_i64_kernel(int64_t *p, int64_t count, int64_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+struct BuildLayout {
+  size_t keys_a, keys_b, vals_a, vals_b, counts, head, idx, scan, scalars, total;
+};
+
+static int key_bits(int64_t n) {
+  const unsigned __int128 e = (unsigned __int128)n * (unsigned __int128)n;  // EMPTY
+  int b = 0;
+  while (b < 127 && (((unsigned __int128)1) << b) <= e) ++b;
+  return std::max(b, 1);
+}
+
+static BuildLayout build_layout(int64_t S) {
+  BuildLayout L{};
+  const int64_t ntiles = std::max<int64_t>(1, ceil_div(S, kRadixTile));
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    const size_t o = off;
+    off += align256(std::max<size_t>(b, 1));
+    return o;
+  };
+  L.keys_a = take((size_t)S * 8);
+  L.keys_b = take((size_t)S * 8);
+  L.vals_a = take((size_t)S * 4);
+  L.vals_b = take((size_t)S * 4);
+  L.counts = take((size_t)256 * ntiles * 4);
+  L.head = take((size_t)S * 4);
+  L.idx = take((size_t)S * 4);
+  L.scan = take(std::max(scan_ws_bytes(256 * ntiles), scan_ws_bytes(S)));
+  L.scalars = take(64);
+  L.total = off;
+  return L;
+}
+
+static int64_t slots(int64_t n, int64_t m, uint32_t flags, float fill) {
+  return ((flags & GSP_UNDIRECTED) ? 2 * m : m) + (fill != 0.0f ? n : 0);
+}
+
+// ----------------------------------------------------------------- normalise
+__global__ void degree_kernel(const int64_t *__restrict__ rp, const float *__restrict__ val, int64_t n,
+                              double *__restrict__ deg) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) s = __dadd_rn(s, (double)val[e]);
+    deg[u] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                        const float *val, int64_t n, const double *__restrict__ deg,
+                                                        float *val_out) {
+  const int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= n) return;
+  const int lane = threadIdx.x & 31;
+  const double du = deg[u];
+  for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
+    const double p = __dmul_rn(du, deg[col[e]]);
+    double r = 0.0;
+    if (p != 0.0) r = __ddiv_rn((double)val[e], __dsqrt_rn(p));
+    val_out[e] = __double2float_rn(r);
+  }
+}
+
+}  // namespace gsp
+
+using namespace gsp;
+
+extern "C" gsp_status gsp_coo_to_csr_workspace(int64_t n, int64_t m, uint32_t flags, float fill, size_t *ws_bytes,
+                                               int64_t *nnz_max) {
+  clear_detail();
+  if (n < 0 || m < 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_coo_to_csr_workspace: bad argument");
+  if (n >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "n must be < 2^31");
+  const int64_t S = slots(n, m, flags, fill);
+  if (S >= (int64_t(1) << 32) - 1) return fail(GSP_ERR_UNSUPPORTED, "2m + n must be < 2^32");
+  *ws_bytes = build_layout(S).total;
+  if (nnz_max) *nnz_max = S;
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, const void *dst, gsp_index_type it,
+                                     const float *w, uint32_t flags, float fill, int64_t *row_ptr, int32_t *col_idx,
+                                     float *val, int64_t *nnz_out, void *ws, size_t ws_bytes, gsp_stream stream) {
+  const char *fn = "gsp_coo_to_csr";
+  clear_detail();
+  if (n < 0 || m < 0) return fail(GSP_ERR_INVALID_ARG, "%s: negative size", fn);
+  if (n >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "%s: n must be < 2^31", fn);
+  if (it != GSP_I32 && it != GSP_I64) return fail(GSP_ERR_INVALID_ARG, "%s: bad index type", fn);
+  if (!std::isfinite(fill)) return fail(GSP_ERR_NONFINITE, "%s: fill is not finite", fn);
+  if (fill < 0.0f) return fail(GSP_ERR_NEGATIVE_WEIGHT, "%s: fill < 0", fn);
+  if (!row_ptr || !nnz_out) return fail(GSP_ERR_INVALID_ARG, "%s: row_ptr / nnz_out is NULL", fn);
+  if (m > 0 && (!src || !dst)) return fail(GSP_ERR_INVALID_ARG, "%s: src / dst is NULL", fn);
+  if (m > 0 && n == 0) return fail(GSP_ERR_INDEX_RANGE, "%s: edges on an empty node set", fn);
+  const int und = (flags & GSP_UNDIRECTED) ? 1 : 0;
+  const int64_t S = slots(n, m, flags, fill);
+  if (S >= (int64_t(1) << 32) - 1) return fail(GSP_ERR_UNSUPPORTED, "%s: 2m + n must be < 2^32", fn);
+  if (S > 0 && (!col_idx || !val)) return fail(GSP_ERR_INVALID_ARG, "%s: col_idx / val is NULL", fn);
+  const BuildLayout Lw = build_layout(S);
+  if (!ws || ws_bytes < Lw.total) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, Lw.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255u) return fail(GSP_ERR_WORKSPACE, "%s: ws must be 256-byte aligned", fn);
+  cudaStream_t s = cs(stream);
+  uint8_t *W = reinterpret_cast<uint8_t *>(ws);
+  if (S == 0) {
+    fill_i64_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n + 1, 256), 4096)), 256, 0, s>>>(
+        row_ptr, n + 1, 0);
+    gsp_status st = check_launch("fill_row_ptr");
+    if (!st) *nnz_out = 0;
+    return st;
+  }
+  uint64_t *ka = reinterpret_cast<uint64_t *>(W + Lw.keys_a), *kb = reinterpret_cast<uint64_t *>(W + Lw.keys_b);
+  uint32_t *va = reinterpret_cast<uint32_t *>(W + Lw.vals_a), *vb = reinterpret_cast<uint32_t *>(W + Lw.vals_b);
+  uint32_t *counts = reinterpret_cast<uint32_t *>(W + Lw.counts);
+  uint32_t *head = reinterpret_cast<uint32_t *>(W + Lw.head), *idx = reinterpret_cast<uint32_t *>(W + Lw.idx);
+  uint8_t *scan_ws = W + Lw.scan;
+  uint32_t *d_err = reinterpret_cast<uint32_t *>(W + Lw.scalars);
+  int64_t *d_nnz = reinterpret_cast<int64_t *>(W + Lw.scalars + 8);
+
+  if (cudaMemsetAsync(W + Lw.scalars, 0, 16, s) != cudaSuccess) return check_launch("memset");
+  const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(S, 256), 65535 * 4);
+  if (it == GSP_I32)
+    make_keys_kernel<int32_t><<<gb, 256, 0, s>>>(n, m, (const int32_t *)src, (const int32_t *)dst, w, und,
+                                                 fill != 0.0f, ka, va, d_err);
+  else
+    make_keys_kernel<int64_t><<<gb, 256, 0, s>>>(n, m, (const int64_t *)src, (const int64_t *)dst, w, und,
+                                                 fill != 0.0f, ka, va, d_err);
+  gsp_status st = check_launch("make_keys");
+  if (st) return st;
+
+  // stable LSD radix sort over the bits of EMPTY = n*n
+  const int bits = key_bits(n);
+  const int64_t ntiles = ceil_div(S, kRadixTile);
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_hist_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, S, shift, counts, ntiles);
+    if ((st = check_launch("radix_hist"))) return st;
+    if ((st = scan_exclusive(counts, counts, 256 * ntiles, scan_ws, s))) return st;  // digit-major offsets
+    radix_scatter_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, va, kb, vb, S, shift, counts, ntiles);
+    if ((st = check_launch("radix_scatter"))) return st;
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
+  head_flags_kernel<<<gb, 256, 0, s>>>(ka, S, EMPTY, head);
+  if ((st = check_launch("head_flags"))) return st;
+  if ((st = scan_exclusive(head, idx, S, scan_ws, s))) return st;
+  fill_i64_kernel<<<1, 256, 0, s>>>(row_ptr, 1, 0);  // row_ptr[0] = 0 even if row 0 is empty
+  coalesce_kernel<<<gb, 256, 0, s>>>(ka, va, S, n, m, und, w, fill, head, idx, row_ptr, col_idx, val, d_nnz);
+  if ((st = check_launch("coalesce"))) return st;
+
+  struct {
+    uint32_t err, pad;
+    int64_t nnz;
+  } h{};
+  if (cudaMemcpyAsync(&h, W + Lw.scalars, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return check_launch("sync");
+  if (h.err & kErrRange) return fail(GSP_ERR_INDEX_RANGE, "%s: an endpoint is outside [0, n)", fn);
+  if (h.err & kErrNonfinite) return fail(GSP_ERR_NONFINITE, "%s: non-finite weight", fn);
+  if (h.err & kErrNeg) return fail(GSP_ERR_NEGATIVE_WEIGHT, "%s: negative weight", fn);
+  *nnz_out = h.nnz;
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, gsp_stream stream) {
+  const char *fn = "gsp_sym_normalize";
+  clear_detail();
+  gsp_status st = check_csr(a, true, fn);
+  if (st) return st;
+  if (a->n_rows != a->n_cols) return fail(GSP_ERR_INVALID_ARG, "%s: matrix must be square", fn);
+  if (a->n_rows == 0) return GSP_OK;
+  if (!deg_out) return fail(GSP_ERR_INVALID_ARG, "%s: deg_out is required (fp64 [n_rows])", fn);
+  if (a->nnz > 0 && !val_out) return fail(GSP_ERR_INVALID_ARG, "%s: val_out is NULL", fn);
+  if (val_out && val_out != a->val && overlaps(val_out, (size_t)a->nnz * 4, a->val, (size_t)a->nnz * 4))
+    return fail(GSP_ERR_ALIAS, "%s: val_out partially overlaps val", fn);
+  cudaStream_t s = cs(stream);
+  const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(a->n_rows, 256), 65535 * 4);
+  degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, deg_out);
+  if ((st = check_launch("degree"))) return st;
+  if (a->nnz == 0) return GSP_OK;
+  normalize_kernel<<<(unsigned)ceil_div(a->n_rows, 8), 256, 0, s>>>(a->row_ptr, a->col_idx, a->val, a->n_rows,
+                                                                   deg_out, val_out);
+  return check_launch("normalize");
+}

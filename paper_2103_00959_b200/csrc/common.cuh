@@ -1,0 +1,71 @@
+// common.cuh -- shared host/device helpers of libgsp (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <algorithm>
+
+#include "../../include/gsp.h"
+
+namespace gsp {
+
+// ---------------------------------------------------------------- errors
+void set_detail(const char *fmt, ...);
+void clear_detail();
+gsp_status fail(gsp_status st, const char *fmt, ...);
+
+inline cudaStream_t cs(gsp_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Report the first launch error of the preceding kernel(s).
+gsp_status check_launch(const char *what);
+
+int sm_count();  // cached per device
+
+constexpr int kWarp = 32;
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned8(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+// Byte-range overlap test for alias checks.
+inline bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return abytes && bbytes && a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+gsp_status check_csr(const gsp_csr *a, bool need_val, const char *fn);
+
+// Device-side helpers --------------------------------------------------------
+
+// Warp-cooperative lower_bound: first r in [0, n) with rp[r] >= t, or n.
+// Every lane of the warp must call it; all lanes get the result.
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ rp, int64_t n,
+                                                    int64_t t) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]; probes stay < hi <= n
+  while (hi - lo > 31) {
+    const int64_t span = hi - lo;
+    const int64_t p = lo + (span * (lane + 1)) / 33;  // strictly inside [lo, hi)
+    const bool ge = __ldg(rp + p) >= t;
+    const unsigned b = __ballot_sync(0xffffffffu, ge);
+    if (b) {
+      const int j = __ffs(b) - 1;
+      const int64_t pj = lo + (span * (j + 1)) / 33;
+      const int64_t pjm = (j == 0) ? lo : lo + (span * j) / 33 + 1;
+      hi = pj;
+      lo = pjm;
+    } else {
+      lo = lo + (span * 32) / 33 + 1;
+    }
+  }
+  const int64_t p = lo + lane;
+  const bool ge = (p < hi) ? (__ldg(rp + p) >= t) : true;
+  const unsigned b = __ballot_sync(0xffffffffu, ge);
+  return lo + (__ffs(b) - 1);
+}
+
+}  // namespace gsp

@@ -1,0 +1,152 @@
+// spmm.cu -- gsp_spmm / gsp_spmm_ex / gsp_multihead_spmm (§4.1,
+// Eq. formula:1 P:640-645; multi-head SpMM P:648-649).
+#include "spmm_engine.cuh"
+
+namespace gsp {
+
+static int64_t pow2_floor(int64_t v) {
+  int64_t p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+// L2 bytes we aim to keep one slab of X in (126 MB L2; leave room for the
+// streamed CSR, Y and the next slab).  DESIGN.md §Kernels / slab sizing.
+static constexpr int64_t kL2SlabBudget = 48ll << 20;
+
+gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
+                       int32_t slab_req, int32_t block_req, EngineLaunch *L) {
+  int V = vmax;
+  int64_t SW = 0;
+  if (head_dim > 0) {
+    while (V > 1 && head_dim % V) V /= 2;
+    if (slab_req > 0) {
+      SW = slab_req;
+      if (SW % V || head_dim % SW || SW / V > 32 || (SW / V & (SW / V - 1)))
+        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must divide head_dim %lld and be V*2^k <= 32V", slab_req,
+                    (long long)head_dim);
+    } else {
+      int64_t G = 32;
+      while (G > 1 && (head_dim % (G * V) || G * V > 128)) G /= 2;
+      SW = G * V;
+    }
+  } else {
+    if (slab_req > 0) {
+      SW = slab_req;
+      if (SW % V || SW / V > 32 || (SW / V & (SW / V - 1)))
+        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must be V*2^k with k<=5 (V=%d)", slab_req, V);
+    } else {
+      const int64_t resident = kL2SlabBudget / (4 * (n_cols > 0 ? n_cols : 1));
+      SW = resident >= 32 ? pow2_floor(resident) : 32 * V;
+      SW = std::min<int64_t>(SW, 32 * V);
+      SW = std::max<int64_t>(SW, V);
+      // no slab wider than the (vector-rounded) feature width
+      int64_t fw = ((f + V - 1) / V) * V;
+      while (SW / 2 >= fw && SW / 2 >= V) SW /= 2;
+    }
+  }
+  L->V = V;
+  L->G = (int)(SW / V);
+  L->slab_cols = SW;
+  L->nslab = ceil_div(f, SW);
+  const int64_t NG = kThreads / L->G;
+  int64_t C = block_req > 0 ? block_req : NG * 256;
+  if (block_req <= 0) {
+    // keep >= ~8 CTAs per SM over the whole grid for small graphs
+    const int64_t want = 8ll * sm_count();
+    const int64_t cap = (nnz * L->nslab) / want;
+    if (cap < C) C = std::max<int64_t>(256, cap);
+  }
+  C = std::min<int64_t>(C, (int64_t)kHub * (kMaxHubPerBlock - 1));
+  C = std::max<int64_t>(C, 1);
+  L->block_nnz = C;
+  L->nblk = nnz / C + 1;
+  (void)n_rows;
+  return GSP_OK;
+}
+
+static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                            const gsp_spmm_opts *opts, cudaStream_t s, const char *fn) {
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!y) return fail(GSP_ERR_INVALID_ARG, "%s: y is NULL", fn);
+  if (a->n_cols > 0 && !x) return fail(GSP_ERR_INVALID_ARG, "%s: x is NULL", fn);
+  const size_t xb = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 4 : 0;
+  const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
+  if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+  int vmax = 1;
+  if (ldx % 4 == 0 && aligned16(x)) vmax = 4;
+  else if (ldx % 2 == 0 && aligned8(x)) vmax = 2;
+  EngineLaunch L;
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, opts ? opts->slab_cols : 0,
+                   opts ? opts->block_nnz : 0, &L);
+  if (st) return st;
+  EngineParams p;
+  p.row_ptr = a->row_ptr;
+  p.col = a->col_idx;
+  p.x = x;
+  p.y = y;
+  p.n_rows = a->n_rows;
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.f = f;
+  p.block_nnz = L.block_nnz;
+  p.nblk = L.nblk;
+  p.head_dim = 0;
+  p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  return engine_launch(L, p, WeightVal{a->val}, s);
+}
+
+}  // namespace gsp
+
+using namespace gsp;
+
+extern "C" gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                               gsp_stream stream) {
+  return spmm_impl(a, x, f, ldx, y, ldy, nullptr, cs(stream), "gsp_spmm");
+}
+
+extern "C" gsp_status gsp_spmm_ex(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                                  const gsp_spmm_opts *opts, gsp_stream stream) {
+  return spmm_impl(a, x, f, ldx, y, ldy, opts, cs(stream), "gsp_spmm_ex");
+}
+
+extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const float *alpha, const float *z,
+                                         int64_t d, int64_t ldz, float *y, int64_t ldy, gsp_stream stream) {
+  const char *fn = "gsp_multihead_spmm";
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (heads <= 0 || d < 0) return fail(GSP_ERR_INVALID_ARG, "%s: heads >= 1 and d >= 0 required", fn);
+  const int64_t f = (int64_t)heads * d;
+  if (ldz < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need ldz, ldy >= heads*d", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!y || (a->n_cols > 0 && !z) || (a->nnz > 0 && !alpha))
+    return fail(GSP_ERR_INVALID_ARG, "%s: null pointer", fn);
+  const size_t zb = a->n_cols ? (size_t)((a->n_cols - 1) * ldz + f) * 4 : 0;
+  const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
+  if (overlaps(z, zb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: z and y overlap", fn);
+  int vmax = 1;
+  if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
+  else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
+  EngineLaunch L;
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L);
+  if (st) return st;
+  EngineParams p;
+  p.row_ptr = a->row_ptr;
+  p.col = a->col_idx;
+  p.x = z;
+  p.y = y;
+  p.n_rows = a->n_rows;
+  p.ldx = ldz;
+  p.ldy = ldy;
+  p.f = f;
+  p.block_nnz = L.block_nnz;
+  p.nblk = L.nblk;
+  p.head_dim = d;
+  p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));
+}

@@ -1,0 +1,363 @@
+// spmm_engine.cuh -- the row-gather/reduce engine behind gsp_spmm,
+// gsp_multihead_spmm and gsp_gat_aggregate (§4.1, Eq. formula:1,
+// P:640-648; multi-head P:648-649; edge softmax P:653-656).
+//
+// Mapping (DESIGN.md §Kernels / K-spmm):
+//  * Column SLABS.  The feature width is cut into slabs of SW = G*V columns.
+//    The grid is slab-major (blockIdx = slab * nblk + blk) so at any moment
+//    the resident CTAs gather from ONE slab of X, whose n x SW x 4 B footprint
+//    is sized to stay resident in the 126 MB L2: every gathered row after the
+//    first hit comes from L2 instead of HBM.
+//  * nnz-balanced ROW BLOCKS (merge-path on row starts): CTA blk owns the rows
+//    whose first nonzero lies in [blk*C, (blk+1)*C); its row range is found by
+//    a warp-cooperative 33-ary search of row_ptr.
+//  * A GROUP of G lanes owns one (row, slab); each lane holds V consecutive
+//    columns (float4 when aligned), so one edge = one coalesced G*V*4-byte
+//    row-slab read ("consecutive threads along the feature dimension").
+//  * Column indices and edge weights of a 32-edge SEGMENT are loaded
+//    cooperatively (lane l loads edges l, l+G, ...) and broadcast by shuffle
+//    (the paper caches them in shared memory; registers + SHFL are the
+//    sm_100a equivalent without an smem round trip).  8 gathers per lane are
+//    issued before the 8 FMAs that consume them.
+//  * Hub rows (degree > kHub) are processed by the whole CTA: the row is cut
+//    into kVirt = 16 contiguous segment ranges whose partials are combined by
+//    a fixed pairwise tree in shared memory.
+//
+// Summation order (depends only on the row, never on G, V, SW, C or the
+// partition -> bitwise reproducible and partition-invariant):
+//    seg_k   = fma chain over the k-th run of 32 edges, from 0, in CSR order
+//    row sum = acc2 + acc1 where acc1 sums segments sequentially and is folded
+//              into acc2 every 32 segments            (degree <= kHub)
+//    hub row = pairwise tree over 16 ranges, each range summed as above.
+#pragma once
+
+#include "common.cuh"
+
+namespace gsp {
+
+constexpr int kThreads = 256;      // threads per CTA (8 warps)
+constexpr int kSeg = 32;           // edges per segment
+constexpr int kUnroll = 8;         // gathers in flight per lane
+constexpr int kHub = 512;          // degree above which a row is CTA-cooperative
+constexpr int kVirt = 16;          // virtual ranges of a hub row
+constexpr int kMaxHubPerBlock = 64;
+
+// ----------------------------------------------------------------- vectors
+template <int V>
+struct Vec;
+template <>
+struct Vec<4> {
+  static __device__ __forceinline__ void ld(float (&r)[4], const float *p) {
+    float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+    r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
+  }
+  static __device__ __forceinline__ void st(float *p, const float (&r)[4]) {
+    __stcs(reinterpret_cast<float4 *>(p), make_float4(r[0], r[1], r[2], r[3]));
+  }
+};
+template <>
+struct Vec<2> {
+  static __device__ __forceinline__ void ld(float (&r)[2], const float *p) {
+    float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+    r[0] = t.x; r[1] = t.y;
+  }
+  static __device__ __forceinline__ void st(float *p, const float (&r)[2]) {
+    __stcs(reinterpret_cast<float2 *>(p), make_float2(r[0], r[1]));
+  }
+};
+template <>
+struct Vec<1> {
+  static __device__ __forceinline__ void ld(float (&r)[1], const float *p) { r[0] = __ldg(p); }
+  static __device__ __forceinline__ void st(float *p, const float (&r)[1]) { __stcs(p, r[0]); }
+};
+
+// Store V values of which the first nvalid are real columns.
+template <int V>
+__device__ __forceinline__ void store_cols(float *p, const float (&r)[V], int nvalid, bool vec_ok) {
+  if (nvalid >= V && vec_ok) {
+    Vec<V>::st(p, r);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (i < nvalid) __stcs(p + i, r[i]);
+  }
+}
+
+// ---------------------------------------------------------- weight functors
+// Each functor provides Row row(int64 r, int head) and Row::w(e, c): the
+// weight of CSR entry e (column c) for this group's head.
+
+struct WeightVal {  // SpMM: A's values, or 1.0 when val == NULL (psi = copy)
+  const float *val;
+  struct Row {
+    const float *val;
+    __device__ __forceinline__ float w(int64_t e, int /*c*/) const { return val ? __ldcs(val + e) : 1.0f; }
+  };
+  __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{val}; }
+};
+
+struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
+  const float *alpha;
+  int heads;
+  struct Row {
+    const float *alpha;
+    int heads, h;
+    __device__ __forceinline__ float w(int64_t e, int) const { return __ldcs(alpha + e * heads + h); }
+  };
+  __device__ __forceinline__ Row row(int64_t, int h, bool) const { return Row{alpha, heads, h}; }
+};
+
+struct GatStat {  // per (row, head) softmax statistics
+  double m;       // row max of the score (fp64)
+  float inv_s;    // 1 / sum exp(s - m)
+  float pad;
+};
+
+struct WeightGat {  // fused score -> softmax weight (A13)
+  const float *el, *er;
+  const GatStat *stat;
+  float *alpha_out;
+  double slope;
+  int heads;
+  struct Row {
+    const float *er;
+    float *alpha_out;
+    double el_u, m, slope;
+    float inv_s;
+    int heads, h;
+    __device__ __forceinline__ float w(int64_t e, int c) const {
+      const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
+      const double s = t >= 0.0 ? t : slope * t;
+      const float a = expf((float)(s - m)) * inv_s;
+      if (alpha_out) alpha_out[e * heads + h] = a;
+      return a;
+    }
+  };
+  // first_slab: only the first slab of a head writes alpha_out (each entry once)
+  __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab) const {
+    const GatStat st = stat[r * heads + h];
+    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), st.m, slope, st.inv_s,
+               heads, h};
+  }
+};
+
+// ------------------------------------------------------------------ params
+struct EngineParams {
+  const int64_t *row_ptr;
+  const int32_t *col;
+  const float *x;
+  float *y;
+  int64_t n_rows, ldx, ldy, f;
+  int64_t block_nnz, nblk;
+  int64_t head_dim;  // D for multi-head modes (slabs never straddle heads); 0 = no heads
+  int y_vec_ok;      // y base and ldy allow V-wide stores
+};
+
+// Accumulate segments [s_begin, s_end) of the row starting at `start` with
+// degree d into out[V] (order described at the top of this file).
+template <int V, int G, class Row>
+__device__ __forceinline__ void row_segments(const EngineParams &p, const Row &wr, int64_t start, int64_t d,
+                                             int64_t s_begin, int64_t s_end, const float *__restrict__ xcol,
+                                             bool active, int gl, unsigned gmask, float (&out)[V]) {
+  constexpr int EPL = kSeg / G;  // edges per lane per segment
+  float acc1[V], acc2[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc1[i] = acc2[i] = 0.0f;
+  int n1 = 0;
+  for (int64_t s = s_begin; s < s_end; ++s) {
+    const int64_t e0 = start + s * kSeg;
+    const int cnt = (int)(d - s * kSeg < kSeg ? d - s * kSeg : kSeg);
+    int c[EPL];
+    float w[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const int j = gl + G * i;
+      if (j < cnt) {
+        c[i] = __ldcs(p.col + e0 + j);
+        w[i] = wr.w(e0 + j, c[i]);
+      } else {
+        c[i] = 0;
+        w[i] = 0.0f;
+      }
+    }
+    float acc0[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc0[i] = 0.0f;
+#pragma unroll
+    for (int j0 = 0; j0 < kSeg; j0 += kUnroll) {
+      if (j0 >= cnt) break;
+      float xv[kUnroll][V];
+      float ww[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int j = j0 + u;
+        const int cj = __shfl_sync(gmask, c[j / G], j % G, G);
+        ww[u] = __shfl_sync(gmask, w[j / G], j % G, G);
+        if (j < cnt && active) {
+          Vec<V>::ld(xv[u], xcol + (int64_t)cj * p.ldx);
+        } else {
+#pragma unroll
+          for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (j0 + u < cnt) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc0[i] = fmaf(ww[u], xv[u][i], acc0[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc1[i] += acc0[i];
+    if (++n1 == kSeg) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        acc2[i] += acc1[i];
+        acc1[i] = 0.0f;
+      }
+      n1 = 0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < V; ++i) out[i] = acc2[i] + acc1[i];
+}
+
+template <int V, int G, class W>
+__global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, const W wf) {
+  constexpr int NG = kThreads / G;  // groups per CTA
+  constexpr int SW = G * V;         // slab width (columns)
+  __shared__ int64_t s_rb[2];
+  __shared__ int s_hub[kMaxHubPerBlock];
+  __shared__ int s_nhub, s_next;
+  __shared__ __align__(16) float s_part[kVirt * SW];
+
+  const int64_t blk = blockIdx.x % p.nblk;
+  const int64_t slab = blockIdx.x / p.nblk;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = tid / G, gl = tid % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+
+  if (warp < 2) {
+    const int64_t t = (blk + warp) * p.block_nnz;
+    const int64_t r = warp_lower_bound(p.row_ptr, p.n_rows, t);
+    if (lane == 0) s_rb[warp] = r;
+  }
+  if (tid == 0) {
+    s_nhub = 0;
+    s_next = 0;
+  }
+  __syncthreads();
+  const int64_t rbeg = s_rb[0];
+  const int64_t rend = (blk == p.nblk - 1) ? p.n_rows : s_rb[1];
+
+  // columns of this lane
+  const int64_t col0 = slab * SW + (int64_t)gl * V;
+  const bool active = col0 < p.f;
+  const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
+  const float *xcol = p.x + col0;
+  const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;
+  const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
+
+  // 1. collect hub rows
+  for (int64_t r = rbeg + tid; r < rend; r += kThreads) {
+    const int64_t d = __ldg(p.row_ptr + r + 1) - __ldg(p.row_ptr + r);
+    if (d > kHub) {
+      const int k = atomicAdd(&s_nhub, 1);
+      if (k < kMaxHubPerBlock) s_hub[k] = (int)(r - rbeg);
+    }
+  }
+  __syncthreads();
+  const int nhub = s_nhub;  // <= kMaxHubPerBlock by the host's block_nnz cap
+
+  // 2. hub rows: all groups cooperate; 16 virtual ranges, pairwise tree
+  for (int k = 0; k < nhub; ++k) {
+    const int64_t r = rbeg + s_hub[k];
+    const int64_t start = __ldg(p.row_ptr + r);
+    const int64_t d = __ldg(p.row_ptr + r + 1) - start;
+    const int64_t S = (d + kSeg - 1) / kSeg;
+    const auto wr = wf.row(r, head, first_slab);
+    for (int v = g; v < kVirt; v += NG) {
+      float part[V];
+      row_segments<V, G>(p, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, gl, gmask, part);
+#pragma unroll
+      for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int stride = 1; stride < kVirt; stride <<= 1) {
+      for (int q = tid; q < (kVirt / (2 * stride)) * SW; q += kThreads) {
+        const int v = (q / SW) * 2 * stride, cidx = q % SW;
+        s_part[v * SW + cidx] += s_part[(v + stride) * SW + cidx];
+      }
+      __syncthreads();
+    }
+    if (g == 0 && active) {
+      float out[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) out[i] = s_part[gl * V + i];
+      store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+    }
+    __syncthreads();
+  }
+
+  // 3. remaining rows: dynamic assignment, one group per row
+  for (;;) {
+    int k = 0;
+    if (gl == 0) k = atomicAdd(&s_next, 1);
+    k = __shfl_sync(gmask, k, 0, G);
+    const int64_t r = rbeg + k;
+    if (r >= rend) break;
+    const int64_t start = __ldg(p.row_ptr + r);
+    const int64_t d = __ldg(p.row_ptr + r + 1) - start;
+    if (d > kHub) continue;
+    const auto wr = wf.row(r, head, first_slab);
+    float out[V];
+    row_segments<V, G>(p, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, gl, gmask, out);
+    if (active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+  }
+}
+
+// Host-side plan: vector width V from alignment, group width G from the slab
+// width, row-block size C, and the slab-major grid.
+struct EngineLaunch {
+  int V, G;
+  int64_t slab_cols, nslab, block_nnz, nblk;
+};
+
+gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
+                       int32_t slab_req, int32_t block_req, EngineLaunch *L);
+
+template <int V, int G, class W>
+gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
+  const int64_t grid = L.nslab * L.nblk;
+  if (grid <= 0) return GSP_OK;
+  if (grid >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", (long long)grid);
+  engine_kernel<V, G, W><<<(unsigned)grid, kThreads, 0, s>>>(p, w);
+  return check_launch("engine_kernel");
+}
+
+template <int V, class W>
+gsp_status engine_launch_v(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
+  switch (L.G) {
+    case 1: return engine_launch_vg<V, 1>(L, p, w, s);
+    case 2: return engine_launch_vg<V, 2>(L, p, w, s);
+    case 4: return engine_launch_vg<V, 4>(L, p, w, s);
+    case 8: return engine_launch_vg<V, 8>(L, p, w, s);
+    case 16: return engine_launch_vg<V, 16>(L, p, w, s);
+    case 32: return engine_launch_vg<V, 32>(L, p, w, s);
+  }
+  return fail(GSP_ERR_UNSUPPORTED, "bad group width %d", L.G);
+}
+
+template <class W>
+gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
+  switch (L.V) {
+    case 4: return engine_launch_v<4>(L, p, w, s);
+    case 2: return engine_launch_v<2>(L, p, w, s);
+    case 1: return engine_launch_v<1>(L, p, w, s);
+  }
+  return fail(GSP_ERR_UNSUPPORTED, "bad vector width %d", L.V);
+}
+
+}  // namespace gsp

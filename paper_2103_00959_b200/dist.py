@@ -1,0 +1,114 @@
+"""Multi-GPU SpMM by row partition.
+
+One process per GPU.  Every rank holds the full normalised CSR (built once,
+replicated: normalisation needs remote degrees), owns the contiguous row block
+[b_r, b_r+1) chosen by gsp_partition_rows (balanced by nnz), and keeps the
+feature rows of exactly those nodes -- so Y's shard is the next layer's X
+shard.  Per SpMM the only exchange is an equal-count all-gather of the padded
+X shards (NCCL over NVLink/NVSwitch), after which the local slice (columns
+remapped by gsp_csr_slice into the gathered layout) is multiplied by the
+gathered X with the same kernel as on one GPU.  Because the kernel's
+summation order depends only on the row, the P-GPU result is bitwise equal
+to the 1-GPU result.
+
+Overlap: the feature dimension is split into column chunks; the all-gather of
+chunk c+1 (communication stream) runs while the SpMM of chunk c runs on the
+compute stream.  Each chunk of the shard is stored contiguously
+(chunk-packed) so every all-gather moves one contiguous buffer.
+
+The collective is an abstract `all_gather(out, inp)` so the same driver runs
+over NCCL (GPU) or gloo (CPU tests of the partition / layout logic).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional
+
+import torch
+
+from . import CSR, gsp_csr_slice, gsp_partition_rows, gsp_spmm
+
+
+class GpuOps:
+    """The product's operators (libgsp kernels)."""
+
+    @staticmethod
+    def partition(a, parts):
+        return gsp_partition_rows(a, parts)[0]
+
+    @staticmethod
+    def slice(a, bounds, rank, npad):
+        return gsp_csr_slice(a, bounds, rank, npad)
+
+    @staticmethod
+    def spmm(local, x, f, y):
+        gsp_spmm(local, x, f=f, y=y)
+
+
+def padded_rows(bounds: List[int]) -> int:
+    return max(bounds[p + 1] - bounds[p] for p in range(len(bounds) - 1))
+
+
+def chunk_bounds(f: int, chunks: int, align: int = 4) -> List[int]:
+    """Column chunk edges, multiples of `align` (so float4 paths survive)."""
+    chunks = max(1, min(chunks, (f + align - 1) // align))
+    step = ((f + chunks - 1) // chunks + align - 1) // align * align
+    edges = list(range(0, f, step)) + [f]
+    return edges
+
+
+class RowPartitionedSpMM:
+    """Y_shard = (A X)[rows of this rank] with X exchanged by all-gather."""
+
+    def __init__(self, a: CSR, rank: int, world: int, f: int, chunks: int = 1,
+                 all_gather: Optional[Callable] = None, device=None, ops=GpuOps):
+        self.rank, self.world, self.f, self.ops = rank, world, f, ops
+        self.bounds = [int(b) for b in ops.partition(a, world)]
+        self.npad = padded_rows(self.bounds)
+        self.r0, self.r1 = self.bounds[rank], self.bounds[rank + 1]
+        self.rows = self.r1 - self.r0
+        self.local = ops.slice(a, self.bounds, rank, self.npad)
+        self.cols = chunk_bounds(f, chunks)
+        self.device = torch.device(device) if device is not None else a.row_ptr.device
+        self.all_gather = all_gather or (lambda out, inp: torch.distributed.all_gather_into_tensor(out, inp))
+        # chunk-packed shard and gathered buffers (each chunk contiguous, ld = chunk width)
+        self.shard = [torch.zeros((self.npad, c1 - c0), dtype=torch.float32, device=self.device)
+                      for c0, c1 in zip(self.cols[:-1], self.cols[1:])]
+        self.gathered = [torch.empty((world * self.npad, c1 - c0), dtype=torch.float32, device=self.device)
+                         for c0, c1 in zip(self.cols[:-1], self.cols[1:])]
+        self.comm = torch.cuda.Stream(device=self.device) if self.device.type == "cuda" else None
+
+    def load_shard(self, x_rows: torch.Tensor):
+        """x_rows: [rows, f] features of this rank's nodes."""
+        for k, (c0, c1) in enumerate(zip(self.cols[:-1], self.cols[1:])):
+            self.shard[k][:self.rows].copy_(x_rows[:, c0:c1])
+
+    def exchange(self, k: int):
+        self.all_gather(self.gathered[k], self.shard[k])
+
+    def __call__(self, y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if y is None:
+            y = torch.empty((self.rows, self.f), dtype=torch.float32, device=self.device)
+        nch = len(self.cols) - 1
+        if self.comm is None:  # CPU / synchronous collectives
+            for k in range(nch):
+                self.exchange(k)
+                self._local(k, y)
+            return y
+        main = torch.cuda.current_stream(self.device)
+        self.comm.wait_stream(main)  # shard writes visible to the all-gather
+        events = []
+        with torch.cuda.stream(self.comm):
+            for k in range(nch):
+                self.exchange(k)
+                ev = torch.cuda.Event()
+                ev.record(self.comm)
+                events.append(ev)
+        for k in range(nch):
+            main.wait_event(events[k])
+            self._local(k, y)
+        return y
+
+    def _local(self, k: int, y: torch.Tensor):
+        c0, c1 = self.cols[k], self.cols[k + 1]
+        if self.rows:
+            self.ops.spmm(self.local, self.gathered[k], c1 - c0, y[:, c0:c1])

@@ -1,0 +1,120 @@
+"""C-ABI checks that need no GPU: libgsp.so builds, loads, exports every
+symbol include/gsp.h declares, and host-side validation rejects bad
+arguments before any launch (gsp.h CONVENTIONS / Errors)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2103_00959_b200 as G
+from paper_2103_00959_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gsp.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    _build.build()
+    return G.lib()
+
+
+def declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(gsp_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_lists_all_exports():
+    assert set(declared()) == set(G.EXPORTS)
+
+
+def test_exports(L):
+    nm = subprocess.run(["nm", "-D", "--defined-only", G.LIB_PATH], capture_output=True, text=True).stdout
+    syms = set(re.findall(r" T (gsp_\w+)", nm))
+    for name in declared():
+        assert name in syms, name
+        assert hasattr(L, name)
+
+
+def test_sm100a_cubin(L):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", G.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_strings(L):
+    assert L.gsp_version() == 1
+    assert L.gsp_status_string(0) == b"GSP_OK"
+    assert L.gsp_status_string(5) == b"GSP_ERR_ALIAS"
+
+
+def _csr(n_rows=10, n_cols=10, nnz=20, rp=0x1000, col=0x2000, val=0x3000):
+    return G.gsp_csr(n_rows, n_cols, nnz, rp, col, val)
+
+
+def test_host_validation(L):
+    P = ctypes.c_void_p
+    s = P(0)
+    c = _csr()
+    # NULL csr view
+    assert L.gsp_spmm(None, P(0x10000), 4, 4, P(0x90000), 4, s) == 1
+    # ld < f
+    assert L.gsp_spmm(ctypes.byref(c), P(0x10000), 8, 4, P(0x90000), 8, s) == 1
+    # negative f
+    assert L.gsp_spmm(ctypes.byref(c), P(0x10000), -1, 4, P(0x90000), 4, s) == 1
+    # x / y overlap -> ALIAS (checked before any launch)
+    assert L.gsp_spmm(ctypes.byref(c), P(0x10000), 4, 4, P(0x10010), 4, s) == 5
+    assert b"overlap" in L.gsp_last_error_detail()
+    # n >= 2^31 unsupported
+    big = _csr(n_rows=1 << 31)
+    assert L.gsp_spmm(ctypes.byref(big), P(0x10000), 4, 4, P(0x90000000), 4, s) == 7
+    # multi-head: heads * d > ldz
+    assert L.gsp_multihead_spmm(ctypes.byref(c), 4, P(0x5000), P(0x10000), 8, 16, P(0x90000), 32, s) == 1
+    # softmax heads <= 0
+    assert L.gsp_edge_softmax(ctypes.byref(c), 0, P(0x5000), P(0x5000), s) == 1
+    # gat workspace too small
+    assert L.gsp_gat_aggregate(ctypes.byref(c), 2, P(0x5000), P(0x6000), 0.2, P(0x10000), 4, 8, P(0x90000), 8,
+                               None, P(0xA000), 8, s) == 6
+    # normalize needs values
+    c0 = _csr(val=None)
+    assert L.gsp_sym_normalize(ctypes.byref(c0), P(0x7000), P(0x8000), s) == 1
+    # partition parts out of range
+    assert L.gsp_partition_rows(ctypes.byref(c), 0, P(0x7000), None, s) == 1
+    # slice: bounds must span [0, n)
+    hb = (ctypes.c_int64 * 3)(0, 4, 9)
+    assert L.gsp_csr_slice(ctypes.byref(c), hb, 2, 0, 5, P(0x7000), P(0x8000), None, s) == 1
+
+
+def test_build_workspace_query(L):
+    ws = ctypes.c_size_t(0)
+    nmax = ctypes.c_int64(0)
+    assert L.gsp_coo_to_csr_workspace(100, 1000, 1, 1.0, ctypes.byref(ws), ctypes.byref(nmax)) == 0
+    assert nmax.value == 2 * 1000 + 100 and ws.value > 0
+    assert L.gsp_coo_to_csr_workspace(100, 1000, 0, 0.0, ctypes.byref(ws), ctypes.byref(nmax)) == 0
+    assert nmax.value == 1000
+    assert L.gsp_coo_to_csr_workspace(100, 1 << 31, 1, 1.0, ctypes.byref(ws), ctypes.byref(nmax)) == 7
+    # host-checked build errors (no launch)
+    n = ctypes.c_int64(0)
+    assert L.gsp_coo_to_csr(10, 5, None, None, 1, None, 1, 1.0, ctypes.c_void_p(0x100), ctypes.c_void_p(0x200),
+                            ctypes.c_void_p(0x300), ctypes.byref(n), ctypes.c_void_p(0x400), 10, None) == 1
+    assert L.gsp_coo_to_csr(10, 0, None, None, 1, None, 1, -1.0, ctypes.c_void_p(0x100), ctypes.c_void_p(0x200),
+                            ctypes.c_void_p(0x300), ctypes.byref(n), ctypes.c_void_p(0x400), 10, None) == 3
+    assert L.gsp_coo_to_csr(10, 0, None, None, 1, None, 1, float("nan"), ctypes.c_void_p(0x100),
+                            ctypes.c_void_p(0x200), ctypes.c_void_p(0x300), ctypes.byref(n), ctypes.c_void_p(0x400),
+                            10, None) == 4
+
+
+def test_product_does_not_import_oracle():
+    """The product package never imports, links or calls the oracle."""
+    pkg = os.path.join(ROOT, "paper_2103_00959_b200")
+    pat = re.compile(r"import\s+oracle|from\s+oracle|liboracle|\borc_[a-z]|oracle\.c\b")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not pat.search(txt), f
+    nm = subprocess.run(["nm", "-D", G.LIB_PATH], capture_output=True, text=True).stdout
+    assert "orc_" not in nm

@@ -1,0 +1,326 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle.
+
+Bars:
+  * CSR structure (row_ptr, col) and A~ values: bit-exact.
+  * normalised values and degrees: bit-exact (same IEEE-RN fp64 formula, A8).
+  * Y (SpMM, multi-head, GAT): |y - y_ref| <= 1e-5 * cond + 1e-6 per element,
+    cond = sum_e |a_e x_e| from the oracle (BASELINE.json north_star).
+  * alpha: |a - a_ref| <= 1e-5 * a_ref + 1e-9; non-empty rows sum to 1 +- 1e-5.
+  * el/er: |el - el_ref| <= 1e-5 * sum_d |a z| + 1e-6.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+import paper_2103_00959_b200 as G
+from synth import CONFIGS, chung_lu, erdos_renyi, features, rmat, uniform, weights
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def assert_within(y, yref, cond, rel=1e-5, abs_=1e-6, what=""):
+    y = np.asarray(y, np.float64)
+    err = np.abs(y - yref)
+    bound = rel * cond + abs_
+    bad = ~(err <= bound)
+    if bad.any():
+        i = np.unravel_index(np.argmax(np.where(bad, err / bound, 0)), err.shape)
+        raise AssertionError(f"{what}: {bad.sum()} / {err.size} elements out of bound; worst at {i}: "
+                             f"y={y[i]} ref={yref[i]} err={err[i]:.3e} bound={bound[i]:.3e}")
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def gpu_build(n, src, dst, w=None, undirected=True, fill=1.0, idx=torch.int64):
+    return G.gsp_coo_to_csr(n, dev(np.asarray(src, np.int64), idx), dev(np.asarray(dst, np.int64), idx),
+                            None if w is None else dev(np.asarray(w, np.float32)), undirected, fill)
+
+
+def graphs_small():
+    """Adversarial small graphs: (name, n, src, dst, w, undirected, fill)."""
+    rng = np.random.default_rng(0)
+    out = [("n1-empty", 1, [], [], None, True, 1.0), ("n3-nofill-empty", 3, [], [], None, True, 0.0),
+           ("k2", 2, [0], [1], None, True, 1.0), ("isolated-nofill", 6, [0, 1], [1, 2], None, True, 0.0)]
+    for t in range(6):
+        n = int(rng.integers(2, 80))
+        m = int(rng.integers(0, 4 * n))
+        src = rng.integers(0, n, m)
+        dst = rng.integers(0, n, m)  # duplicates + self-loops in the input
+        w = rng.integers(0, 4, m).astype(np.float32) if t % 2 else None
+        out.append((f"multi{t}", n, src, dst, w, bool(t % 3), 1.0 if t != 4 else 0.0))
+    s, d = erdos_renyi(300, 2000, seed=3)
+    out.append(("er300-weighted", 300, s, d, weights(2000, seed=1), True, 1.0))
+    s, d = chung_lu(4000, 30000, seed=2)
+    out.append(("cl4000", 4000, s, d, None, True, 1.0))
+    s, d = rmat(3000, 25000, seed=4)
+    out.append(("rmat3000", 3000, s, d, None, True, 1.0))
+    # hub rows around the CTA-cooperative threshold and a big star
+    hub_deg = [1, 31, 32, 33, 511, 512, 513, 1024, 5000]
+    src, dst = [], []
+    base = len(hub_deg)
+    for i, dg in enumerate(hub_deg):
+        src += [i] * dg
+        dst += list(range(base, base + dg))
+        base += dg
+    out.append(("hubs", base, src, dst, None, False, 1.0))
+    out.append(("star100k", 100001, [0] * 100000, list(range(1, 100001)), None, True, 1.0))
+    return out
+
+
+SMALL = graphs_small()
+
+
+@pytest.fixture(scope="module")
+def built():
+    """name -> (oracle CSR, gpu CSR, (deg, a64, a32) oracle, gpu normalised CSR)"""
+    res = {}
+    for name, n, s, d, w, und, fill in SMALL:
+        go = orc.build_csr(n, s, d, w, und, fill)
+        gg = gpu_build(n, s, d, w, und, fill)
+        no = orc.sym_norm(go)
+        gn = G.gsp_sym_normalize(gg)
+        res[name] = (go, gg, no, gn)
+    return res
+
+
+# ---------------------------------------------------------------- a1, a2
+
+def test_build_bit_exact(built):
+    for name, (go, gg, _, _) in built.items():
+        assert gg.nnz == go.nnz, name
+        np.testing.assert_array_equal(host(gg.row_ptr), go.row_ptr, err_msg=name)
+        np.testing.assert_array_equal(host(gg.col), go.col, err_msg=name)
+        np.testing.assert_array_equal(host(gg.val).view(np.uint32), go.val.view(np.uint32), err_msg=name)
+
+
+@pytest.mark.parametrize("idx", [torch.int32, torch.int64])
+def test_build_index_types_and_brute_force(idx):
+    import itertools
+    n = 5
+    pairs = list(itertools.combinations(range(n), 2))
+    for mask in range(0, 1 << len(pairs), 7):
+        e = np.array([p for i, p in enumerate(pairs) if mask >> i & 1], np.int64).reshape(-1, 2)
+        go = orc.build_csr(n, e[:, 0], e[:, 1], None, True, 1.0)
+        gg = gpu_build(n, e[:, 0], e[:, 1], None, True, 1.0, idx=idx)
+        np.testing.assert_array_equal(host(gg.row_ptr), go.row_ptr)
+        np.testing.assert_array_equal(host(gg.col), go.col)
+        np.testing.assert_array_equal(host(gg.val), go.val)
+
+
+def test_build_errors():
+    with pytest.raises(G.GspError) as ei:
+        gpu_build(5, [0, 1], [1, 5])
+    assert ei.value.status == 2
+    with pytest.raises(G.GspError) as ei:
+        gpu_build(5, [0, 1], [1, 2], w=[1.0, -1.0])
+    assert ei.value.status == 3
+    with pytest.raises(G.GspError) as ei:
+        gpu_build(5, [0, 1], [1, 2], w=[np.inf, 1.0])
+    assert ei.value.status == 4
+
+
+def test_normalize_bit_exact(built):
+    for name, (go, gg, (deg, a64, a32), gn) in built.items():
+        np.testing.assert_array_equal(host(gn.deg), deg, err_msg=name)
+        np.testing.assert_array_equal(host(gn.val).view(np.uint32), a32.view(np.uint32), err_msg=name)
+
+
+def test_normalize_in_place(built):
+    go, gg, (deg, a64, a32), _ = built["cl4000"]
+    g2 = G.CSR(gg.row_ptr, gg.col, gg.val.clone(), gg.n_cols)
+    gn = G.gsp_sym_normalize(g2, in_place=True)
+    assert gn.val.data_ptr() == g2.val.data_ptr()
+    np.testing.assert_array_equal(host(gn.val), a32)
+
+
+# ---------------------------------------------------------------- a3
+
+FS = [1, 2, 3, 4, 5, 31, 32, 33, 127, 128, 129, 602, 1433]
+
+
+@pytest.mark.parametrize("f", FS)
+def test_spmm_parity(built, f):
+    for name in ("k2", "isolated-nofill", "multi1", "multi4", "er300-weighted", "cl4000", "rmat3000", "hubs"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        n = go.n
+        for ld in sorted({f, (f + 3) // 4 * 4}):
+            x = features(n, f, ld, seed=f)
+            yref, cond = orc.spmm(go.row_ptr, go.col, a64, x, f=f)
+            y = G.gsp_spmm(gn, dev(x), f=f)
+            assert_within(host(y), yref, cond, what=f"{name} f={f} ld={ld}")
+            # psi = copy (val == NULL): unit weights
+            yref1, cond1 = orc.spmm(go.row_ptr, go.col, None, x, f=f)
+            y1 = G.gsp_spmm(gn.with_val(None), dev(x), f=f)
+            assert_within(host(y1), yref1, cond1, what=f"{name} unweighted f={f}")
+
+
+def test_spmm_unaligned_and_strided(built):
+    go, gg, (deg, a64, a32), gn = built["cl4000"]
+    n = go.n
+    f = 37
+    big = features(n, 40, 41, seed=9)  # ld = 41 (odd), base offset 1 float
+    xt = dev(big)[:, 1:1 + f]
+    yref, cond = orc.spmm(go.row_ptr, go.col, a64, big[:, 1:1 + f].copy(), f=f)
+    yfull = torch.full((n, 50), 7.0, device=DEV)
+    y = yfull[:, 3:3 + f]
+    G.gsp_spmm(gn, xt, f=f, y=y)
+    assert_within(host(y), yref, cond, what="unaligned")
+    # padding columns untouched
+    assert torch.all(yfull[:, :3] == 7.0) and torch.all(yfull[:, 3 + f:] == 7.0)
+
+
+def test_spmm_hub_rows_and_star(built):
+    for name in ("hubs", "star100k"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        x = features(go.n, 64, seed=4)
+        yref, cond = orc.spmm(go.row_ptr, go.col, a64, x)
+        assert_within(host(G.gsp_spmm(gn, dev(x))), yref, cond, what=name)
+
+
+def test_spmm_deterministic_and_config_invariant(built):
+    go, gg, _, gn = built["rmat3000"]
+    x = dev(features(go.n, 256, seed=5))
+    y0 = G.gsp_spmm(gn, x)
+    for slab, blk in [(0, 0), (4, 0), (32, 512), (64, 300), (128, 10000), (256, 0)]:
+        y = G.gsp_spmm(gn, x, slab_cols=slab, block_nnz=blk)
+        assert torch.equal(y, y0), (slab, blk)
+
+
+def test_spmm_identity_sqrt_degree_full_c2():
+    cfg = CONFIGS["C2"]
+    s, d = chung_lu(cfg.n, cfg.m, seed=1)
+    gn = G.gsp_sym_normalize(gpu_build(cfg.n, s, d))
+    x = torch.sqrt(gn.deg).float()[:, None].contiguous()
+    y = G.gsp_spmm(gn, x)
+    np.testing.assert_allclose(host(y)[:, 0], np.sqrt(host(gn.deg)), rtol=2e-6)
+
+
+def test_spmm_errors(built):
+    _, _, _, gn = built["cl4000"]
+    x = torch.zeros((gn.n_cols, 8), device=DEV)
+    with pytest.raises(G.GspError) as ei:
+        G.gsp_spmm(gn, x, y=x)
+    assert ei.value.status == 5
+
+
+# ---------------------------------------------------------------- a4 - a7
+
+@pytest.mark.parametrize("H", [1, 2, 3, 4, 8, 16])
+def test_edge_softmax_parity(built, H):
+    for name in ("multi0", "cl4000", "hubs", "star100k"):
+        go, gg, _, _ = built[name]
+        for lo, hi in [(-3, 3), (-1e4, 1e4)]:
+            lg = uniform((go.nnz, H), seed=H, low=lo, high=hi)
+            aref = orc.edge_softmax(go.row_ptr, lg.astype(np.float64), H)
+            a = host(G.gsp_edge_softmax(gg, dev(lg), H))
+            assert np.all(np.isfinite(a))
+            err = np.abs(a - aref)
+            assert np.all(err <= 1e-5 * aref + 1e-9), (name, H, lo, err.max())
+            rows = np.repeat(np.arange(go.n), np.diff(go.row_ptr))
+            sums = np.zeros((go.n, H))
+            np.add.at(sums, rows, a.astype(np.float64))
+            nonempty = np.diff(go.row_ptr) > 0
+            assert np.all(np.abs(sums[nonempty] - 1) <= 1e-5)
+    # in place
+    go, gg, _, _ = built["cl4000"]
+    lg = uniform((go.nnz, H), seed=1)
+    t = dev(lg)
+    G.gsp_edge_softmax(gg, t, H, alpha=t)
+    aref = orc.edge_softmax(go.row_ptr, lg.astype(np.float64), H)
+    assert np.all(np.abs(host(t) - aref) <= 1e-5 * aref + 1e-9)
+
+
+@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 128)])
+def test_attn_project_parity(H, D):
+    n = 5000
+    z = uniform((n, H * D), seed=3)
+    al = uniform((H, D), seed=4)
+    ar = uniform((H, D), seed=5)
+    el_ref, er_ref, elc, erc = orc.attn_project(z, al, ar, H, D)
+    el, er = G.gsp_attn_project(dev(z), dev(al.reshape(-1)), dev(ar.reshape(-1)), H, D)
+    assert_within(host(el), el_ref, elc, what="el")
+    assert_within(host(er), er_ref, erc, what="er")
+
+
+@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16)])
+def test_multihead_spmm_parity(built, H, D):
+    for name in ("multi2", "cl4000", "hubs"):
+        go, gg, _, _ = built[name]
+        z = uniform((go.n, H * D), seed=3)
+        alpha = uniform((go.nnz, H), seed=4, low=0, high=1)
+        yref, cond = orc.multihead_spmm(go.row_ptr, go.col, alpha.astype(np.float64), z, H, D)
+        y = G.gsp_multihead_spmm(gg, dev(alpha), dev(z), H, D)
+        assert_within(host(y), yref, cond, what=f"{name} H={H} D={D}")
+
+
+def _gat_ref(go, el, er, z, H, D, slope):
+    s = orc.gat_scores(go.row_ptr, go.col, el, er, H, slope)
+    a = orc.edge_softmax(go.row_ptr, s, H)
+    y, cond = orc.multihead_spmm(go.row_ptr, go.col, a, z, H, D)
+    return y, cond, a
+
+
+@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16)])
+def test_gat_aggregate_parity(built, H, D):
+    for name in ("multi0", "cl4000", "rmat3000", "hubs"):
+        go, gg, _, _ = built[name]
+        n = go.n
+        z = uniform((n, H * D), seed=3)
+        for lo, hi in [(-3, 3), (-1e4, 1e4)]:
+            el = uniform((n, H), seed=4, low=lo, high=hi)
+            er = uniform((n, H), seed=5, low=lo, high=hi)
+            yref, cond, aref = _gat_ref(go, el, er, z, H, D, 0.2)
+            y, a = G.gsp_gat_aggregate(gg, dev(el), dev(er), dev(z), H, D, 0.2, alpha_out=True)
+            assert_within(host(y), yref, cond, what=f"{name} H={H} D={D} range={hi}")
+            err = np.abs(host(a) - aref)
+            assert np.all(err <= 1e-5 * aref + 1e-9), (name, H, D, err.max())
+
+
+def test_gat_uniform_scores_give_mean(built):
+    go, gg, _, _ = built["cl4000"]
+    H, D = 4, 8
+    z = uniform((go.n, H * D), seed=3)
+    zero = torch.zeros((go.n, H), device=DEV)
+    y = host(G.gsp_gat_aggregate(gg, zero, zero, dev(z), H, D))
+    for u in (0, 5, 77, 1234):
+        nb = go.col[go.row_ptr[u]:go.row_ptr[u + 1]]
+        np.testing.assert_allclose(y[u], z[nb].astype(np.float64).mean(0), rtol=1e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------- multi-GPU partition
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partition_slice_bit_exact_and_invariant(built, P):
+    go, gg, (deg, a64, a32), gn = built["rmat3000"]
+    bref = orc.partition_rows(go.row_ptr, P)
+    b, bdev = G.gsp_partition_rows(gn, P)
+    np.testing.assert_array_equal(np.array(b), bref)
+    np.testing.assert_array_equal(host(bdev), bref)
+    npad = int(np.diff(bref).max())
+    f = 96
+    x = features(go.n, f, seed=8)
+    y_global = host(G.gsp_spmm(gn, dev(x)))
+    xg = np.zeros((P * npad, f), np.float32)
+    for q in range(P):
+        xg[q * npad:q * npad + bref[q + 1] - bref[q]] = x[bref[q]:bref[q + 1]]
+    for r in range(P):
+        rp, co, vo = orc.csr_slice(go.row_ptr, go.col, a32, bref, r, npad)
+        sl = G.gsp_csr_slice(gn, b, r, npad)
+        np.testing.assert_array_equal(host(sl.row_ptr), rp)
+        np.testing.assert_array_equal(host(sl.col), co)
+        np.testing.assert_array_equal(host(sl.val), vo)
+        yl = host(G.gsp_spmm(sl, dev(xg)))
+        # partition invariance: bitwise equal to the single-GPU result
+        np.testing.assert_array_equal(yl, y_global[bref[r]:bref[r + 1]])
