@@ -11,21 +11,24 @@
 //  * nnz-balanced ROW BLOCKS (merge-path on row starts): CTA blk owns the rows
 //    whose first nonzero lies in [blk*C, (blk+1)*C); its row range is found by
 //    a warp-cooperative 33-ary search of row_ptr.
-//  * A GROUP of G lanes owns one (row, slab); each lane holds V consecutive
-//    columns (float4 when aligned), so one edge = one coalesced G*V*4-byte
-//    row-slab read ("consecutive threads along the feature dimension").
-//  * Column indices and edge weights of a 32-edge SEGMENT are loaded
-//    cooperatively (lane l loads edges l, l+G, ...) and broadcast by shuffle
-//    (the paper caches them in shared memory; registers + SHFL are the
-//    sm_100a equivalent without an smem round trip).  8 gathers per lane are
-//    issued before the 8 FMAs that consume them.
+//  * A TEAM (a warp when G >= 8) owns one (row, slab).  It is split into
+//    SPR = T/G sub-groups of G lanes; each lane holds V consecutive columns
+//    (float4 when aligned), so one edge = one coalesced G*V*4-byte row-slab
+//    read ("consecutive threads along the feature dimension"), and the
+//    sub-groups take interleaved edges so a warp keeps 32 gathers in flight
+//    without intra-warp divergence.
+//  * Column indices and edge weights of a 32-edge SEGMENT are loaded once,
+//    coalesced (lane l loads edge l), and broadcast by shuffle (the paper
+//    caches them in shared memory; registers + SHFL are the sm_100a
+//    equivalent without an smem round trip).
 //  * Hub rows (degree > kHub) are processed by the whole CTA: the row is cut
 //    into kVirt = 16 contiguous segment ranges whose partials are combined by
 //    a fixed pairwise tree in shared memory.
 //
 // Summation order (depends only on the row, never on G, V, SW, C or the
 // partition -> bitwise reproducible and partition-invariant):
-//    seg_k   = fma chain over the k-th run of 32 edges, from 0, in CSR order
+//    segment = (r0 + r1) + (r2 + r3), r_k = fma chain over the segment's
+//              edges j = k mod 4 (32-edge segments from the row start)
 //    row sum = acc2 + acc1 where acc1 sums segments sequentially and is folded
 //              into acc2 every 32 segments            (degree <= kHub)
 //    hub row = pairwise tree over 16 ranges, each range summed as above.
@@ -153,13 +156,34 @@ struct EngineParams {
   int y_vec_ok;      // y base and ldy allow V-wide stores
 };
 
-// Accumulate segments [s_begin, s_end) of the row starting at `start` with
-// degree d into out[V] (order described at the top of this file).
+// Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
+// group width G >= 8 (a whole warp per row), else 4G (several rows per warp).
+// The team holds SPR = T/G sub-groups; each sub-group covers the slab's SW
+// columns and processes every SPR-th edge of a segment.
+template <int G>
+struct Team {
+  static constexpr int T = (G >= 8) ? 32 : 4 * G;
+  static constexpr int SPR = T / G;        // sub-groups per team: 1, 2 or 4
+  static constexpr int NACC = 4 / SPR;     // residue accumulators per sub-group
+  static constexpr int EPL = kSeg / T;     // metadata entries per lane per segment
+  static constexpr int EPS = kSeg / SPR;   // edges per sub-group per segment
+  static constexpr int U = EPS < kUnroll ? EPS : kUnroll;
+};
+
+// Accumulate segments [s_begin, s_end) of the row starting at `start` (degree
+// d) into out[V].  Canonical order (independent of G, V, T):
+//   residue chain r_k = fma chain, from 0, over the segment's edges j with
+//                       j % 4 == k, in increasing j
+//   segment sum       = (r_0 + r_1) + (r_2 + r_3)
+//   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
+//   out = acc2 + acc1
+// Every lane of the team ends with the same out[] (all sub-groups combine).
 template <int V, int G, class Row>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &wr, int64_t start, int64_t d,
                                              int64_t s_begin, int64_t s_end, const float *__restrict__ xcol,
-                                             bool active, int gl, unsigned gmask, float (&out)[V]) {
-  constexpr int EPL = kSeg / G;  // edges per lane per segment
+                                             bool active, int tl, int sg, unsigned tmask, float (&out)[V]) {
+  using TM = Team<G>;
+  constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL, EPS = TM::EPS, U = TM::U;
   float acc1[V], acc2[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc1[i] = acc2[i] = 0.0f;
@@ -167,11 +191,12 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &w
   for (int64_t s = s_begin; s < s_end; ++s) {
     const int64_t e0 = start + s * kSeg;
     const int cnt = (int)(d - s * kSeg < kSeg ? d - s * kSeg : kSeg);
+    // cooperative, coalesced metadata load: lane tl holds edges tl + T*i
     int c[EPL];
     float w[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
-      const int j = gl + G * i;
+      const int j = tl + T * i;
       if (j < cnt) {
         c[i] = __ldcs(p.col + e0 + j);
         w[i] = wr.w(e0 + j, c[i]);
@@ -180,19 +205,24 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &w
         w[i] = 0.0f;
       }
     }
-    float acc0[V];
+    float a[NACC][V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc0[i] = 0.0f;
+    for (int q = 0; q < NACC; ++q)
 #pragma unroll
-    for (int j0 = 0; j0 < kSeg; j0 += kUnroll) {
-      if (j0 >= cnt) break;
-      float xv[kUnroll][V];
-      float ww[kUnroll];
+      for (int i = 0; i < V; ++i) a[q][i] = 0.0f;
+    // sub-group sg handles edges j = sg + SPR*t; edge j's metadata sits in
+    // lane j % T at index j / T == (SPR*t) / T (static)
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int j = j0 + u;
-        const int cj = __shfl_sync(gmask, c[j / G], j % G, G);
-        ww[u] = __shfl_sync(gmask, w[j / G], j % G, G);
+    for (int t0 = 0; t0 < EPS; t0 += U) {
+      if (SPR * t0 >= cnt) break;  // team-uniform: every lane of the team shuffles
+      float xv[U][V];
+      float ww[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int j = sg + SPR * t;
+        const int cj = __shfl_sync(tmask, c[(SPR * t) / T], j % T, T);
+        ww[u] = __shfl_sync(tmask, w[(SPR * t) / T], j % T, T);
         if (j < cnt && active) {
           Vec<V>::ld(xv[u], xcol + (int64_t)cj * p.ldx);
         } else {
@@ -201,15 +231,32 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &w
         }
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (j0 + u < cnt) {
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        if (sg + SPR * t < cnt) {
 #pragma unroll
-          for (int i = 0; i < V; ++i) acc0[i] = fmaf(ww[u], xv[u][i], acc0[i]);
+          for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww[u], xv[u][i], a[t % NACC][i]);
         }
       }
     }
+    // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
+    // accumulator k / SPR
+    float seg[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc1[i] += acc0[i];
+    for (int i = 0; i < V; ++i) {
+      if (SPR == 1) {
+        seg[i] = (a[0][i] + a[1 % NACC][i]) + (a[2 % NACC][i] + a[3 % NACC][i]);
+      } else if (SPR == 2) {
+        const float b0 = a[0][i] + __shfl_xor_sync(tmask, a[0][i], G, T);
+        const float b1 = a[NACC - 1][i] + __shfl_xor_sync(tmask, a[NACC - 1][i], G, T);
+        seg[i] = b0 + b1;
+      } else {
+        const float b = a[0][i] + __shfl_xor_sync(tmask, a[0][i], G, T);
+        seg[i] = b + __shfl_xor_sync(tmask, b, 2 * G, T);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc1[i] += seg[i];
     if (++n1 == kSeg) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
@@ -225,7 +272,9 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &w
 
 template <int V, int G, class W>
 __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, const W wf) {
-  constexpr int NG = kThreads / G;  // groups per CTA
+  using TM = Team<G>;
+  constexpr int T = TM::T;
+  constexpr int NT = kThreads / T;  // teams per CTA
   constexpr int SW = G * V;         // slab width (columns)
   __shared__ int64_t s_rb[2];
   __shared__ int s_hub[kMaxHubPerBlock];
@@ -235,8 +284,9 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   const int64_t blk = blockIdx.x % p.nblk;
   const int64_t slab = blockIdx.x / p.nblk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = tid / G, gl = tid % G;
-  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+  const int team = tid / T, tl = tid % T;
+  const int sg = tl / G, gl = tl % G;
+  const unsigned tmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << ((lane / T) * T));
 
   if (warp < 2) {
     const int64_t t = (blk + warp) * p.block_nnz;
@@ -251,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   const int64_t rbeg = s_rb[0];
   const int64_t rend = (blk == p.nblk - 1) ? p.n_rows : s_rb[1];
 
-  // columns of this lane
+  // columns of this lane (identical for every sub-group of a team)
   const int64_t col0 = slab * SW + (int64_t)gl * V;
   const bool active = col0 < p.f;
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
@@ -270,18 +320,21 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   __syncthreads();
   const int nhub = s_nhub;  // <= kMaxHubPerBlock by the host's block_nnz cap
 
-  // 2. hub rows: all groups cooperate; 16 virtual ranges, pairwise tree
+  // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree
   for (int k = 0; k < nhub; ++k) {
     const int64_t r = rbeg + s_hub[k];
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
     const auto wr = wf.row(r, head, first_slab);
-    for (int v = g; v < kVirt; v += NG) {
+    for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G>(p, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, gl, gmask, part);
+      row_segments<V, G>(p, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, tl, sg, tmask,
+                         part);
+      if (sg == 0) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
+        for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -292,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
       }
       __syncthreads();
     }
-    if (g == 0 && active) {
+    if (team == 0 && sg == 0 && active) {
       float out[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) out[i] = s_part[gl * V + i];
@@ -301,11 +354,11 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     __syncthreads();
   }
 
-  // 3. remaining rows: dynamic assignment, one group per row
+  // 3. remaining rows: dynamic assignment, one team per row
   for (;;) {
     int k = 0;
-    if (gl == 0) k = atomicAdd(&s_next, 1);
-    k = __shfl_sync(gmask, k, 0, G);
+    if (tl == 0) k = atomicAdd(&s_next, 1);
+    k = __shfl_sync(tmask, k, 0, T);
     const int64_t r = rbeg + k;
     if (r >= rend) break;
     const int64_t start = __ldg(p.row_ptr + r);
@@ -313,8 +366,8 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     if (d > kHub) continue;
     const auto wr = wf.row(r, head, first_slab);
     float out[V];
-    row_segments<V, G>(p, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, gl, gmask, out);
-    if (active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+    row_segments<V, G>(p, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, out);
+    if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
 }
 
