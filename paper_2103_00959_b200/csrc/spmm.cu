@@ -49,8 +49,8 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
   L->G = (int)(SW / V);
   L->slab_cols = SW;
   L->nslab = ceil_div(f, SW);
-  const int64_t NG = kThreads / L->G;
-  int64_t C = block_req > 0 ? block_req : NG * 256;
+  const int64_t T = L->G >= 8 ? 32 : 4 * L->G;  // team size (see Team<G>)
+  int64_t C = block_req > 0 ? block_req : std::min<int64_t>(8192, (kThreads / T) * 512);
   if (block_req <= 0) {
     // keep >= ~8 CTAs per SM over the whole grid for small graphs
     const int64_t want = 8ll * sm_count();
@@ -97,6 +97,7 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   p.nblk = L.nblk;
   p.head_dim = 0;
   p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  engine_stage(p, L, a->nnz, a->col_idx, a->val);
   return engine_launch(L, p, WeightVal{a->val}, s);
 }
 
@@ -148,5 +149,6 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   p.nblk = L.nblk;
   p.head_dim = d;
   p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  engine_stage(p, L, a->nnz, a->col_idx, nullptr);
   return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));
 }

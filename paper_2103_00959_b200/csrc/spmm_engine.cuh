@@ -44,6 +44,7 @@ constexpr int kUnroll = 8;         // gathers in flight per lane
 constexpr int kHub = 512;          // degree above which a row is CTA-cooperative
 constexpr int kVirt = 16;          // virtual ranges of a hub row
 constexpr int kMaxHubPerBlock = 64;
+constexpr int kStageChunks = 4;   // TMA bulk-copy chunks of the CSR window
 
 // ----------------------------------------------------------------- vectors
 template <int V>
@@ -86,6 +87,22 @@ __device__ __forceinline__ void store_cols(float *p, const float (&r)[V], int nv
   }
 }
 
+// ------------------------------------------------------- staged CSR window
+// Entries [wb, we) of col (and val when staged) live in shared memory, copied
+// by the TMA engine at CTA start (cp.async.bulk, 4 chunks, one mbarrier each);
+// anything outside the window (hub rows reaching past it, misaligned arrays)
+// is read from global memory with streaming loads.
+struct Window {
+  const int32_t *scol;
+  const float *sval;  // NULL when values are not staged
+  int64_t wb, we;
+  __device__ __forceinline__ bool in(int64_t e) const { return e >= wb && e < we; }
+  __device__ __forceinline__ int col(const int32_t *g, int64_t e) const { return in(e) ? scol[e - wb] : __ldcs(g + e); }
+  __device__ __forceinline__ float val(const float *g, int64_t e) const {
+    return (sval && in(e)) ? sval[e - wb] : __ldcs(g + e);
+  }
+};
+
 // ---------------------------------------------------------- weight functors
 // Each functor provides Row row(int64 r, int head) and Row::w(e, c): the
 // weight of CSR entry e (column c) for this group's head.
@@ -94,7 +111,9 @@ struct WeightVal {  // SpMM: A's values, or 1.0 when val == NULL (psi = copy)
   const float *val;
   struct Row {
     const float *val;
-    __device__ __forceinline__ float w(int64_t e, int /*c*/) const { return val ? __ldcs(val + e) : 1.0f; }
+    __device__ __forceinline__ float w(int64_t e, int /*c*/, const Window &win) const {
+      return val ? win.val(val, e) : 1.0f;
+    }
   };
   __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{val}; }
 };
@@ -105,7 +124,7 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   struct Row {
     const float *alpha;
     int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int) const { return __ldcs(alpha + e * heads + h); }
+    __device__ __forceinline__ float w(int64_t e, int, const Window &) const { return __ldcs(alpha + e * heads + h); }
   };
   __device__ __forceinline__ Row row(int64_t, int h, bool) const { return Row{alpha, heads, h}; }
 };
@@ -128,7 +147,7 @@ struct WeightGat {  // fused score -> softmax weight (A13)
     double el_u, m, slope;
     float inv_s;
     int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int c) const {
+    __device__ __forceinline__ float w(int64_t e, int c, const Window &) const {
       const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
       const double s = t >= 0.0 ? t : slope * t;
       const float a = expf((float)(s - m)) * inv_s;
@@ -154,6 +173,10 @@ struct EngineParams {
   int64_t block_nnz, nblk;
   int64_t head_dim;  // D for multi-head modes (slabs never straddle heads); 0 = no heads
   int y_vec_ok;      // y base and ldy allow V-wide stores
+  int64_t nnz;
+  const float *stage_val;  // val array to stage in smem (NULL: none)
+  int stage;               // 1: stage col (and stage_val) in shared memory
+  int win_cap;             // window capacity in entries (multiple of 4)
 };
 
 // Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
@@ -179,9 +202,10 @@ struct Team {
 //   out = acc2 + acc1
 // Every lane of the team ends with the same out[] (all sub-groups combine).
 template <int V, int G, class Row>
-__device__ __forceinline__ void row_segments(const EngineParams &p, const Row &wr, int64_t start, int64_t d,
-                                             int64_t s_begin, int64_t s_end, const float *__restrict__ xcol,
-                                             bool active, int tl, int sg, unsigned tmask, float (&out)[V]) {
+__device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
+                                             int64_t d, int64_t s_begin, int64_t s_end,
+                                             const float *__restrict__ xcol, bool active, int tl, int sg,
+                                             unsigned tmask, float (&out)[V]) {
   using TM = Team<G>;
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL, EPS = TM::EPS, U = TM::U;
   float acc1[V], acc2[V];
@@ -198,8 +222,8 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Row &w
     for (int i = 0; i < EPL; ++i) {
       const int j = tl + T * i;
       if (j < cnt) {
-        c[i] = __ldcs(p.col + e0 + j);
-        w[i] = wr.w(e0 + j, c[i]);
+        c[i] = win.col(p.col, e0 + j);
+        w[i] = wr.w(e0 + j, c[i], win);
       } else {
         c[i] = 0;
         w[i] = 0.0f;
@@ -280,6 +304,9 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   __shared__ int s_hub[kMaxHubPerBlock];
   __shared__ int s_nhub, s_next;
   __shared__ __align__(16) float s_part[kVirt * SW];
+  __shared__ __align__(8) uint64_t s_bar[kStageChunks];
+  __shared__ int64_t s_win[3];  // wb, we, chunk
+  extern __shared__ __align__(16) uint8_t s_dyn[];  // staged col [win_cap] then val [win_cap]
 
   const int64_t blk = blockIdx.x % p.nblk;
   const int64_t slab = blockIdx.x / p.nblk;
@@ -296,10 +323,44 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   if (tid == 0) {
     s_nhub = 0;
     s_next = 0;
+    if (p.stage) {
+#pragma unroll
+      for (int k = 0; k < kStageChunks; ++k) mbar_init(&s_bar[k], 1);
+      fence_mbar_init();
+    }
   }
   __syncthreads();
   const int64_t rbeg = s_rb[0];
   const int64_t rend = (blk == p.nblk - 1) ? p.n_rows : s_rb[1];
+  int32_t *s_col = reinterpret_cast<int32_t *>(s_dyn);
+  float *s_val = reinterpret_cast<float *>(s_dyn + (size_t)p.win_cap * 4);
+
+  // 0. TMA: stage the CSR window [wb, we) -- every non-hub row of this block
+  //    lies inside [row_ptr[rbeg], row_ptr[rbeg] + block_nnz + kHub)
+  if (tid == 0) {
+    int64_t wb = 0, we = 0, ch = 1;
+    if (p.stage && rbeg < rend) {
+      const int64_t s0 = __ldg(p.row_ptr + rbeg);
+      wb = s0 & ~int64_t(3);
+      we = min(min(p.nnz, s0 + p.block_nnz + kHub), wb + (int64_t)p.win_cap) & ~int64_t(3);
+      if (we < wb) we = wb;
+      ch = (((we - wb + kStageChunks - 1) / kStageChunks) + 3) & ~int64_t(3);
+      if (ch == 0) ch = 4;
+      for (int k = 0; k < kStageChunks; ++k) {
+        const int64_t c0 = wb + k * ch, c1 = min(we, c0 + ch);
+        const uint32_t n = c1 > c0 ? (uint32_t)(c1 - c0) : 0u;
+        const uint32_t bytes = n * 4u * (p.stage_val ? 2u : 1u);
+        mbar_arrive_expect_tx(&s_bar[k], bytes);
+        if (n) {
+          bulk_g2s(s_col + (c0 - wb), p.col + c0, n * 4u, &s_bar[k]);
+          if (p.stage_val) bulk_g2s(s_val + (c0 - wb), p.stage_val + c0, n * 4u, &s_bar[k]);
+        }
+      }
+    }
+    s_win[0] = wb;
+    s_win[1] = we;
+    s_win[2] = ch;
+  }
 
   // columns of this lane (identical for every sub-group of a team)
   const int64_t col0 = slab * SW + (int64_t)gl * V;
@@ -319,6 +380,17 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   }
   __syncthreads();
   const int nhub = s_nhub;  // <= kMaxHubPerBlock by the host's block_nnz cap
+  const Window win{s_col, p.stage_val ? s_val : nullptr, s_win[0], s_win[1]};
+  const int64_t wchunk = s_win[2];
+  int ready = 0;  // chunks this thread has seen complete
+  // wait until the window covers [.., e_end) (or all of it)
+  auto ensure = [&](int64_t e_end) {
+    if (!p.stage) return;
+    while (ready < kStageChunks && win.wb + ready * wchunk < min(e_end, win.we)) {
+      mbar_wait(&s_bar[ready], 0);
+      ++ready;
+    }
+  };
 
   // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree
   for (int k = 0; k < nhub; ++k) {
@@ -327,9 +399,10 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
     const auto wr = wf.row(r, head, first_slab);
+    ensure(start + d);
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G>(p, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, tl, sg, tmask,
+      row_segments<V, G>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, tl, sg, tmask,
                          part);
       if (sg == 0) {
 #pragma unroll
@@ -365,10 +438,13 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     if (d > kHub) continue;
     const auto wr = wf.row(r, head, first_slab);
+    ensure(start + d);
     float out[V];
-    row_segments<V, G>(p, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, out);
+    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, out);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
+  // no CTA may exit with bulk copies still writing its shared memory
+  if (tid == 0) ensure(win.we);
 }
 
 // Host-side plan: vector width V from alignment, group width G from the slab
@@ -381,12 +457,24 @@ struct EngineLaunch {
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L);
 
+// Fill the CSR-window staging fields of p: col (and val, if given) are
+// staged through shared memory by TMA when 16-byte aligned.
+inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, const int32_t *col, const float *val) {
+  p.nnz = nnz;
+  p.stage = (nnz > 0 && aligned16(col)) ? 1 : 0;
+  p.stage_val = (p.stage && val && aligned16(val)) ? val : nullptr;
+  p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
+}
+
 template <int V, int G, class W>
 gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   const int64_t grid = L.nslab * L.nblk;
   if (grid <= 0) return GSP_OK;
   if (grid >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", (long long)grid);
-  engine_kernel<V, G, W><<<(unsigned)grid, kThreads, 0, s>>>(p, w);
+  const size_t smem = p.stage ? (size_t)p.win_cap * (p.stage_val ? 8 : 4) : 0;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(engine_kernel<V, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  engine_kernel<V, G, W><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
   return check_launch("engine_kernel");
 }
 
