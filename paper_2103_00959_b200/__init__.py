@@ -18,7 +18,8 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsp.so")
+# GSP_LIB selects a tuning variant of the same library (tools/variants.sh); default: the in-tree build
+LIB_PATH = os.environ.get("GSP_LIB") or os.path.join(_HERE, "libgsp.so")
 
 GSP_OK = 0
 GSP_UNDIRECTED = 1

@@ -40,11 +40,18 @@ namespace gsp {
 
 constexpr int kThreads = 256;      // threads per CTA (8 warps)
 constexpr int kSeg = 32;           // edges per segment
-constexpr int kUnroll = 8;         // gathers in flight per lane
+#ifndef GSP_UNROLL
+#define GSP_UNROLL 8
+#endif
+constexpr int kUnroll = GSP_UNROLL;  // gathers in flight per lane
 constexpr int kHub = 512;          // degree above which a row is CTA-cooperative
 constexpr int kVirt = 16;          // virtual ranges of a hub row
 constexpr int kMaxHubPerBlock = 64;
 constexpr int kStageChunks = 4;   // TMA bulk-copy chunks of the CSR window
+#ifndef GSP_MIN_BLOCKS
+#define GSP_MIN_BLOCKS 3
+#endif
+constexpr int kMinBlocks = GSP_MIN_BLOCKS;  // CTAs per SM the register budget is sized for
 
 // ----------------------------------------------------------------- vectors
 template <int V>
@@ -110,6 +117,7 @@ struct Window {
 struct WeightVal {  // SpMM: A's values, or 1.0 when val == NULL (psi = copy)
   const float *val;
   struct Row {
+    static constexpr bool kComputed = false;
     const float *val;
     __device__ __forceinline__ float w(int64_t e, int /*c*/, const Window &win) const {
       return val ? win.val(val, e) : 1.0f;
@@ -122,6 +130,7 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   const float *alpha;
   int heads;
   struct Row {
+    static constexpr bool kComputed = false;
     const float *alpha;
     int heads, h;
     __device__ __forceinline__ float w(int64_t e, int, const Window &) const { return __ldcs(alpha + e * heads + h); }
@@ -142,6 +151,7 @@ struct WeightGat {  // fused score -> softmax weight (A13)
   double slope;
   int heads;
   struct Row {
+    static constexpr bool kComputed = true;
     const float *er;
     float *alpha_out;
     double el_u, m, slope;
@@ -205,7 +215,7 @@ template <int V, int G, class Row>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const float *__restrict__ xcol, bool active, int tl, int sg,
-                                             unsigned tmask, float (&out)[V]) {
+                                             unsigned tmask, float *s_w, float (&out)[V]) {
   using TM = Team<G>;
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL, EPS = TM::EPS, U = TM::U;
   float acc1[V], acc2[V];
@@ -215,39 +225,44 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
   for (int64_t s = s_begin; s < s_end; ++s) {
     const int64_t e0 = start + s * kSeg;
     const int cnt = (int)(d - s * kSeg < kSeg ? d - s * kSeg : kSeg);
-    // cooperative, coalesced metadata load: lane tl holds edges tl + T*i
-    int c[EPL];
-    float w[EPL];
+    const bool seg_in = win.in(e0) && e0 + cnt <= win.we;  // team-uniform
+    const int64_t rel = e0 - win.wb;
+    if (Row::kComputed) {
+      // weights that need arithmetic (softmax) are made once per edge by the
+      // team, cooperatively, into the team's scratch (no redundancy)
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
-      const int j = tl + T * i;
-      if (j < cnt) {
-        c[i] = win.col(p.col, e0 + j);
-        w[i] = wr.w(e0 + j, c[i], win);
-      } else {
-        c[i] = 0;
-        w[i] = 0.0f;
+      for (int i = 0; i < EPL; ++i) {
+        const int j = tl + T * i;
+        if (j < cnt) {
+          const int c = seg_in ? win.scol[rel + j] : __ldcs(p.col + e0 + j);
+          s_w[j] = wr.w(e0 + j, c, win);
+        }
       }
+      __syncwarp(tmask);
     }
     float a[NACC][V];
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < V; ++i) a[q][i] = 0.0f;
-    // sub-group sg handles edges j = sg + SPR*t; edge j's metadata sits in
-    // lane j % T at index j / T == (SPR*t) / T (static)
+    // sub-group sg handles edges j = sg + SPR*t; metadata comes straight from
+    // the shared-memory window (broadcast LDS within a sub-group)
 #pragma unroll
     for (int t0 = 0; t0 < EPS; t0 += U) {
-      if (SPR * t0 >= cnt) break;  // team-uniform: every lane of the team shuffles
+      if (SPR * t0 >= cnt) break;
       float xv[U][V];
       float ww[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int t = t0 + u;
-        const int j = sg + SPR * t;
-        const int cj = __shfl_sync(tmask, c[(SPR * t) / T], j % T, T);
-        ww[u] = __shfl_sync(tmask, w[(SPR * t) / T], j % T, T);
-        if (j < cnt && active) {
+        const int j = sg + SPR * (t0 + u);
+        const bool ok = j < cnt;
+        int cj = 0;
+        ww[u] = 0.0f;
+        if (ok) {
+          cj = seg_in ? win.scol[rel + j] : __ldcs(p.col + e0 + j);
+          ww[u] = Row::kComputed ? s_w[j] : wr.w(e0 + j, cj, win);
+        }
+        if (ok && active) {
           Vec<V>::ld(xv[u], xcol + (int64_t)cj * p.ldx);
         } else {
 #pragma unroll
@@ -263,6 +278,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
         }
       }
     }
+    if (Row::kComputed) __syncwarp(tmask);  // s_w is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
     float seg[V];
@@ -295,7 +311,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
 }
 
 template <int V, int G, class W>
-__global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, const W wf) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const EngineParams p, const W wf) {
   using TM = Team<G>;
   constexpr int T = TM::T;
   constexpr int NT = kThreads / T;  // teams per CTA
@@ -305,6 +321,7 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
   __shared__ int s_nhub, s_next;
   __shared__ __align__(16) float s_part[kVirt * SW];
   __shared__ __align__(8) uint64_t s_bar[kStageChunks];
+  __shared__ float s_wt[NT][kSeg];  // per-team scratch for computed weights
   __shared__ int64_t s_win[3];  // wb, we, chunk
   extern __shared__ __align__(16) uint8_t s_dyn[];  // staged col [win_cap] then val [win_cap]
 
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
       row_segments<V, G>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, tl, sg, tmask,
-                         part);
+                         s_wt[team], part);
       if (sg == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(kThreads) engine_kernel(const EngineParams p, 
     const auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
     float out[V];
-    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, out);
+    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, s_wt[team], out);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
   // no CTA may exit with bulk copies still writing its shared memory
