@@ -260,6 +260,7 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   p.head_dim = d;
   p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
+  if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   WeightGat w{el, er, stats, alpha_out, negative_slope, heads};
   return engine_launch(L, p, w, s);
 }

@@ -98,7 +98,8 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   p.head_dim = 0;
   p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
-  return engine_launch(L, p, WeightVal{a->val}, s);
+  if ((st = engine_ldxv(p, L, a->n_cols, ldx))) return st;
+  return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
 }
 
 }  // namespace gsp
@@ -150,5 +151,6 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   p.head_dim = d;
   p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
+  if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));
 }

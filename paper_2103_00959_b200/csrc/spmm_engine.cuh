@@ -82,6 +82,20 @@ struct Vec<1> {
   static __device__ __forceinline__ void st(float *p, const float (&r)[1]) { __stcs(p, r[0]); }
 };
 
+template <int V>
+struct VecT;
+template <>
+struct VecT<4> { using T = float4; };
+template <>
+struct VecT<2> { using T = float2; };
+template <>
+struct VecT<1> { using T = float; };
+
+template <int V>
+__device__ __forceinline__ void vld(float (&r)[V], const typename VecT<V>::T *p) {
+  Vec<V>::ld(r, reinterpret_cast<const float *>(p));
+}
+
 // Store V values of which the first nvalid are real columns.
 template <int V>
 __device__ __forceinline__ void store_cols(float *p, const float (&r)[V], int nvalid, bool vec_ok) {
@@ -114,26 +128,35 @@ struct Window {
 // Each functor provides Row row(int64 r, int head) and Row::w(e, c): the
 // weight of CSR entry e (column c) for this group's head.
 
-struct WeightVal {  // SpMM: A's values, or 1.0 when val == NULL (psi = copy)
+// kUnit: every weight is 1 (no weight array); kComputed: the weight needs
+// arithmetic (made once per edge by the team into shared scratch); otherwise
+// the weight is a stored value (staged with the window when possible).
+struct WeightVal {  // SpMM with A's values
   const float *val;
   struct Row {
-    static constexpr bool kComputed = false;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = true;
     const float *val;
-    __device__ __forceinline__ float w(int64_t e, int /*c*/, const Window &win) const {
-      return val ? win.val(val, e) : 1.0f;
-    }
+    __device__ __forceinline__ float w(int64_t e, int /*c*/) const { return __ldcs(val + e); }
   };
   __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{val}; }
+};
+
+struct WeightOne {  // SpMM with val == NULL: psi = copy
+  struct Row {
+    static constexpr bool kUnit = true, kComputed = false, kStagedVal = false;
+    __device__ __forceinline__ float w(int64_t, int) const { return 1.0f; }
+  };
+  __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{}; }
 };
 
 struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   const float *alpha;
   int heads;
   struct Row {
-    static constexpr bool kComputed = false;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false;
     const float *alpha;
     int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int, const Window &) const { return __ldcs(alpha + e * heads + h); }
+    __device__ __forceinline__ float w(int64_t e, int) const { return __ldcs(alpha + e * heads + h); }
   };
   __device__ __forceinline__ Row row(int64_t, int h, bool) const { return Row{alpha, heads, h}; }
 };
@@ -151,13 +174,13 @@ struct WeightGat {  // fused score -> softmax weight (A13)
   double slope;
   int heads;
   struct Row {
-    static constexpr bool kComputed = true;
+    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false;
     const float *er;
     float *alpha_out;
     double el_u, m, slope;
     float inv_s;
     int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int c, const Window &) const {
+    __device__ __forceinline__ float w(int64_t e, int c) const {
       const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
       const double s = t >= 0.0 ? t : slope * t;
       const float a = expf((float)(s - m)) * inv_s;
@@ -180,6 +203,7 @@ struct EngineParams {
   const float *x;
   float *y;
   int64_t n_rows, ldx, ldy, f;
+  uint32_t ldxv;  // ldx / V: row stride of x in V-wide vectors (32-bit gather offsets)
   int64_t block_nnz, nblk;
   int64_t head_dim;  // D for multi-head modes (slabs never straddle heads); 0 = no heads
   int y_vec_ok;      // y base and ldy allow V-wide stores
@@ -211,13 +235,61 @@ struct Team {
 //   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
 //   out = acc2 + acc1
 // Every lane of the team ends with the same out[] (all sub-groups combine).
+// Gather + FMA over one segment whose metadata is in shared memory (sc: 32
+// column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
+template <int V, int G, class Row, bool kFull>
+__device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
+                                           const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
+                                           int sg, float (&a)[Team<G>::NACC][V]) {
+  using TM = Team<G>;
+  constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS, U = TM::U;
+#pragma unroll
+  for (int t0 = 0; t0 < EPS; t0 += U) {
+    if (!kFull && SPR * t0 >= cnt) break;
+    float xv[U][V];
+    float ww[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = sg + SPR * (t0 + u);
+      const bool ok = kFull || j < cnt;
+      const uint32_t cj = ok ? (uint32_t)sc[j] : 0u;
+      ww[u] = Row::kUnit ? 1.0f : (ok ? sw[j] : 0.0f);
+      if (ok && active) {
+        vld<V>(xv[u], xb + cj * ldxv);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u;
+      if (kFull || sg + SPR * t < cnt) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww[u], xv[u][i], a[t % NACC][i]);
+      }
+    }
+  }
+}
+
+// Accumulate segments [s_begin, s_end) of the row starting at `start` (degree
+// d) into out[V].  Canonical order (independent of G, V, T):
+//   residue chain r_k = fma chain, from 0, over the segment's edges j with
+//                       j % 4 == k, in increasing j
+//   segment sum       = (r_0 + r_1) + (r_2 + r_3)
+//   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
+//   out = acc2 + acc1
+// Every lane of the team ends with the same out[] (all sub-groups combine).
+// Metadata: segments inside the TMA-staged window are read from it directly;
+// other segments (hub rows beyond the window, unstaged arrays) and computed
+// weights go through the team's 32-entry shared scratch (tc, tw).
 template <int V, int G, class Row>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
-                                             const float *__restrict__ xcol, bool active, int tl, int sg,
-                                             unsigned tmask, float *s_w, float (&out)[V]) {
+                                             const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
+                                             unsigned tmask, int32_t *tc, float *tw, float (&out)[V]) {
   using TM = Team<G>;
-  constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL, EPS = TM::EPS, U = TM::U;
+  constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL;
   float acc1[V], acc2[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc1[i] = acc2[i] = 0.0f;
@@ -226,16 +298,25 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     const int64_t e0 = start + s * kSeg;
     const int cnt = (int)(d - s * kSeg < kSeg ? d - s * kSeg : kSeg);
     const bool seg_in = win.in(e0) && e0 + cnt <= win.we;  // team-uniform
-    const int64_t rel = e0 - win.wb;
-    if (Row::kComputed) {
-      // weights that need arithmetic (softmax) are made once per edge by the
-      // team, cooperatively, into the team's scratch (no redundancy)
+    const int32_t *sc;
+    const float *sw = tw;
+    bool scratch = false;
+    if (seg_in) {
+      sc = win.scol + (e0 - win.wb);
+      if (Row::kStagedVal && win.sval) sw = win.sval + (e0 - win.wb);
+      else scratch = !Row::kUnit;
+    } else {
+      sc = tc;
+      scratch = true;
+    }
+    if (scratch) {  // cooperative: lane tl makes entries tl + T*i
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         const int j = tl + T * i;
         if (j < cnt) {
-          const int c = seg_in ? win.scol[rel + j] : __ldcs(p.col + e0 + j);
-          s_w[j] = wr.w(e0 + j, c, win);
+          const int c = seg_in ? sc[j] : __ldcs(p.col + e0 + j);
+          if (!seg_in) tc[j] = c;
+          if (!Row::kUnit) tw[j] = wr.w(e0 + j, c);
         }
       }
       __syncwarp(tmask);
@@ -245,40 +326,9 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < V; ++i) a[q][i] = 0.0f;
-    // sub-group sg handles edges j = sg + SPR*t; metadata comes straight from
-    // the shared-memory window (broadcast LDS within a sub-group)
-#pragma unroll
-    for (int t0 = 0; t0 < EPS; t0 += U) {
-      if (SPR * t0 >= cnt) break;
-      float xv[U][V];
-      float ww[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = sg + SPR * (t0 + u);
-        const bool ok = j < cnt;
-        int cj = 0;
-        ww[u] = 0.0f;
-        if (ok) {
-          cj = seg_in ? win.scol[rel + j] : __ldcs(p.col + e0 + j);
-          ww[u] = Row::kComputed ? s_w[j] : wr.w(e0 + j, cj, win);
-        }
-        if (ok && active) {
-          Vec<V>::ld(xv[u], xcol + (int64_t)cj * p.ldx);
-        } else {
-#pragma unroll
-          for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u;
-        if (sg + SPR * t < cnt) {
-#pragma unroll
-          for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww[u], xv[u][i], a[t % NACC][i]);
-        }
-      }
-    }
-    if (Row::kComputed) __syncwarp(tmask);  // s_w is rewritten by the next segment
+    if (cnt == kSeg) seg_gather<V, G, Row, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a);
+    else seg_gather<V, G, Row, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a);
+    if (scratch) __syncwarp(tmask);  // scratch is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
     float seg[V];
@@ -321,7 +371,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   __shared__ int s_nhub, s_next;
   __shared__ __align__(16) float s_part[kVirt * SW];
   __shared__ __align__(8) uint64_t s_bar[kStageChunks];
-  __shared__ float s_wt[NT][kSeg];  // per-team scratch for computed weights
+  __shared__ float s_tw[NT][kSeg];    // per-team scratch: weights
+  __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
   __shared__ int64_t s_win[3];  // wb, we, chunk
   extern __shared__ __align__(16) uint8_t s_dyn[];  // staged col [win_cap] then val [win_cap]
 
@@ -383,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   const int64_t col0 = slab * SW + (int64_t)gl * V;
   const bool active = col0 < p.f;
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
-  const float *xcol = p.x + col0;
+  const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
 
@@ -419,8 +470,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     ensure(start + d);
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xcol, active, tl, sg, tmask,
-                         s_wt[team], part);
+      row_segments<V, G>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
+                         s_tc[team], s_tw[team], part);
       if (sg == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
@@ -457,7 +508,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
     float out[V];
-    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xcol, active, tl, sg, tmask, s_wt[team], out);
+    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
+                       s_tw[team], out);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
   // no CTA may exit with bulk copies still writing its shared memory
@@ -473,6 +525,15 @@ struct EngineLaunch {
 
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L);
+
+// 32-bit gather offsets: row c of x starts at vector c * ldxv.
+inline gsp_status engine_ldxv(EngineParams &p, const EngineLaunch &L, int64_t n_cols, int64_t ldx) {
+  const int64_t ldxv = ldx / L.V;
+  if (n_cols > 0 && (n_cols - 1) * ldxv + ldxv >= (int64_t(1) << 32))
+    return fail(GSP_ERR_UNSUPPORTED, "feature matrix too large for 32-bit vector offsets");
+  p.ldxv = (uint32_t)ldxv;
+  return GSP_OK;
+}
 
 // Fill the CSR-window staging fields of p: col (and val, if given) are
 // staged through shared memory by TMA when 16-byte aligned.
