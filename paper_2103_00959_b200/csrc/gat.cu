@@ -258,7 +258,7 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   p.block_nnz = L.block_nnz;
   p.nblk = L.nblk;
   p.head_dim = d;
-  p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   WeightGat w{el, er, stats, alpha_out, negative_slope, heads};

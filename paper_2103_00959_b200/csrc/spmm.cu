@@ -33,13 +33,17 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
   } else {
     if (slab_req > 0) {
       SW = slab_req;
-      if (SW % V || SW / V > 32 || (SW / V & (SW / V - 1)))
-        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must be V*2^k with k<=5 (V=%d)", slab_req, V);
+      if (SW == 256 && V == 4) {
+        V = 8;  // two float4 per lane
+      } else if (SW % V || SW / V > 32 || (SW / V & (SW / V - 1))) {
+        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must be V*2^k with k<=5 (V=%d) or 256", slab_req, V);
+      }
     } else {
-      const int64_t resident = kL2SlabBudget / (4 * (n_cols > 0 ? n_cols : 1));
-      SW = resident >= 32 ? pow2_floor(resident) : 32 * V;
-      SW = std::min<int64_t>(SW, 32 * V);
-      SW = std::max<int64_t>(SW, V);
+      // widest single-float4-per-lane slab (measured best on C4, DESIGN.md
+      // §Slab sizing); the L2-resident width is kept for reference
+      (void)kL2SlabBudget;
+      (void)pow2_floor;
+      SW = 32 * V;
       // no slab wider than the (vector-rounded) feature width
       int64_t fw = ((f + V - 1) / V) * V;
       while (SW / 2 >= fw && SW / 2 >= V) SW /= 2;
@@ -96,7 +100,7 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   p.block_nnz = L.block_nnz;
   p.nblk = L.nblk;
   p.head_dim = 0;
-  p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
   if ((st = engine_ldxv(p, L, a->n_cols, ldx))) return st;
   return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
@@ -149,7 +153,7 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   p.block_nnz = L.block_nnz;
   p.nblk = L.nblk;
   p.head_dim = d;
-  p.y_vec_ok = (ldy % L.V == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * L.V)) == 0);
+  p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));

@@ -29,9 +29,9 @@
 // partition -> bitwise reproducible and partition-invariant):
 //    segment = (r0 + r1) + (r2 + r3), r_k = fma chain over the segment's
 //              edges j = k mod 4 (32-edge segments from the row start)
-//    row sum = acc2 + acc1 where acc1 sums segments sequentially and is folded
-//              into acc2 every 32 segments            (degree <= kHub)
-//    hub row = pairwise tree over 16 ranges, each range summed as above.
+//    row sum = sequential sum of its segments           (degree <= kHub)
+//    hub row = pairwise tree over 16 ranges; a range sums its segments into
+//              acc1, folded into acc2 every 32 segments.
 #pragma once
 
 #include "common.cuh"
@@ -49,7 +49,7 @@ constexpr int kVirt = 16;          // virtual ranges of a hub row
 constexpr int kMaxHubPerBlock = 64;
 constexpr int kStageChunks = 4;   // TMA bulk-copy chunks of the CSR window
 #ifndef GSP_MIN_BLOCKS
-#define GSP_MIN_BLOCKS 3
+#define GSP_MIN_BLOCKS 4
 #endif
 constexpr int kMinBlocks = GSP_MIN_BLOCKS;  // CTAs per SM the register budget is sized for
 
@@ -64,6 +64,19 @@ struct Vec<4> {
   }
   static __device__ __forceinline__ void st(float *p, const float (&r)[4]) {
     __stcs(reinterpret_cast<float4 *>(p), make_float4(r[0], r[1], r[2], r[3]));
+  }
+};
+template <>
+struct Vec<8> {  // two float4 per lane (256-column slabs)
+  static __device__ __forceinline__ void ld(float (&r)[8], const float *p) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+    r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+  }
+  static __device__ __forceinline__ void st(float *p, const float (&r)[8]) {
+    __stcs(reinterpret_cast<float4 *>(p), make_float4(r[0], r[1], r[2], r[3]));
+    __stcs(reinterpret_cast<float4 *>(p) + 1, make_float4(r[4], r[5], r[6], r[7]));
   }
 };
 template <>
@@ -84,6 +97,8 @@ struct Vec<1> {
 
 template <int V>
 struct VecT;
+template <>
+struct VecT<8> { using T = float4; };  // addressed in float4 units (ldxv = ldx / 4)
 template <>
 struct VecT<4> { using T = float4; };
 template <>
@@ -226,6 +241,10 @@ struct Team {
   static constexpr int EPS = kSeg / SPR;   // edges per sub-group per segment
   static constexpr int U = EPS < kUnroll ? EPS : kUnroll;
 };
+template <int V>
+struct UnrollFor {  // gathers in flight per lane, capped by register budget
+  static constexpr int U = V >= 8 ? (kUnroll < 4 ? kUnroll : 4) : kUnroll;
+};
 
 // Accumulate segments [s_begin, s_end) of the row starting at `start` (degree
 // d) into out[V].  Canonical order (independent of G, V, T):
@@ -233,7 +252,8 @@ struct Team {
 //                       j % 4 == k, in increasing j
 //   segment sum       = (r_0 + r_1) + (r_2 + r_3)
 //   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
-//   out = acc2 + acc1
+//   out = acc2 + acc1 (kLong: hub ranges) or acc1 (rows of <= kHub edges,
+//   i.e. <= 16 segments, where acc2 would stay 0)
 // Every lane of the team ends with the same out[] (all sub-groups combine).
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
@@ -242,7 +262,8 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
                                            const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
                                            int sg, float (&a)[Team<G>::NACC][V]) {
   using TM = Team<G>;
-  constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS, U = TM::U;
+  constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
+  constexpr int U = TM::U < UnrollFor<V>::U ? TM::U : UnrollFor<V>::U;
 #pragma unroll
   for (int t0 = 0; t0 < EPS; t0 += U) {
     if (!kFull && SPR * t0 >= cnt) break;
@@ -278,12 +299,13 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 //                       j % 4 == k, in increasing j
 //   segment sum       = (r_0 + r_1) + (r_2 + r_3)
 //   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
-//   out = acc2 + acc1
+//   out = acc2 + acc1 (kLong: hub ranges) or acc1 (rows of <= kHub edges,
+//   i.e. <= 16 segments, where acc2 would stay 0)
 // Every lane of the team ends with the same out[] (all sub-groups combine).
 // Metadata: segments inside the TMA-staged window are read from it directly;
 // other segments (hub rows beyond the window, unstaged arrays) and computed
 // weights go through the team's 32-entry shared scratch (tc, tw).
-template <int V, int G, class Row>
+template <int V, int G, bool kLong, class Row>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
@@ -347,7 +369,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     }
 #pragma unroll
     for (int i = 0; i < V; ++i) acc1[i] += seg[i];
-    if (++n1 == kSeg) {
+    if (kLong && ++n1 == kSeg) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         acc2[i] += acc1[i];
@@ -357,7 +379,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     }
   }
 #pragma unroll
-  for (int i = 0; i < V; ++i) out[i] = acc2[i] + acc1[i];
+  for (int i = 0; i < V; ++i) out[i] = kLong ? acc2[i] + acc1[i] : acc1[i];
 }
 
 template <int V, int G, class W>
@@ -470,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     ensure(start + d);
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
+      row_segments<V, G, true>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
                          s_tc[team], s_tw[team], part);
       if (sg == 0) {
 #pragma unroll
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
     float out[V];
-    row_segments<V, G>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
+    row_segments<V, G, false>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
                        s_tw[team], out);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
@@ -526,9 +548,15 @@ struct EngineLaunch {
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L);
 
+// y may take the V-wide (at most float4) stores
+inline int engine_y_vec_ok(const EngineLaunch &L, const float *y, int64_t ldy) {
+  const int vw = L.V == 8 ? 4 : L.V;
+  return (ldy % vw == 0) && ((reinterpret_cast<uintptr_t>(y) % (4 * vw)) == 0);
+}
+
 // 32-bit gather offsets: row c of x starts at vector c * ldxv.
 inline gsp_status engine_ldxv(EngineParams &p, const EngineLaunch &L, int64_t n_cols, int64_t ldx) {
-  const int64_t ldxv = ldx / L.V;
+  const int64_t ldxv = ldx / (L.V == 8 ? 4 : L.V);
   if (n_cols > 0 && (n_cols - 1) * ldxv + ldxv >= (int64_t(1) << 32))
     return fail(GSP_ERR_UNSUPPORTED, "feature matrix too large for 32-bit vector offsets");
   p.ldxv = (uint32_t)ldxv;
@@ -572,6 +600,7 @@ gsp_status engine_launch_v(const EngineLaunch &L, const EngineParams &p, const W
 template <class W>
 gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   switch (L.V) {
+    case 8: return engine_launch_vg<8, 32>(L, p, w, s);
     case 4: return engine_launch_v<4>(L, p, w, s);
     case 2: return engine_launch_v<2>(L, p, w, s);
     case 1: return engine_launch_v<1>(L, p, w, s);
