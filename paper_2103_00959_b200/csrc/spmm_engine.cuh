@@ -578,8 +578,17 @@ gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const 
   if (grid <= 0) return GSP_OK;
   if (grid >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", (long long)grid);
   const size_t smem = p.stage ? (size_t)p.win_cap * (p.stage_val ? 8 : 4) : 0;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(engine_kernel<V, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 0) {  // static + dynamic may exceed the 48 KB default: raise the cap once per device
+    static int granted[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || granted[dev] < (int)smem) {
+      if (cudaFuncSetAttribute(engine_kernel<V, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return check_launch("cudaFuncSetAttribute(engine_kernel)");
+      if (dev >= 0 && dev < 64) granted[dev] = (int)smem;
+    }
+  }
   engine_kernel<V, G, W><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
   return check_launch("engine_kernel");
 }
