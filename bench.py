@@ -253,13 +253,14 @@ def main():
 
         def step():
             op(y)
-        launches_per_step = len(op.cols) - 1
+        launches_per_step = sum(G.gsp_spmm_plan_info(op.local, g_, c1 - c0)[0]
+                                for g_, c0, c1 in zip(op.gathered, op.cols[:-1], op.cols[1:])) if op.rows else 0
     else:
         y = torch.empty((n, f), dtype=torch.float32, device=dev)
 
         def step():
             G.gsp_spmm(gn, x, f=f, y=y, slab_cols=args.slab_cols, block_nnz=args.block_nnz)
-        launches_per_step = 1
+        launches_per_step, plan_slab, plan_tail = G.gsp_spmm_plan_info(gn, x, f, args.slab_cols, args.block_nnz)
 
     for _ in range(args.warmup):
         step()
@@ -299,7 +300,9 @@ def main():
                    "graph": "chung-lu gamma=2.5 seed=1 (Reddit node/edge counts, P:25)",
                    "l2": "flushed before every step (256 MB memset, untimed); X (562 MB) > L2 as well",
                    "parallelism": f"row-partition x{world}" + (f" + NCCL all-gather ({args.chunks} chunks)" if world > 1 else ""),
-                   "slab_cols": args.slab_cols or "auto", "block_nnz": args.block_nnz or "auto"},
+                   "slab_cols": args.slab_cols or "auto", "block_nnz": args.block_nnz or "auto",
+                   "plan": None if world > 1 else {"launches": launches_per_step, "slab_cols": plan_slab,
+                                                   "tail_slab_cols": plan_tail}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(cfg.name) if world == 1 else None,
                      "kernel": "engine_kernel<4,*,WeightVal> (gsp_spmm)",

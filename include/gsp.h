@@ -157,6 +157,14 @@ typedef struct {
 gsp_status gsp_spmm_ex(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
                        int64_t ldy, const gsp_spmm_opts *opts, gsp_stream stream);
 
+/* The launch plan gsp_spmm / gsp_spmm_ex(opts) would use for these arguments
+ * (host only, no launch): number of kernel launches (1, or 2 when a narrower
+ * tail launch covers the last columns), the main slab width and the tail slab
+ * width (0 if none).  Any output pointer may be NULL. */
+gsp_status gsp_spmm_plan_info(const gsp_csr *a, const float *x, int64_t f, int64_t ldx,
+                              const gsp_spmm_opts *opts, int32_t *launches, int32_t *slab_cols,
+                              int32_t *tail_slab_cols);
+
 /* ---------------------------------------------------------------------------
  * a6. Edge-wise softmax per head, max-subtracted.
  * P:653-656 (§4.1: alpha'_uv = exp(alpha_uv) / sum_{w in N(u)} exp(alpha_uw);
@@ -195,14 +203,16 @@ gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, const float *z,
  *   s[e,h]  = LeakyReLU(el[u,h] + er[v,h]; negative_slope)     e = (u,v), A13
  *   alpha   = edge softmax of s over row u, per head
  *   Y[u,h,:] = sum_e alpha[e,h] Z[v,h,:]
- * Two launches: a per-(row, head) statistics pass (max and sum of exp, kept in
- * the workspace, never per-edge) and the fused score -> softmax -> aggregate
- * pass.  Per-edge scores and alpha are never materialised unless alpha_out is
- * non-NULL.
+ * ONE launch: the team that owns a (row, head) first reduces the row's
+ * softmax statistics (max and sum of exp, fp64, warp-shuffle butterflies;
+ * hub rows: the whole CTA) and then runs the fused score -> softmax ->
+ * aggregate pass.  Per-edge scores and alpha are never materialised unless
+ * alpha_out is non-NULL.
  *   el  device fp32 [a->n_rows][heads];  er device fp32 [a->n_cols][heads]
  *   z   device fp32 [a->n_cols][ldz] ([H][D]);  y device fp32 [a->n_rows][ldy]
  *   alpha_out  device fp32 [nnz][heads] or NULL
- *   ws  device workspace >= gsp_gat_workspace(a, heads) bytes
+ *   ws  device workspace of gsp_gat_workspace(a, heads) bytes (currently 0:
+ *       ws may be NULL; the parameter is kept for ABI stability)
  * The score is formed in fp64 (el + er, slope multiply, minus the row max) and
  * rounded once before the fp32 exponential.
  */

@@ -31,7 +31,8 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
 # every symbol include/gsp.h declares
 EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
-           "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version")
+           "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
+           "gsp_spmm_plan_info")
 
 
 class GspError(RuntimeError):
@@ -70,6 +71,8 @@ def lib() -> ctypes.CDLL:
             "gsp_sym_normalize": [CP, P, P, P],
             "gsp_spmm": [CP, P, I, I, P, I, P],
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
+            "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
             "gsp_multihead_spmm": [CP, I32, P, P, I, I, P, I, P],
             "gsp_attn_project": [I, I32, I, P, I, P, P, P, P, P],
@@ -218,6 +221,18 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
 
 
 gsp_spmm_ex = gsp_spmm
+
+
+def gsp_spmm_plan_info(a: CSR, x: torch.Tensor, f: Optional[int] = None, slab_cols: int = 0, block_nnz: int = 0):
+    """(launches, slab_cols, tail_slab_cols) gsp_spmm would use (host only)."""
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    o = gsp_spmm_opts(slab_cols, block_nnz)
+    n, sc, tc = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    v = a.view()
+    _check(lib().gsp_spmm_plan_info(ctypes.byref(v), _ptr(x), f, ldx, ctypes.byref(o), ctypes.byref(n),
+                                    ctypes.byref(sc), ctypes.byref(tc)), "gsp_spmm_plan_info")
+    return n.value, sc.value, tc.value
 
 
 # ---------------------------------------------------------------------------

@@ -213,7 +213,7 @@ extern "C" gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, cons
 extern "C" gsp_status gsp_gat_workspace(const gsp_csr *a, int32_t heads, size_t *ws_bytes) {
   clear_detail();
   if (!a || heads <= 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_gat_workspace: bad argument");
-  *ws_bytes = (size_t)(a->n_rows > 0 ? a->n_rows : 0) * heads * sizeof(GatStat);
+  *ws_bytes = 0;  // the softmax statistics live in registers / shared memory of the fused kernel
   return GSP_OK;
 }
 
@@ -222,24 +222,20 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
                                         int64_t ldy, float *alpha_out, void *ws, size_t ws_bytes, gsp_stream stream) {
   const char *fn = "gsp_gat_aggregate";
   clear_detail();
+  (void)ws;
+  (void)ws_bytes;
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
   if (heads <= 0 || d < 0) return fail(GSP_ERR_INVALID_ARG, "%s: heads >= 1 and d >= 0 required", fn);
   const int64_t f = (int64_t)heads * d;
   if (ldz < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need ldz, ldy >= heads*d", fn);
-  if (a->n_rows == 0) return GSP_OK;
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
   if (!y || !el || (a->n_cols > 0 && (!z || !er)))
     return fail(GSP_ERR_INVALID_ARG, "%s: null pointer", fn);
-  const size_t need = (size_t)a->n_rows * heads * sizeof(GatStat);
-  if (!ws || ws_bytes < need) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, need);
-  if ((reinterpret_cast<uintptr_t>(ws) & 15u) != 0) return fail(GSP_ERR_WORKSPACE, "%s: ws must be 16B aligned", fn);
   const size_t zb = a->n_cols ? (size_t)((a->n_cols - 1) * ldz + f) * 4 : 0;
   const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
-  if (f > 0 && overlaps(z, zb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: z and y overlap", fn);
+  if (overlaps(z, zb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: z and y overlap", fn);
   cudaStream_t s = cs(stream);
-  GatStat *stats = reinterpret_cast<GatStat *>(ws);
-  st = launch_stats<true, false>(a, el, er, nullptr, negative_slope, heads, stats, nullptr, s);
-  if (st || f == 0) return st;
   int vmax = 1;
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
@@ -261,6 +257,6 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
-  WeightGat w{el, er, stats, alpha_out, negative_slope, heads};
+  WeightGat w{el, er, alpha_out, negative_slope, heads};
   return engine_launch(L, p, w, s);
 }

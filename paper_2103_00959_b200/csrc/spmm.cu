@@ -69,25 +69,39 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
   return GSP_OK;
 }
 
-static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
-                            const gsp_spmm_opts *opts, cudaStream_t s, const char *fn) {
-  clear_detail();
-  gsp_status st = check_csr(a, false, fn);
-  if (st) return st;
-  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
-  if (a->n_rows == 0 || f == 0) return GSP_OK;
-  if (!y) return fail(GSP_ERR_INVALID_ARG, "%s: y is NULL", fn);
-  if (a->n_cols > 0 && !x) return fail(GSP_ERR_INVALID_ARG, "%s: x is NULL", fn);
-  const size_t xb = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 4 : 0;
-  const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
-  if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+// The slab plan of one gsp_spmm call: the main launch covers [0, f_main) with
+// slab width L.slab_cols; when the last slab would leave more than half of its
+// lanes idle, the remaining columns [f_main, f) go to a second, narrower launch.
+struct SpmmPlan {
+  EngineLaunch main, tail;
+  int64_t f_main, f_tail;
+};
+
+static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, const gsp_spmm_opts *opts,
+                            SpmmPlan *P) {
   int vmax = 1;
   if (ldx % 4 == 0 && aligned16(x)) vmax = 4;
   else if (ldx % 2 == 0 && aligned8(x)) vmax = 2;
-  EngineLaunch L;
-  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, opts ? opts->slab_cols : 0,
-                   opts ? opts->block_nnz : 0, &L);
+  const int32_t slab_req = opts ? opts->slab_cols : 0, block_req = opts ? opts->block_nnz : 0;
+  gsp_status st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, slab_req, block_req, &P->main);
   if (st) return st;
+  P->f_main = f;
+  P->f_tail = 0;
+  const int64_t SW = P->main.slab_cols, rem = f % SW;
+  if (slab_req == 0 && P->main.V == 4 && f > SW && rem && rem <= SW / 2) {
+    int64_t tw = 16;
+    while (tw < rem) tw *= 2;
+    st = engine_plan(a->n_rows, a->n_cols, a->nnz, rem, 0, vmax, (int32_t)tw, block_req, &P->tail);
+    if (st) return st;
+    P->f_main = f - rem;
+    P->f_tail = rem;
+    P->main.nslab = P->f_main / SW;
+  }
+  return GSP_OK;
+}
+
+static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
+                                   float *y, int64_t ldy, cudaStream_t s) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -102,8 +116,28 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   p.head_dim = 0;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
-  if ((st = engine_ldxv(p, L, a->n_cols, ldx))) return st;
+  gsp_status st = engine_ldxv(p, L, a->n_cols, ldx);
+  if (st) return st;
   return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
+}
+
+static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                            const gsp_spmm_opts *opts, cudaStream_t s, const char *fn) {
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!y) return fail(GSP_ERR_INVALID_ARG, "%s: y is NULL", fn);
+  if (a->n_cols > 0 && !x) return fail(GSP_ERR_INVALID_ARG, "%s: x is NULL", fn);
+  const size_t xb = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 4 : 0;
+  const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
+  if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+  SpmmPlan P;
+  if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, s))) return st;
+  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, s);
+  return st;
 }
 
 }  // namespace gsp
@@ -118,6 +152,25 @@ extern "C" gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int6
 extern "C" gsp_status gsp_spmm_ex(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
                                   const gsp_spmm_opts *opts, gsp_stream stream) {
   return spmm_impl(a, x, f, ldx, y, ldy, opts, cs(stream), "gsp_spmm_ex");
+}
+
+extern "C" gsp_status gsp_spmm_plan_info(const gsp_csr *a, const float *x, int64_t f, int64_t ldx,
+                                         const gsp_spmm_opts *opts, int32_t *launches, int32_t *slab_cols,
+                                         int32_t *tail_slab_cols) {
+  clear_detail();
+  gsp_status st = check_csr(a, false, "gsp_spmm_plan_info");
+  if (st) return st;
+  if (f < 0 || ldx < f) return fail(GSP_ERR_INVALID_ARG, "gsp_spmm_plan_info: need f >= 0, ldx >= f");
+  SpmmPlan P{};
+  if (a->n_rows == 0 || f == 0) {
+    if (launches) *launches = 0;
+    return GSP_OK;
+  }
+  if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
+  if (launches) *launches = P.f_tail ? 2 : 1;
+  if (slab_cols) *slab_cols = (int32_t)P.main.slab_cols;
+  if (tail_slab_cols) *tail_slab_cols = P.f_tail ? (int32_t)P.tail.slab_cols : 0;
+  return GSP_OK;
 }
 
 extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const float *alpha, const float *z,

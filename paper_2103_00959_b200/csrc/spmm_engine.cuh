@@ -176,15 +176,17 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   __device__ __forceinline__ Row row(int64_t, int h, bool) const { return Row{alpha, heads, h}; }
 };
 
-struct GatStat {  // per (row, head) softmax statistics
+struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax)
   double m;       // row max of the score (fp64)
   float inv_s;    // 1 / sum exp(s - m)
   float pad;
 };
 
-struct WeightGat {  // fused score -> softmax weight (A13)
+// Fused GAT weight (A13): s = LeakyReLU(el[u] + er[v]) in fp64,
+// alpha = exp(s - m) / S with the row statistics (m, S) computed inside the
+// aggregate kernel by the team that owns the (row, head) -- no stats pass.
+struct WeightGat {
   const float *el, *er;
-  const GatStat *stat;
   float *alpha_out;
   double slope;
   int heads;
@@ -195,19 +197,20 @@ struct WeightGat {  // fused score -> softmax weight (A13)
     double el_u, m, slope;
     float inv_s;
     int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int c) const {
+    __device__ __forceinline__ double score(int c) const {
       const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
-      const double s = t >= 0.0 ? t : slope * t;
+      return t >= 0.0 ? t : slope * t;
+    }
+    __device__ __forceinline__ float finish(int64_t e, double s) const {
       const float a = expf((float)(s - m)) * inv_s;
       if (alpha_out) alpha_out[e * heads + h] = a;
       return a;
     }
+    __device__ __forceinline__ float w(int64_t e, int c) const { return finish(e, score(c)); }
   };
   // first_slab: only the first slab of a head writes alpha_out (each entry once)
   __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab) const {
-    const GatStat st = stat[r * heads + h];
-    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), st.m, slope, st.inv_s,
-               heads, h};
+    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), 0.0, slope, 0.0f, heads, h};
   }
 };
 
@@ -255,6 +258,19 @@ struct UnrollFor {  // gathers in flight per lane, capped by register budget
 //   out = acc2 + acc1 (kLong: hub ranges) or acc1 (rows of <= kHub edges,
 //   i.e. <= 16 segments, where acc2 would stay 0)
 // Every lane of the team ends with the same out[] (all sub-groups combine).
+template <int T>
+__device__ __forceinline__ double team_max(double v, unsigned tmask) {
+#pragma unroll
+  for (int o = 1; o < T; o <<= 1) v = fmax(v, __shfl_xor_sync(tmask, v, o, T));
+  return v;
+}
+template <int T>
+__device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor butterfly: fixed order, all lanes equal
+#pragma unroll
+  for (int o = 1; o < T; o <<= 1) v += __shfl_xor_sync(tmask, v, o, T);
+  return v;
+}
+
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
 template <int V, int G, class Row, bool kFull>
@@ -309,7 +325,8 @@ template <int V, int G, bool kLong, class Row>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
-                                             unsigned tmask, int32_t *tc, float *tw, float (&out)[V]) {
+                                             unsigned tmask, int32_t *tc, float *tw, const double *cache, int ncache,
+                                             float (&out)[V]) {
   using TM = Team<G>;
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL;
   float acc1[V], acc2[V];
@@ -338,7 +355,12 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
         if (j < cnt) {
           const int c = seg_in ? sc[j] : __ldcs(p.col + e0 + j);
           if (!seg_in) tc[j] = c;
-          if (!Row::kUnit) tw[j] = wr.w(e0 + j, c);
+          if constexpr (Row::kComputed) {
+            const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
+            tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
+          } else if constexpr (!Row::kUnit) {
+            tw[j] = wr.w(e0 + j, c);
+          }
         }
       }
       __syncwarp(tmask);
@@ -395,6 +417,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   __shared__ __align__(8) uint64_t s_bar[kStageChunks];
   __shared__ float s_tw[NT][kSeg];    // per-team scratch: weights
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
+  constexpr bool kGat = decltype(wf.row(0, 0, false))::kComputed;
+  constexpr int kCache = kGat ? 1024 / NT : 1;  // per-team fp64 score cache (GAT)
+  __shared__ double s_cache[NT][kCache];
+  __shared__ double s_red[kThreads / 32];
   __shared__ int64_t s_win[3];  // wb, we, chunk
   extern __shared__ __align__(16) uint8_t s_dyn[];  // staged col [win_cap] then val [win_cap]
 
@@ -488,12 +514,35 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
-    const auto wr = wf.row(r, head, first_slab);
+    auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
+    if constexpr (kGat) {
+      // CTA-wide softmax statistics of a hub row: thread tid takes edges
+      // tid + 256k; warp xor butterflies, then warps 0..7 in order (fixed)
+      double m = -INFINITY;
+      for (int64_t q = tid; q < d; q += kThreads) m = fmax(m, wr.score(win.col(p.col, start + q)));
+      m = team_max<32>(m, 0xffffffffu);
+      if (lane == 0) s_red[warp] = m;
+      __syncthreads();
+      m = s_red[0];
+      for (int w2 = 1; w2 < kThreads / 32; ++w2) m = fmax(m, s_red[w2]);
+      __syncthreads();
+      double S = 0.0;
+      for (int64_t q = tid; q < d; q += kThreads)
+        S += (double)expf((float)(wr.score(win.col(p.col, start + q)) - m));
+      S = team_sum<32>(S, 0xffffffffu);
+      if (lane == 0) s_red[warp] = S;
+      __syncthreads();
+      S = s_red[0];
+      for (int w2 = 1; w2 < kThreads / 32; ++w2) S += s_red[w2];
+      __syncthreads();
+      wr.m = m;
+      wr.inv_s = (float)(1.0 / S);
+    }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
       row_segments<V, G, true>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
-                         s_tc[team], s_tw[team], part);
+                               s_tc[team], s_tw[team], nullptr, 0, part);
       if (sg == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
@@ -527,11 +576,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     if (d > kHub) continue;
-    const auto wr = wf.row(r, head, first_slab);
+    auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
+    if constexpr (kGat) {
+      // team softmax statistics; scores of the first kCache edges are cached
+      // in fp64 by the lane that will turn them into alpha (q % T == tl)
+      double m = -INFINITY;
+      for (int64_t q = tl; q < d; q += T) {
+        const double sc = wr.score(win.col(p.col, start + q));
+        if (q < kCache) s_cache[team][q] = sc;
+        m = fmax(m, sc);
+      }
+      m = team_max<T>(m, tmask);
+      double S = 0.0;
+      for (int64_t q = tl; q < d; q += T) {
+        const double sc = q < kCache ? s_cache[team][q] : wr.score(win.col(p.col, start + q));
+        S += (double)expf((float)(sc - m));
+      }
+      S = team_sum<T>(S, tmask);
+      wr.m = m;
+      wr.inv_s = (float)(1.0 / S);
+    }
     float out[V];
     row_segments<V, G, false>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
-                       s_tw[team], out);
+                              s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
   // no CTA may exit with bulk copies still writing its shared memory

@@ -75,9 +75,9 @@ def test_host_validation(L):
     assert L.gsp_multihead_spmm(ctypes.byref(c), 4, P(0x5000), P(0x10000), 8, 16, P(0x90000), 32, s) == 1
     # softmax heads <= 0
     assert L.gsp_edge_softmax(ctypes.byref(c), 0, P(0x5000), P(0x5000), s) == 1
-    # gat workspace too small
-    assert L.gsp_gat_aggregate(ctypes.byref(c), 2, P(0x5000), P(0x6000), 0.2, P(0x10000), 4, 8, P(0x90000), 8,
-                               None, P(0xA000), 8, s) == 6
+    # gat: heads * d > ldz
+    assert L.gsp_gat_aggregate(ctypes.byref(c), 4, P(0x5000), P(0x6000), 0.2, P(0x10000), 4, 8, P(0x90000), 16,
+                               None, None, 0, s) == 1
     # normalize needs values
     c0 = _csr(val=None)
     assert L.gsp_sym_normalize(ctypes.byref(c0), P(0x7000), P(0x8000), s) == 1

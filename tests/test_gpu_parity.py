@@ -189,13 +189,19 @@ def test_spmm_hub_rows_and_star(built):
         assert_within(host(G.gsp_spmm(gn, dev(x))), yref, cond, what=name)
 
 
-def test_spmm_deterministic_and_config_invariant(built):
+@pytest.mark.parametrize("f", [256, 300])
+def test_spmm_deterministic_and_config_invariant(built, f):
+    """Bitwise identical for every slab width / block size (incl. the 256-col
+    two-float4 path and the narrow tail launch: F=300 -> 2x128 + 64)."""
     go, gg, _, gn = built["rmat3000"]
-    x = dev(features(go.n, 256, seed=5))
+    x = dev(features(go.n, f, seed=5))
     y0 = G.gsp_spmm(gn, x)
-    for slab, blk in [(0, 0), (4, 0), (32, 512), (64, 300), (128, 10000), (8, 0), (16, 64)]:
+    if f == 300:
+        assert G.gsp_spmm_plan_info(gn, x) == (2, 128, 64)
+    for slab, blk in [(0, 0), (4, 0), (32, 512), (64, 300), (128, 10000), (8, 0), (16, 64), (256, 0), (256, 777)]:
         y = G.gsp_spmm(gn, x, slab_cols=slab, block_nnz=blk)
         assert torch.equal(y, y0), (slab, blk)
+    assert torch.equal(G.gsp_spmm(gn, x), y0)
 
 
 def test_spmm_identity_sqrt_degree_full_c2():
