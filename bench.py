@@ -224,7 +224,8 @@ def main():
     G.lib()  # fail loudly if the extension is missing
 
     cfg = CONFIGS[args.config]
-    src, dst = graph_for(cfg, seed=1)
+    from synth.graphs import GENERATOR
+    src, dst = graph_for(cfg, seed=1, gen=GENERATOR.get(args.config, "chung_lu"))
     s_t = torch.from_numpy(src).to(dev)
     d_t = torch.from_numpy(dst).to(dev)
     # --- a1 + a2: one-off build + normalisation (components) ---

@@ -55,7 +55,13 @@ CONFIGS = {
     # P:26 Yelp 716,847 nodes, 6,977,410 edges, 300 features
     "C5": Config("C5-yelp-gcn", 716847, 6977410, 300, note="Yelp-shaped, GCN SpMM"),
     "C6": Config("C6-yelp10x-gcn", 7168470, 69774100, 300, note="Yelp x10 power-law"),
+    # calibration probes (not paper shapes): uniform random graphs whose X is
+    # L2-resident (P1: 60K x 128 fp32 = 31 MB) or far larger than L2 (P2: 2M x 128 = 1 GB)
+    "P1": Config("P1-probe-l2resident", 60000, 11600000, 128, note="L2-resident gather probe (ER)"),
+    "P2": Config("P2-probe-dram", 2000000, 11600000, 128, note="DRAM gather probe (ER)"),
 }
+
+GENERATOR = {"P1": "er", "P2": "er"}  # default generator per config (else chung_lu)
 
 
 # --------------------------------------------------------------------------
