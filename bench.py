@@ -201,7 +201,6 @@ def main():
     ap.add_argument("--cpu-budget-ge", type=float, default=1.5e9)
     ap.add_argument("--ref-budget-ge", type=float, default=0.25e9)
     ap.add_argument("--sweep", default="", help="comma list of slab widths to time (diagnostic)")
-    ap.add_argument("--sweep-prefetch", default="", help="comma list of L2 prefetch distances (-1 = off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -332,24 +331,6 @@ def main():
             sw[str(sc)] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3),
                            "alg_GB/s": spmm_alg_bytes(n, nnz, f) / (np.mean(ts) * 1e-3) / 1e9}
         out["sweep_slab_cols"] = sw
-    if world == 1 and args.sweep_prefetch:
-        sw = {}
-        for pf in [int(v) for v in args.sweep_prefetch.split(",")]:
-            for sc in ([int(v) for v in args.sweep.split(",")] if args.sweep else [0]):
-                ts = []
-                for i in range(args.warmup + 10):
-                    flush.zero_()
-                    a0 = torch.cuda.Event(enable_timing=True)
-                    a1 = torch.cuda.Event(enable_timing=True)
-                    a0.record()
-                    G.gsp_spmm(gn, x, f=f, y=y, slab_cols=sc, prefetch=pf)
-                    a1.record()
-                    torch.cuda.synchronize()
-                    if i >= args.warmup:
-                        ts.append(a0.elapsed_time(a1))
-                sw[f"pf{pf}_sw{sc}"] = float(np.mean(ts))
-        out["sweep_prefetch_ms"] = sw
-
     # --- e2e: host buffers, H2D + kernel + D2H inside the timed region ---
     if world == 1 and not args.no_e2e:
         xh = torch.from_numpy(x_host).pin_memory()
@@ -405,7 +386,7 @@ def main():
             "aggregate_ms": tgm, "attn_project_ms": float(np.mean(tp)),
             "GE/s": g3.nnz * H * D / (tgm * 1e-3),
             "alg_GB/s": gb / (tgm * 1e-3) / 1e9, "frac_of_hbm_peak": gb / (tgm * 1e-3) / 1e9 / peak,
-            "launches": "row_stats + engine_kernel<*,*,WeightGat> per aggregate"}}
+            "launches": "one engine_kernel<4,16,WeightGat> per aggregate (softmax statistics fused)"}}
 
     # --- cpu_baseline: the oracle as it stands, bounded sample, rank 0 at N=1 ---
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

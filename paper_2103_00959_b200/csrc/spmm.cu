@@ -13,7 +13,6 @@ static int64_t pow2_floor(int64_t v) {
 // L2 bytes we aim to keep one slab of X in (126 MB L2; leave room for the
 // streamed CSR, Y and the next slab).  DESIGN.md §Kernels / slab sizing.
 static constexpr int64_t kL2SlabBudget = 48ll << 20;
-static constexpr int kDefaultPrefetch = 0;  // L2 prefetch distance (row claims); tuned in DESIGN.md §5
 
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L) {
@@ -102,7 +101,7 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
 }
 
 static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
-                                   float *y, int64_t ldy, int pf_rows, cudaStream_t s) {
+                                   float *y, int64_t ldy, cudaStream_t s) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -117,7 +116,6 @@ static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, cons
   p.head_dim = 0;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
-  p.pf_rows = pf_rows;
   gsp_status st = engine_ldxv(p, L, a->n_cols, ldx);
   if (st) return st;
   return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
@@ -137,10 +135,8 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
   SpmmPlan P;
   if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
-  // reserved[0]: L2 prefetch distance in row claims (-1 = off, 0 = default)
-  const int pf = (opts && opts->reserved[0] != 0) ? (opts->reserved[0] < 0 ? 0 : opts->reserved[0]) : kDefaultPrefetch;
-  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, pf, s))) return st;
-  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, pf, s);
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, s))) return st;
+  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, s);
   return st;
 }
 

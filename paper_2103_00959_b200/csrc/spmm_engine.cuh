@@ -56,10 +56,32 @@ constexpr int kMinBlocks = GSP_MIN_BLOCKS;  // CTAs per SM the register budget i
 // ----------------------------------------------------------------- vectors
 template <int V>
 struct Vec;
+#ifndef GSP_L2HINT
+#define GSP_L2HINT 0
+#endif
+// GSP_L2HINT=1: gathers of X carry an L2 evict_last policy and the staged CSR
+// window evict_first, so the streamed CSR does not push X slabs out of L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 template <>
 struct Vec<4> {
   static __device__ __forceinline__ void ld(float (&r)[4], const float *p) {
+#if GSP_L2HINT
+    float4 t;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(t.x), "=f"(t.y), "=f"(t.z), "=f"(t.w)
+                 : "l"(p), "l"(l2_policy_evict_last()));
+#else
     float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+#endif
     r[0] = t.x; r[1] = t.y; r[2] = t.z; r[3] = t.w;
   }
   static __device__ __forceinline__ void st(float *p, const float (&r)[4]) {
@@ -229,7 +251,6 @@ struct EngineParams {
   const float *stage_val;  // val array to stage in smem (NULL: none)
   int stage;               // 1: stage col (and stage_val) in shared memory
   int win_cap;             // window capacity in entries (multiple of 4)
-  int pf_rows;             // L2-prefetch the X slabs of the row this many claims ahead (0 = off)
 };
 
 // Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
@@ -579,22 +600,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     if (d > kHub) continue;
     auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
-    if (V >= 4 && p.pf_rows > 0 && active) {
-      // TMA L2 prefetch of the X row-slabs the team will likely gather next
-      // (row k + pf_rows is claimed pf_rows claims from now); its columns are
-      // already in the staged window, so this costs no global metadata reads.
-      const int64_t rn = r + p.pf_rows;
-      if (rn < rend) {
-        const int64_t sn = __ldg(p.row_ptr + rn), dn = __ldg(p.row_ptr + rn + 1) - sn;
-        if (dn <= kHub && win.in(sn) && sn + dn <= win.we) {
-          ensure(sn + dn);
-          const int nv = (int)(p.f - slab * SW < SW ? p.f - slab * SW : SW);  // valid columns of this slab
-          const uint32_t bytes = (uint32_t)(((nv + 3) & ~3) * 4);
-          for (int64_t q = tl; q < dn; q += T)
-            bulk_prefetch_l2(p.x + slab * SW + (size_t)win.scol[sn + q - win.wb] * p.ldx, bytes);
-        }
-      }
-    }
     if constexpr (kGat) {
       // team softmax statistics; scores of the first kCache edges are cached
       // in fp64 by the lane that will turn them into alpha (q % T == tl)
@@ -655,7 +660,6 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.stage = (nnz > 0 && aligned16(col)) ? 1 : 0;
   p.stage_val = (p.stage && val && aligned16(val)) ? val : nullptr;
   p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
-  p.pf_rows = 0;
 }
 
 template <int V, int G, class W>
