@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--slab-cols", type=int, default=0)
     ap.add_argument("--block-nnz", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=4, help="feature chunks for comm/compute overlap (N>1)")
+    ap.add_argument("--dist", action="store_true", help="use the row-partitioned NCCL path even at N=1")
     ap.add_argument("--no-gat", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -216,10 +217,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", local if use_dist else 0)
     torch.cuda.set_device(dev)
     G.lib()  # fail loudly if the extension is missing
 
@@ -245,7 +251,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    if world > 1:
+    if use_dist:
         from paper_2103_00959_b200.dist import RowPartitionedSpMM
         op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev)
         op.load_shard(x[op.r0:op.r1, :f])
@@ -266,7 +272,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -278,11 +284,11 @@ def main():
             step()
             ends[i].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = float(np.mean(times))
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
@@ -300,9 +306,9 @@ def main():
         "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ld": cfg.ld,
                    "graph": "chung-lu gamma=2.5 seed=1 (Reddit node/edge counts, P:25)",
                    "l2": "flushed before every step (256 MB memset, untimed); X (562 MB) > L2 as well",
-                   "parallelism": f"row-partition x{world}" + (f" + NCCL all-gather ({args.chunks} chunks)" if world > 1 else ""),
+                   "parallelism": f"row-partition x{world}" + (f" + NCCL all-gather ({args.chunks} chunks)" if use_dist else ""),
                    "slab_cols": args.slab_cols or "auto", "block_nnz": args.block_nnz or "auto",
-                   "plan": None if world > 1 else {"launches": launches_per_step, "slab_cols": plan_slab,
+                   "plan": None if use_dist else {"launches": launches_per_step, "slab_cols": plan_slab,
                                                    "tail_slab_cols": plan_tail}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(cfg.name) if world == 1 else None,
@@ -314,7 +320,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
     }
 
-    if world == 1 and args.sweep:
+    if not use_dist and args.sweep:
         sw = {}
         for sc in [int(v) for v in args.sweep.split(",")]:
             ts = []
@@ -332,7 +338,7 @@ def main():
                            "alg_GB/s": spmm_alg_bytes(n, nnz, f) / (np.mean(ts) * 1e-3) / 1e9}
         out["sweep_slab_cols"] = sw
     # --- e2e: host buffers, H2D + kernel + D2H inside the timed region ---
-    if world == 1 and not args.no_e2e:
+    if not use_dist and not args.no_e2e:
         xh = torch.from_numpy(x_host).pin_memory()
         yh = torch.empty((n, f), dtype=torch.float32).pin_memory()
         ts = []
@@ -351,11 +357,34 @@ def main():
         out["e2e"] = {"value": ge / (te * 1e-3), "unit": "GE/s", "ms_per_step": te,
                       "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4),
                       "api": "gsp_spmm via the Python binding of the C ABI, pinned host X -> device -> host Y"}
-    elif world > 1:
-        out["e2e"] = None
+    elif use_dist and not args.no_e2e:
+        # each rank: pinned host X shard -> device, all-gather + local SpMM, Y shard -> host
+        xh = torch.from_numpy(np.ascontiguousarray(x_host[op.r0:op.r1, :f])).pin_memory()
+        yh = torch.empty((op.rows, f), dtype=torch.float32).pin_memory()
+        xs = torch.empty((op.rows, f), dtype=torch.float32, device=dev)
+        ts = []
+        for i in range(args.warmup + max(3, args.steps // 3)):
+            dist.barrier()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            xs.copy_(xh, non_blocking=True)
+            op.load_shard(xs)
+            op(y)
+            yh.copy_(y, non_blocking=True)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ts.append(a0.elapsed_time(a1))
+        te = torch.tensor([float(np.mean(ts))], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        out["e2e"] = {"value": ge / (te * 1e-3), "unit": "GE/s", "ms_per_step": te,
+                      "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(yh.numel() * 4) * world,
+                      "api": "RowPartitionedSpMM (gsp_csr_slice + NCCL all-gather + gsp_spmm), pinned host shards"}
 
     # --- secondary: fused GAT aggregate on the Flickr-shaped graph (C3) ---
-    if world == 1 and not args.no_gat:
+    if not use_dist and not args.no_gat:
         c3 = CONFIGS["C3"]
         H, D = c3.heads, c3.d
         s3, d3 = graph_for(c3, seed=1)
@@ -389,7 +418,7 @@ def main():
             "launches": "one engine_kernel<4,16,WeightGat> per aggregate (softmax statistics fused)"}}
 
     # --- cpu_baseline: the oracle as it stands, bounded sample, rank 0 at N=1 ---
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+    if not use_dist and rank == 0 and not args.no_cpu_baseline:
         try:
             import oracle as orc
             gh_rp = gn.row_ptr.cpu().numpy()
@@ -404,7 +433,7 @@ def main():
 
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

@@ -1,0 +1,106 @@
+"""Multi-process (world size 2 and 3, gloo, CPU) tests of the row-partitioned
+SpMM driver paper_2103_00959_b200.dist.RowPartitionedSpMM: partition, padded
+all-gather layout, feature chunking and shard assembly.  The per-rank compute
+steps are the oracle's (injected as `ops`), so these run without a GPU; the
+CUDA kernels behind the same steps are checked on one GPU by
+test_gpu_parity.py::test_partition_slice_bit_exact_and_invariant."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as orc
+from synth import chung_lu, features
+
+
+class OracleCSR:
+    def __init__(self, row_ptr, col, val, n_cols):
+        self.row_ptr, self.col, self.val, self.n_cols = row_ptr, col, val, n_cols
+        self.n_rows = row_ptr.size - 1
+
+
+class OracleOps:
+    """Host stand-ins for gsp_partition_rows / gsp_csr_slice / gsp_spmm."""
+
+    @staticmethod
+    def partition(a, parts):
+        return orc.partition_rows(a.row_ptr, parts)
+
+    @staticmethod
+    def slice(a, bounds, rank, npad):
+        rp, co, vo = orc.csr_slice(a.row_ptr, a.col, a.val, np.asarray(bounds), rank, npad)
+        return OracleCSR(rp, co, vo, len(bounds) * npad - npad)
+
+    @staticmethod
+    def spmm(local, x, f, y):
+        yy, _ = orc.spmm(local.row_ptr, local.col, local.val.astype(np.float64), x.numpy(), f=f, want_cond=False)
+        y.copy_(torch.from_numpy(yy.astype(np.float32)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gather(out, inp):
+    parts = list(out.chunk(dist.get_world_size(), dim=0))
+    dist.all_gather(parts, inp.contiguous())
+    out.copy_(torch.cat(parts, 0))
+
+
+def _worker(rank, world, port, n, m, f, chunks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_00959_b200.dist import RowPartitionedSpMM
+        s, d = chung_lu(n, m, seed=3)
+        g = orc.build_csr(n, s, d, None, True, 1.0)
+        _, _, a32 = orc.sym_norm(g)
+        a = OracleCSR(g.row_ptr, g.col, a32, n)
+        x = features(n, f, seed=4)
+        op = RowPartitionedSpMM(a, rank, world, f, chunks=chunks, all_gather=_gather, device="cpu", ops=OracleOps)
+        op.load_shard(torch.from_numpy(x[op.r0:op.r1]))
+        y = op()
+        yref, _ = orc.spmm(g.row_ptr, g.col, a32.astype(np.float64), x, want_cond=False)
+        ok = np.array_equal(y.numpy(), yref[op.r0:op.r1].astype(np.float32))
+        q.put((rank, ok, op.r0, op.r1, op.npad, op.cols))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3), (3, 4)])
+def test_row_partitioned_spmm_gloo(world, chunks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n, m, f = 3000, 20000, 37
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, f, chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    assert all(ok for _, ok, *_ in res), res
+    # the row blocks tile [0, n) and the chunks tile [0, f)
+    assert res[0][2] == 0 and res[-1][3] == n
+    for a, b in zip(res[:-1], res[1:]):
+        assert a[3] == b[2]
+    cols = res[0][5]
+    assert cols[0] == 0 and cols[-1] == f and all(c % 4 == 0 for c in cols[:-1])
+
+
+def test_chunk_bounds_and_padding():
+    from paper_2103_00959_b200.dist import chunk_bounds, padded_rows
+    assert chunk_bounds(602, 4) == [0, 152, 304, 456, 602]
+    assert chunk_bounds(3, 4) == [0, 3]
+    assert chunk_bounds(8, 1) == [0, 8]
+    assert padded_rows([0, 5, 5, 12]) == 7

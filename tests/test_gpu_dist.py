@@ -1,0 +1,75 @@
+"""The multi-GPU product path (RowPartitionedSpMM with the libgsp kernels) on
+the one GPU a test box has: P ranks share cuda:0 and exchange their padded X
+shards through a gloo all-gather staged via host memory (NCCL refuses two ranks
+on one device), plus a world-size-1 NCCL run of the same driver.  Each rank's Y
+shard must be bitwise equal to the single-process gsp_spmm result (DESIGN.md
+§6, §9)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _staged_gather(out, inp):
+    parts = [torch.empty_like(inp, device="cpu") for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, inp.cpu())
+    out.copy_(torch.cat(parts, 0))
+
+
+def _worker(rank, world, port, backend, chunks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2103_00959_b200 as G
+        from paper_2103_00959_b200.dist import RowPartitionedSpMM
+        from synth import chung_lu, features
+        n, m, f = 20000, 150000, 300
+        s, d = chung_lu(n, m, seed=5)
+        dev = torch.device("cuda", 0)
+        g = G.gsp_sym_normalize(G.gsp_coo_to_csr(n, torch.from_numpy(s).to(dev), torch.from_numpy(d).to(dev)))
+        x = torch.from_numpy(features(n, f, (f + 3) // 4 * 4, seed=6)).to(dev)
+        y_ref = G.gsp_spmm(g, x, f=f)
+        op = RowPartitionedSpMM(g, rank, world, f, chunks=chunks, device=dev,
+                                all_gather=None if backend == "nccl" else _staged_gather)
+        op.load_shard(x[op.r0:op.r1, :f])
+        y = op()
+        torch.cuda.synchronize()
+        ok = torch.equal(y, y_ref[op.r0:op.r1])
+        q.put((rank, ok, op.r0, op.r1))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), -1, -1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend,chunks", [(1, "nccl", 4), (2, "gloo", 1), (2, "gloo", 4), (3, "gloo", 2)])
+def test_row_partitioned_spmm_on_one_gpu(world, backend, chunks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(ok is True for _, ok, *_ in res), res
+    assert res[0][2] == 0 and res[-1][3] == 20000
