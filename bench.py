@@ -194,7 +194,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--slab-cols", type=int, default=0)
     ap.add_argument("--block-nnz", type=int, default=0)
-    ap.add_argument("--chunks", type=int, default=4, help="feature chunks for comm/compute overlap (N>1)")
+    ap.add_argument("--chunks", type=int, default=5, help="feature chunks (128-col aligned) for comm/compute overlap (N>1)")
     ap.add_argument("--dist", action="store_true", help="use the row-partitioned NCCL path even at N=1")
     ap.add_argument("--no-gat", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -48,8 +48,9 @@ def padded_rows(bounds: List[int]) -> int:
     return max(bounds[p + 1] - bounds[p] for p in range(len(bounds) - 1))
 
 
-def chunk_bounds(f: int, chunks: int, align: int = 4) -> List[int]:
-    """Column chunk edges, multiples of `align` (so float4 paths survive)."""
+def chunk_bounds(f: int, chunks: int, align: int = 128) -> List[int]:
+    """Column chunk edges, multiples of `align` (default: the 128-column slab
+    width, so every chunk is whole slabs and needs no narrow tail launch)."""
     chunks = max(1, min(chunks, (f + align - 1) // align))
     step = ((f + chunks - 1) // chunks + align - 1) // align * align
     edges = list(range(0, f, step)) + [f]

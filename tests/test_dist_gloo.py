@@ -80,7 +80,7 @@ def test_row_partitioned_spmm_gloo(world, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    n, m, f = 3000, 20000, 37
+    n, m, f = 3000, 20000, 300
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, f, chunks, q)) for r in range(world)]
     for p in procs:
         p.start()
@@ -95,12 +95,14 @@ def test_row_partitioned_spmm_gloo(world, chunks):
     for a, b in zip(res[:-1], res[1:]):
         assert a[3] == b[2]
     cols = res[0][5]
-    assert cols[0] == 0 and cols[-1] == f and all(c % 4 == 0 for c in cols[:-1])
+    assert cols[0] == 0 and cols[-1] == f and all(c % 128 == 0 for c in cols[:-1])
 
 
 def test_chunk_bounds_and_padding():
     from paper_2103_00959_b200.dist import chunk_bounds, padded_rows
-    assert chunk_bounds(602, 4) == [0, 152, 304, 456, 602]
+    assert chunk_bounds(602, 4, align=4) == [0, 152, 304, 456, 602]
+    assert chunk_bounds(602, 5) == [0, 128, 256, 384, 512, 602]
+    assert chunk_bounds(602, 4) == [0, 256, 512, 602]
     assert chunk_bounds(3, 4) == [0, 3]
     assert chunk_bounds(8, 1) == [0, 8]
     assert padded_rows([0, 5, 5, 12]) == 7
