@@ -271,15 +271,6 @@ struct UnrollFor {  // gathers in flight per lane, capped by register budget
   static constexpr int U = V >= 8 ? (kUnroll < 4 ? kUnroll : 4) : kUnroll;
 };
 
-// Accumulate segments [s_begin, s_end) of the row starting at `start` (degree
-// d) into out[V].  Canonical order (independent of G, V, T):
-//   residue chain r_k = fma chain, from 0, over the segment's edges j with
-//                       j % 4 == k, in increasing j
-//   segment sum       = (r_0 + r_1) + (r_2 + r_3)
-//   acc1 += segment (sequential); every 32 segments acc2 += acc1, acc1 = 0
-//   out = acc2 + acc1 (kLong: hub ranges) or acc1 (rows of <= kHub edges,
-//   i.e. <= 16 segments, where acc2 would stay 0)
-// Every lane of the team ends with the same out[] (all sub-groups combine).
 template <int T>
 __device__ __forceinline__ double team_max(double v, unsigned tmask) {
 #pragma unroll
@@ -295,10 +286,10 @@ __device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor b
 
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
-template <int V, int G, class Row, bool kFull>
+template <int V, int G, class Row, bool kFull, class Pre>
 __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
                                            const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
-                                           int sg, float (&a)[Team<G>::NACC][V]) {
+                                           int sg, float (&a)[Team<G>::NACC][V], Pre &&pre) {
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
   constexpr int U = TM::U < UnrollFor<V>::U ? TM::U : UnrollFor<V>::U;
@@ -306,13 +297,11 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
   for (int t0 = 0; t0 < EPS; t0 += U) {
     if (!kFull && SPR * t0 >= cnt) break;
     float xv[U][V];
-    float ww[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = sg + SPR * (t0 + u);
       const bool ok = kFull || j < cnt;
       const uint32_t cj = ok ? (uint32_t)sc[j] : 0u;
-      ww[u] = Row::kUnit ? 1.0f : (ok ? sw[j] : 0.0f);
       if (ok && active) {
         vld<V>(xv[u], xb + cj * ldxv);
       } else {
@@ -320,12 +309,17 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
         for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
       }
     }
+    // the first chunk's gathers are in flight: now make the weights (team-
+    // uniform hook; fills sw when the weights need arithmetic or loads)
+    if (t0 == 0) pre();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int t = t0 + u;
-      if (kFull || sg + SPR * t < cnt) {
+      const int j = sg + SPR * t;
+      if (kFull || j < cnt) {
+        const float ww = Row::kUnit ? 1.0f : sw[j];
 #pragma unroll
-        for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww[u], xv[u][i], a[t % NACC][i]);
+        for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww, xv[u][i], a[t % NACC][i]);
       }
     }
   }
@@ -343,12 +337,12 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 // Metadata: segments inside the TMA-staged window are read from it directly;
 // other segments (hub rows beyond the window, unstaged arrays) and computed
 // weights go through the team's 32-entry shared scratch (tc, tw).
-template <int V, int G, bool kLong, class Row>
-__device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, const Row &wr, int64_t start,
+template <int V, int G, bool kLong, class Row, class Pro>
+__device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
                                              unsigned tmask, int32_t *tc, float *tw, const double *cache, int ncache,
-                                             float (&out)[V]) {
+                                             float (&out)[V], Pro &&prologue) {
   using TM = Team<G>;
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL;
   float acc1[V], acc2[V];
@@ -370,30 +364,42 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
       sc = tc;
       scratch = true;
     }
-    if (scratch) {  // cooperative: lane tl makes entries tl + T*i
+    if (!seg_in) {  // column indices from global memory into the team scratch
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         const int j = tl + T * i;
-        if (j < cnt) {
-          const int c = seg_in ? sc[j] : __ldcs(p.col + e0 + j);
-          if (!seg_in) tc[j] = c;
-          if constexpr (Row::kComputed) {
-            const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
-            tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
-          } else if constexpr (!Row::kUnit) {
-            tw[j] = wr.w(e0 + j, c);
-          }
-        }
+        if (j < cnt) tc[j] = __ldcs(p.col + e0 + j);
       }
       __syncwarp(tmask);
     }
+    // weights are made while the first chunk of gathers is in flight
+    const bool first = (s == s_begin);
+    auto pre = [&]() {
+      if (first) prologue();
+      if (scratch && !Row::kUnit) {  // cooperative: lane tl makes entries tl + T*i
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const int j = tl + T * i;
+          if (j < cnt) {
+            const int c = sc[j];
+            if constexpr (Row::kComputed) {
+              const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
+              tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
+            } else {
+              tw[j] = wr.w(e0 + j, c);
+            }
+          }
+        }
+        __syncwarp(tmask);
+      }
+    };
     float a[NACC][V];
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < V; ++i) a[q][i] = 0.0f;
-    if (cnt == kSeg) seg_gather<V, G, Row, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a);
-    else seg_gather<V, G, Row, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a);
+    if (cnt == kSeg) seg_gather<V, G, Row, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
+    else seg_gather<V, G, Row, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
     if (scratch) __syncwarp(tmask);  // scratch is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
       row_segments<V, G, true>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
-                               s_tc[team], s_tw[team], nullptr, 0, part);
+                               s_tc[team], s_tw[team], nullptr, 0, part, [] {});
       if (sg == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
@@ -600,28 +606,31 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     if (d > kHub) continue;
     auto wr = wf.row(r, head, first_slab);
     ensure(start + d);
-    if constexpr (kGat) {
-      // team softmax statistics; scores of the first kCache edges are cached
-      // in fp64 by the lane that will turn them into alpha (q % T == tl)
-      double m = -INFINITY;
-      for (int64_t q = tl; q < d; q += T) {
-        const double sc = wr.score(win.col(p.col, start + q));
-        if (q < kCache) s_cache[team][q] = sc;
-        m = fmax(m, sc);
+    // GAT: the team's softmax statistics run inside the first segment, after
+    // its first chunk of Z gathers has been issued; scores of the first kCache
+    // edges are cached in fp64 by the lane that later turns them into alpha
+    auto stats = [&]() {
+      if constexpr (kGat) {
+        double m = -INFINITY;
+        for (int64_t q = tl; q < d; q += T) {
+          const double sc = wr.score(win.col(p.col, start + q));
+          if (q < kCache) s_cache[team][q] = sc;
+          m = fmax(m, sc);
+        }
+        m = team_max<T>(m, tmask);
+        double S = 0.0;
+        for (int64_t q = tl; q < d; q += T) {
+          const double sc = q < kCache ? s_cache[team][q] : wr.score(win.col(p.col, start + q));
+          S += (double)expf((float)(sc - m));
+        }
+        S = team_sum<T>(S, tmask);
+        wr.m = m;
+        wr.inv_s = (float)(1.0 / S);
       }
-      m = team_max<T>(m, tmask);
-      double S = 0.0;
-      for (int64_t q = tl; q < d; q += T) {
-        const double sc = q < kCache ? s_cache[team][q] : wr.score(win.col(p.col, start + q));
-        S += (double)expf((float)(sc - m));
-      }
-      S = team_sum<T>(S, tmask);
-      wr.m = m;
-      wr.inv_s = (float)(1.0 / S);
-    }
+    };
     float out[V];
     row_segments<V, G, false>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
-                              s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out);
+                              s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out, stats);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
   // no CTA may exit with bulk copies still writing its shared memory
