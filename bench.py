@@ -114,7 +114,7 @@ def ncu_traffic(workload):
             d = json.load(open(p))
         except Exception:
             continue
-        if d.get("workload") == workload and d.get("dram_bytes_per_launch"):
+        if isinstance(d, dict) and d.get("workload") == workload and d.get("dram_bytes_per_launch"):
             best = d["dram_bytes_per_launch"]
     return best
 
