@@ -48,13 +48,14 @@ def lib():
         L.orc_build_csr.argtypes = [I, I, P, P, P, ctypes.c_int, ctypes.c_float, P, P, P, I, P]
         L.orc_sym_norm.argtypes = [I, P, P, P, P, P, P]
         L.orc_spmm.argtypes = [I, I, P, P, P, P, I, I, P, P, I]
+        L.orc_gspmm.argtypes = [I, I, P, P, P, P, I, I, ctypes.c_int, P, I]
         L.orc_edge_softmax.argtypes = [I, I, P, I, P, P]
         L.orc_gat_scores.argtypes = [I, I, P, P, I, P, P, ctypes.c_double, P]
         L.orc_multihead_spmm.argtypes = [I, I, P, P, I, P, P, I, I, P, P, I]
         L.orc_attn_project.argtypes = [I, I, I, I, P, I, P, P, P, P, P, P]
         L.orc_partition_rows.argtypes = [I, P, I, P]
         L.orc_csr_slice.argtypes = [I, P, P, P, P, I, I, I, P, P, P]
-        for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_edge_softmax", "orc_gat_scores",
+        for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_edge_softmax", "orc_gat_scores",
                   "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice"):
             getattr(L, f).restype = ctypes.c_int
     return _lib
@@ -140,6 +141,24 @@ def spmm(row_ptr, col, a, x, f=None, r0=0, r1=None, want_cond=True):
     cond = np.zeros_like(y) if want_cond else None
     _chk(lib().orc_spmm(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], _p(y), _p(cond), y.shape[1]))
     return y[:, :f], (cond[:, :f] if want_cond else None)
+
+
+REDUCE = {"sum": 0, "mean": 1, "max": 2, "min": 3}
+
+
+def gspmm(row_ptr, col, a, x, reduce="sum", f=None, r0=0, r1=None):
+    """y fp64 [r1-r0, f] = phi_e psi(a_e, x[col_e]) (oracle.c §3b); a None -> copy."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    a = _c(a, np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n = row_ptr.size - 1
+    r1 = n if r1 is None else r1
+    f = x.shape[1] if f is None else f
+    y = np.zeros((r1 - r0, max(f, 1)), np.float64)
+    _chk(lib().orc_gspmm(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], REDUCE[reduce], _p(y),
+                         y.shape[1]))
+    return y[:, :f]
 
 
 def edge_softmax(row_ptr, logits, heads=1, r0=0, r1=None):

@@ -180,6 +180,39 @@ int orc_spmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col,
 }
 
 /* ---------------------------------------------------------------------------
+ * 3b. GSpMM with a selectable reduce operator (NEXT-2).
+ *    P:640-646 [§4.1 Eq. formula:1: h_u = phi(psi(h_v, h_e)); "users could
+ *    choose the reduce or compute operator"], P:648 ["min and max as reduce
+ *    functions"], P:1355 Fig. gspmm ["mean and sum as reduce functions"];
+ *    an empty row gives 0 for every reduce; mean divides
+ *    by the number of entries in the row.
+ *    reduce: 0 sum, 1 mean, 2 max, 3 min.  psi: a == NULL -> copy (h_v),
+ *    else multiply (a_e * h_v), formed in fp64 (exact for fp32 operands).
+ * ------------------------------------------------------------------------- */
+int orc_gspmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *a,
+              const float *x, int64_t f, int64_t ldx, int reduce, double *y, int64_t ldy) {
+  if (r0 < 0 || r1 < r0 || f < 0 || ldx < f || ldy < f || !row_ptr || !x || !y || reduce < 0 || reduce > 3)
+    return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u) {
+    double *yu = y + (u - r0) * ldy;
+    const int64_t b = row_ptr[u], e1 = row_ptr[u + 1];
+    for (int64_t k = 0; k < f; ++k) {
+      double acc = 0.0;
+      for (int64_t e = b; e < e1; ++e) {
+        const double v = (a ? a[e] : 1.0) * (double)x[(int64_t)col[e] * ldx + k];
+        if (reduce <= 1) acc += v;
+        else if (e == b) acc = v;
+        else if (reduce == 2 && v > acc) acc = v;
+        else if (reduce == 3 && v < acc) acc = v;
+      }
+      if (reduce == 1 && e1 > b) acc /= (double)(e1 - b);
+      yu[k] = (e1 > b) ? acc : 0.0;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * 4. Edge-wise softmax, per head.
  *    P:653-656 [§4.1: alpha'_uv = exp(alpha_uv) / sum_{w in N(u)} exp(alpha_uw);
  *    "first apply the scan to find the max value ... subtract this maximum ...

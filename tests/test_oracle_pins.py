@@ -428,3 +428,44 @@ def test_slice_gathered_layout_equals_global(P):
         rp, co, vo = orc.csr_slice(g.row_ptr, g.col, a32, b, r, npad)
         yl, _ = orc.spmm(rp, co, vo.astype(np.float64), xg)
         np.testing.assert_array_equal(yl, yg[b[r]:b[r + 1]])
+
+
+# ---------------------------------------------------------------------------
+# 3b. GSpMM reduce variants (oracle.c §3b, NEXT-2)
+# ---------------------------------------------------------------------------
+
+def test_gspmm_spec_example(golden):
+    """row 0 -> {1,2}, h=[[1,2],[3,4],[5,6]]: sum [8,10], mean [4,5],
+    max [5,6] (min [3,4] by the same hand evaluation); empty rows give zeros."""
+    case = golden["spec_examples"]["gspmm_reduce"][0]
+    h = np.array(case["h"], np.float32)
+    for red in ("sum", "mean", "max", "min"):
+        y = orc.gspmm(case["row_ptr"], case["col"], None, h, red)
+        np.testing.assert_array_equal(y, np.array(case[red], np.float64), err_msg=red)
+
+
+def test_gspmm_vs_dense_numpy():
+    """Against NumPy reductions over each row's gathered rows (masked dense),
+    with and without edge weights; sum equals orc.spmm exactly."""
+    rng = np.random.default_rng(21)
+    for t in range(60):
+        n = int(rng.integers(1, 50))
+        m = int(rng.integers(0, 3 * n + 1))
+        src = rng.integers(0, n, m)
+        dst = rng.integers(0, n, m)
+        g = orc.build_csr(n, src, dst, None, bool(t % 2), 0.0 if t % 3 == 0 else 1.0)
+        w = uniform(g.nnz, seed=t, low=-2, high=2).astype(np.float64) if t % 4 else None
+        f = int(rng.integers(1, 9))
+        x = uniform((n, f), seed=100 + t)
+        for red in ("sum", "mean", "max", "min"):
+            y = orc.gspmm(g.row_ptr, g.col, w, x, red)
+            for u in range(n):
+                b, e = g.row_ptr[u], g.row_ptr[u + 1]
+                if b == e:
+                    assert np.all(y[u] == 0)
+                    continue
+                vals = (w[b:e, None] if w is not None else 1.0) * x[g.col[b:e]].astype(np.float64)
+                ref = {"sum": vals.sum(0), "mean": vals.mean(0), "max": vals.max(0), "min": vals.min(0)}[red]
+                np.testing.assert_allclose(y[u], ref, rtol=1e-13, atol=1e-15, err_msg=red)
+        ys, _ = orc.spmm(g.row_ptr, g.col, w, x)
+        np.testing.assert_array_equal(orc.gspmm(g.row_ptr, g.col, w, x, "sum"), ys)
