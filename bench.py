@@ -386,6 +386,24 @@ def main():
                       "h2d_bytes_per_step": int(xh.numel() * 4) * world, "d2h_bytes_per_step": int(yh.numel() * 4) * world,
                       "api": "RowPartitionedSpMM (gsp_csr_slice + NCCL all-gather + gsp_spmm), pinned host shards"}
 
+    # --- secondary: GSpMM reduce variants on the same graph (NEXT-2) ---
+    if not use_dist and not args.no_gat:
+        red = {}
+        for r_ in ("mean", "max", "min"):
+            ts = []
+            for i in range(args.warmup + 10):
+                flush.zero_()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                G.gsp_gspmm(gn, x, r_, f=f, y=y)
+                a1.record()
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    ts.append(a0.elapsed_time(a1))
+            red[r_] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3)}
+        out.setdefault("secondary", {})["C4_gspmm_reduce"] = red
+
     # --- secondary: fused GAT aggregate on the Flickr-shaped graph (C3) ---
     if not use_dist and not args.no_gat:
         c3 = CONFIGS["C3"]
@@ -413,12 +431,12 @@ def main():
                 tg.append(a1.elapsed_time(a2))
         tgm = float(np.mean(tg))
         gb = gat_alg_bytes(c3.n, g3.nnz, H, D)
-        out["secondary"] = {"C3_gat": {
+        out.setdefault("secondary", {})["C3_gat"] = {
             "workload": c3.name, "n": c3.n, "nnz": g3.nnz, "heads": H, "d": D,
             "aggregate_ms": tgm, "attn_project_ms": float(np.mean(tp)),
             "GE/s": g3.nnz * H * D / (tgm * 1e-3),
             "alg_GB/s": gb / (tgm * 1e-3) / 1e9, "frac_of_hbm_peak": gb / (tgm * 1e-3) / 1e9 / peak,
-            "launches": "one engine_kernel<4,16,WeightGat> per aggregate (softmax statistics fused)"}}
+            "launches": "one engine_kernel<4,16,WeightGat> per aggregate (softmax statistics fused)"}
 
     # --- cpu_baseline: the oracle as it stands, bounded sample, rank 0 at N=1 ---
     if not use_dist and rank == 0 and not args.no_cpu_baseline:

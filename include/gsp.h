@@ -147,6 +147,21 @@ gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, 
 gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
                     int64_t ldy, gsp_stream stream);
 
+/* ---------------------------------------------------------------------------
+ * GSpMM with a selectable reduce operator phi (NEXT-2).
+ * P:640-646 (§4.1 Eq. formula:1, "users could choose the reduce or compute
+ * operator"), P:648 ("min and max as reduce functions"), P:1355 (Fig. gspmm:
+ * "mean and sum as reduce functions").  psi is multiply by a->val, or copy
+ * when a->val is NULL.  y[u,k] = phi over row u of psi(x[col_e,k], val_e):
+ *   GSP_REDUCE_SUM   sum (== gsp_spmm)
+ *   GSP_REDUCE_MEAN  sum / (number of entries in row u)
+ *   GSP_REDUCE_MAX / GSP_REDUCE_MIN  row-wise extremum; exact (no rounding
+ *                    beyond the fp32 product), so bit-identical to any order
+ * Empty rows give 0 for every operator.  Arguments as gsp_spmm. */
+typedef enum { GSP_REDUCE_SUM = 0, GSP_REDUCE_MEAN = 1, GSP_REDUCE_MAX = 2, GSP_REDUCE_MIN = 3 } gsp_reduce;
+gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_t f, int64_t ldx, float *y,
+                     int64_t ldy, gsp_stream stream);
+
 /* Tuning knobs for gsp_spmm_ex (0 = automatic).  Results are bitwise
  * identical for every setting (the summation order does not depend on them). */
 typedef struct {

@@ -32,7 +32,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
 EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
-           "gsp_spmm_plan_info")
+           "gsp_spmm_plan_info", "gsp_gspmm")
 
 
 class GspError(RuntimeError):
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
             "gsp_sym_normalize": [CP, P, P, P],
             "gsp_spmm": [CP, P, I, I, P, I, P],
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
+            "gsp_gspmm": [CP, ctypes.c_int, P, I, I, P, I, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -221,6 +222,22 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
 
 
 gsp_spmm_ex = gsp_spmm
+
+REDUCE = {"sum": 0, "mean": 1, "max": 2, "min": 3}
+
+
+def gsp_gspmm(a: CSR, x: torch.Tensor, reduce: str = "sum", f: Optional[int] = None,
+              y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """GSpMM with reduce in {sum, mean, max, min}; psi = mul by a.val (copy if None)."""
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    if y is None:
+        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    _check(lib().gsp_gspmm(ctypes.byref(v), REDUCE[reduce], _ptr(x), f, ldx, _ptr(y), ldy, _stream(stream)),
+           "gsp_gspmm")
+    return y
 
 
 def gsp_spmm_plan_info(a: CSR, x: torch.Tensor, f: Optional[int] = None, slab_cols: int = 0, block_nnz: int = 0):

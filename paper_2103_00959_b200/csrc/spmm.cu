@@ -101,7 +101,7 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
 }
 
 static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
-                                   float *y, int64_t ldy, cudaStream_t s) {
+                                   float *y, int64_t ldy, gsp_reduce red, cudaStream_t s) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -118,12 +118,25 @@ static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, cons
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
   gsp_status st = engine_ldxv(p, L, a->n_cols, ldx);
   if (st) return st;
-  return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
+  p.mean = red == GSP_REDUCE_MEAN;
+  switch (red) {
+    case GSP_REDUCE_SUM:
+    case GSP_REDUCE_MEAN:
+      return a->val ? engine_launch(L, p, WeightVal{a->val}, s) : engine_launch(L, p, WeightOne{}, s);
+    case GSP_REDUCE_MAX:
+      return a->val ? engine_launch<WeightVal, RedMax>(L, p, WeightVal{a->val}, s)
+                    : engine_launch<WeightOne, RedMax>(L, p, WeightOne{}, s);
+    case GSP_REDUCE_MIN:
+      return a->val ? engine_launch<WeightVal, RedMin>(L, p, WeightVal{a->val}, s)
+                    : engine_launch<WeightOne, RedMin>(L, p, WeightOne{}, s);
+  }
+  return fail(GSP_ERR_INVALID_ARG, "bad reduce op %d", (int)red);
 }
 
 static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
-                            const gsp_spmm_opts *opts, cudaStream_t s, const char *fn) {
+                            const gsp_spmm_opts *opts, gsp_reduce red, cudaStream_t s, const char *fn) {
   clear_detail();
+  if (red < GSP_REDUCE_SUM || red > GSP_REDUCE_MIN) return fail(GSP_ERR_INVALID_ARG, "%s: bad reduce op", fn);
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
   if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
@@ -135,8 +148,8 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
   SpmmPlan P;
   if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
-  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, s))) return st;
-  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, s);
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, red, s))) return st;
+  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, red, s);
   return st;
 }
 
@@ -146,12 +159,17 @@ using namespace gsp;
 
 extern "C" gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
                                gsp_stream stream) {
-  return spmm_impl(a, x, f, ldx, y, ldy, nullptr, cs(stream), "gsp_spmm");
+  return spmm_impl(a, x, f, ldx, y, ldy, nullptr, GSP_REDUCE_SUM, cs(stream), "gsp_spmm");
+}
+
+extern "C" gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_t f, int64_t ldx, float *y,
+                                int64_t ldy, gsp_stream stream) {
+  return spmm_impl(a, x, f, ldx, y, ldy, nullptr, reduce, cs(stream), "gsp_gspmm");
 }
 
 extern "C" gsp_status gsp_spmm_ex(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
                                   const gsp_spmm_opts *opts, gsp_stream stream) {
-  return spmm_impl(a, x, f, ldx, y, ldy, opts, cs(stream), "gsp_spmm_ex");
+  return spmm_impl(a, x, f, ldx, y, ldy, opts, GSP_REDUCE_SUM, cs(stream), "gsp_spmm_ex");
 }
 
 extern "C" gsp_status gsp_spmm_plan_info(const gsp_csr *a, const float *x, int64_t f, int64_t ldx,

@@ -161,6 +161,28 @@ struct Window {
   }
 };
 
+// ---------------------------------------------------------- reduce policies
+// phi of Eq. formula:1: sum (also mean = sum / row count) or the
+// row-wise max / min of psi(x, w) = w * x ("min and max as reduce").
+struct RedSum {
+  static constexpr bool kSum = true;
+  static __device__ __forceinline__ float init() { return 0.0f; }
+  static __device__ __forceinline__ float step(float acc, float w, float x) { return fmaf(w, x, acc); }
+  static __device__ __forceinline__ float comb(float a, float b) { return a + b; }
+};
+struct RedMax {
+  static constexpr bool kSum = false;
+  static __device__ __forceinline__ float init() { return -INFINITY; }
+  static __device__ __forceinline__ float step(float acc, float w, float x) { return fmaxf(acc, w * x); }
+  static __device__ __forceinline__ float comb(float a, float b) { return fmaxf(a, b); }
+};
+struct RedMin {
+  static constexpr bool kSum = false;
+  static __device__ __forceinline__ float init() { return INFINITY; }
+  static __device__ __forceinline__ float step(float acc, float w, float x) { return fminf(acc, w * x); }
+  static __device__ __forceinline__ float comb(float a, float b) { return fminf(a, b); }
+};
+
 // ---------------------------------------------------------- weight functors
 // Each functor provides Row row(int64 r, int head) and Row::w(e, c): the
 // weight of CSR entry e (column c) for this group's head.
@@ -251,6 +273,7 @@ struct EngineParams {
   const float *stage_val;  // val array to stage in smem (NULL: none)
   int stage;               // 1: stage col (and stage_val) in shared memory
   int win_cap;             // window capacity in entries (multiple of 4)
+  int mean;                // GSpMM mean: divide the row sum by the row's entry count
 };
 
 // Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
@@ -286,7 +309,7 @@ __device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor b
 
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
-template <int V, int G, class Row, bool kFull, class Pre>
+template <int V, int G, class Row, class R, bool kFull, class Pre>
 __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
                                            const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
                                            int sg, float (&a)[Team<G>::NACC][V], Pre &&pre) {
@@ -319,7 +342,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       if (kFull || j < cnt) {
         const float ww = Row::kUnit ? 1.0f : sw[j];
 #pragma unroll
-        for (int i = 0; i < V; ++i) a[t % NACC][i] = fmaf(ww, xv[u][i], a[t % NACC][i]);
+        for (int i = 0; i < V; ++i) a[t % NACC][i] = R::step(a[t % NACC][i], ww, xv[u][i]);
       }
     }
   }
@@ -337,7 +360,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 // Metadata: segments inside the TMA-staged window are read from it directly;
 // other segments (hub rows beyond the window, unstaged arrays) and computed
 // weights go through the team's 32-entry shared scratch (tc, tw).
-template <int V, int G, bool kLong, class Row, class Pro>
+template <int V, int G, bool kLong, class R, class Row, class Pro>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
@@ -347,7 +370,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL;
   float acc1[V], acc2[V];
 #pragma unroll
-  for (int i = 0; i < V; ++i) acc1[i] = acc2[i] = 0.0f;
+  for (int i = 0; i < V; ++i) acc1[i] = acc2[i] = R::init();
   int n1 = 0;
   for (int64_t s = s_begin; s < s_end; ++s) {
     const int64_t e0 = start + s * kSeg;
@@ -397,9 +420,9 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
-      for (int i = 0; i < V; ++i) a[q][i] = 0.0f;
-    if (cnt == kSeg) seg_gather<V, G, Row, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
-    else seg_gather<V, G, Row, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
+      for (int i = 0; i < V; ++i) a[q][i] = R::init();
+    if (cnt == kSeg) seg_gather<V, G, Row, R, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
+    else seg_gather<V, G, Row, R, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
     if (scratch) __syncwarp(tmask);  // scratch is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
@@ -407,32 +430,43 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       if (SPR == 1) {
-        seg[i] = (a[0][i] + a[1 % NACC][i]) + (a[2 % NACC][i] + a[3 % NACC][i]);
+        seg[i] = R::comb(R::comb(a[0][i], a[1 % NACC][i]), R::comb(a[2 % NACC][i], a[3 % NACC][i]));
       } else if (SPR == 2) {
-        const float b0 = a[0][i] + __shfl_xor_sync(tmask, a[0][i], G, T);
-        const float b1 = a[NACC - 1][i] + __shfl_xor_sync(tmask, a[NACC - 1][i], G, T);
-        seg[i] = b0 + b1;
+        const float b0 = R::comb(a[0][i], __shfl_xor_sync(tmask, a[0][i], G, T));
+        const float b1 = R::comb(a[NACC - 1][i], __shfl_xor_sync(tmask, a[NACC - 1][i], G, T));
+        seg[i] = R::comb(b0, b1);
       } else {
-        const float b = a[0][i] + __shfl_xor_sync(tmask, a[0][i], G, T);
-        seg[i] = b + __shfl_xor_sync(tmask, b, 2 * G, T);
+        const float b = R::comb(a[0][i], __shfl_xor_sync(tmask, a[0][i], G, T));
+        seg[i] = R::comb(b, __shfl_xor_sync(tmask, b, 2 * G, T));
       }
     }
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc1[i] += seg[i];
+    for (int i = 0; i < V; ++i) acc1[i] = R::comb(acc1[i], seg[i]);
     if (kLong && ++n1 == kSeg) {
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        acc2[i] += acc1[i];
-        acc1[i] = 0.0f;
+        acc2[i] = R::comb(acc2[i], acc1[i]);
+        acc1[i] = R::init();
       }
       n1 = 0;
     }
   }
 #pragma unroll
-  for (int i = 0; i < V; ++i) out[i] = kLong ? acc2[i] + acc1[i] : acc1[i];
+  for (int i = 0; i < V; ++i) out[i] = kLong ? R::comb(acc2[i], acc1[i]) : acc1[i];
 }
 
-template <int V, int G, class W>
+// epilogue: empty rows give 0 for every reduce; mean divides by the
+// row's entry count
+template <class R, int V>
+__device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    if (d == 0) out[i] = 0.0f;
+    else if (R::kSum && mean) out[i] = out[i] / (float)d;
+  }
+}
+
+template <int V, int G, class W, class R>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const EngineParams p, const W wf) {
   using TM = Team<G>;
   constexpr int T = TM::T;
@@ -569,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G, true>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
+      row_segments<V, G, true, R>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
                                s_tc[team], s_tw[team], nullptr, 0, part, [] {});
       if (sg == 0) {
 #pragma unroll
@@ -581,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     for (int stride = 1; stride < kVirt; stride <<= 1) {
       for (int q = tid; q < (kVirt / (2 * stride)) * SW; q += kThreads) {
         const int v = (q / SW) * 2 * stride, cidx = q % SW;
-        s_part[v * SW + cidx] += s_part[(v + stride) * SW + cidx];
+        s_part[v * SW + cidx] = R::comb(s_part[v * SW + cidx], s_part[(v + stride) * SW + cidx]);
       }
       __syncthreads();
     }
@@ -589,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
       float out[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) out[i] = s_part[gl * V + i];
+      finish_row<R, V>(out, d, p.mean);
       store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
     }
     __syncthreads();
@@ -629,8 +664,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
       }
     };
     float out[V];
-    row_segments<V, G, false>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask, s_tc[team],
-                              s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out, stats);
+    row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask,
+                                 s_tc[team], s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out, stats);
+    finish_row<R, V>(out, d, p.mean);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
   // no CTA may exit with bulk copies still writing its shared memory
@@ -669,9 +705,10 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.stage = (nnz > 0 && aligned16(col)) ? 1 : 0;
   p.stage_val = (p.stage && val && aligned16(val)) ? val : nullptr;
   p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
+  p.mean = 0;
 }
 
-template <int V, int G, class W>
+template <int V, int G, class W, class R>
 gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   const int64_t grid = L.nslab * L.nblk;
   if (grid <= 0) return GSP_OK;
@@ -682,36 +719,36 @@ gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const 
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || granted[dev] < (int)smem) {
-      if (cudaFuncSetAttribute(engine_kernel<V, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      if (cudaFuncSetAttribute(engine_kernel<V, G, W, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
         return check_launch("cudaFuncSetAttribute(engine_kernel)");
       if (dev >= 0 && dev < 64) granted[dev] = (int)smem;
     }
   }
-  engine_kernel<V, G, W><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
+  engine_kernel<V, G, W, R><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
   return check_launch("engine_kernel");
 }
 
-template <int V, class W>
+template <int V, class W, class R>
 gsp_status engine_launch_v(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   switch (L.G) {
-    case 1: return engine_launch_vg<V, 1>(L, p, w, s);
-    case 2: return engine_launch_vg<V, 2>(L, p, w, s);
-    case 4: return engine_launch_vg<V, 4>(L, p, w, s);
-    case 8: return engine_launch_vg<V, 8>(L, p, w, s);
-    case 16: return engine_launch_vg<V, 16>(L, p, w, s);
-    case 32: return engine_launch_vg<V, 32>(L, p, w, s);
+    case 1: return engine_launch_vg<V, 1, W, R>(L, p, w, s);
+    case 2: return engine_launch_vg<V, 2, W, R>(L, p, w, s);
+    case 4: return engine_launch_vg<V, 4, W, R>(L, p, w, s);
+    case 8: return engine_launch_vg<V, 8, W, R>(L, p, w, s);
+    case 16: return engine_launch_vg<V, 16, W, R>(L, p, w, s);
+    case 32: return engine_launch_vg<V, 32, W, R>(L, p, w, s);
   }
   return fail(GSP_ERR_UNSUPPORTED, "bad group width %d", L.G);
 }
 
-template <class W>
+template <class W, class R = RedSum>
 gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   switch (L.V) {
-    case 8: return engine_launch_vg<8, 32>(L, p, w, s);
-    case 4: return engine_launch_v<4>(L, p, w, s);
-    case 2: return engine_launch_v<2>(L, p, w, s);
-    case 1: return engine_launch_v<1>(L, p, w, s);
+    case 8: return engine_launch_vg<8, 32, W, R>(L, p, w, s);
+    case 4: return engine_launch_v<4, W, R>(L, p, w, s);
+    case 2: return engine_launch_v<2, W, R>(L, p, w, s);
+    case 1: return engine_launch_v<1, W, R>(L, p, w, s);
   }
   return fail(GSP_ERR_UNSUPPORTED, "bad vector width %d", L.V);
 }

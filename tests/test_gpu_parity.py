@@ -330,3 +330,32 @@ def test_partition_slice_bit_exact_and_invariant(built, P):
         yl = host(G.gsp_spmm(sl, dev(xg)))
         # partition invariance: bitwise equal to the single-GPU result
         np.testing.assert_array_equal(yl, y_global[bref[r]:bref[r + 1]])
+
+
+# ---------------------------------------------------------------- NEXT-2: GSpMM reduce variants
+
+@pytest.mark.parametrize("reduce", ["sum", "mean", "max", "min"])
+@pytest.mark.parametrize("f", [1, 5, 33, 128, 300])
+def test_gspmm_reduce_parity(built, reduce, f):
+    """max / min are exact (monotone rounding of exact products) -> bit-equal to
+    the oracle on the same fp32 weights; sum / mean within 1e-5*cond(/deg)+1e-6."""
+    for name in ("isolated-nofill", "multi1", "multi4", "er300-weighted", "cl4000", "hubs", "star100k"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        x = features(go.n, f, (f + 3) // 4 * 4, seed=f + 11)
+        for g, a in ((gn, a32.astype(np.float64)), (gn.with_val(None), None)):
+            y = host(G.gsp_gspmm(g, dev(x), reduce, f=f))
+            yref = orc.gspmm(go.row_ptr, go.col, a, x, reduce, f=f)
+            if reduce in ("max", "min"):
+                np.testing.assert_array_equal(y, yref.astype(np.float32), err_msg=f"{name} {reduce} f={f}")
+            else:
+                _, cond = orc.spmm(go.row_ptr, go.col, a, x, f=f)
+                if reduce == "mean":
+                    cnt = np.maximum(np.diff(go.row_ptr), 1)[:, None]
+                    cond = cond / cnt
+                assert_within(y, yref, cond, what=f"{name} {reduce} f={f}")
+
+
+def test_gspmm_sum_equals_spmm_bitwise(built):
+    go, gg, _, gn = built["rmat3000"]
+    x = dev(features(go.n, 300, seed=3))
+    assert torch.equal(G.gsp_gspmm(gn, x, "sum"), G.gsp_spmm(gn, x))
