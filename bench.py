@@ -202,7 +202,6 @@ def main():
     ap.add_argument("--cpu-budget-ge", type=float, default=1.5e9)
     ap.add_argument("--ref-budget-ge", type=float, default=0.25e9)
     ap.add_argument("--sweep", default="", help="comma list of slab widths to time (diagnostic)")
-    ap.add_argument("--sweep-warm", action="store_true", help="also time the per-slab L2 warm-up variant")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -323,19 +322,19 @@ def main():
 
     if not use_dist and args.sweep:
         sw = {}
-        for sc, wm in [(int(v), w_) for v in args.sweep.split(",") for w_ in ((0, 1) if args.sweep_warm else (0,))]:
+        for sc in [int(v) for v in args.sweep.split(",")]:
             ts = []
             for i in range(args.warmup + 10):
                 flush.zero_()
                 a0 = torch.cuda.Event(enable_timing=True)
                 a1 = torch.cuda.Event(enable_timing=True)
                 a0.record()
-                G.gsp_spmm(gn, x, f=f, y=y, slab_cols=sc, warm=wm)
+                G.gsp_spmm(gn, x, f=f, y=y, slab_cols=sc)
                 a1.record()
                 torch.cuda.synchronize()
                 if i >= args.warmup:
                     ts.append(a0.elapsed_time(a1))
-            sw[str(sc) + ("w" if wm else "")] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3),
+            sw[str(sc)] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3),
                            "alg_GB/s": spmm_alg_bytes(n, nnz, f) / (np.mean(ts) * 1e-3) / 1e9}
         out["sweep_slab_cols"] = sw
     # --- e2e: host buffers, H2D + kernel + D2H inside the timed region ---

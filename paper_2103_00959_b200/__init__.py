@@ -204,7 +204,7 @@ def gsp_sym_normalize(a: CSR, in_place: bool = False, stream=None) -> CSR:
 # ---------------------------------------------------------------------------
 
 def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch.Tensor] = None, stream=None,
-             slab_cols: int = 0, block_nnz: int = 0, warm: int = 0) -> torch.Tensor:
+             slab_cols: int = 0, block_nnz: int = 0) -> torch.Tensor:
     """Y = A X (gsp.h a3).  x: [n_cols, >= f] fp32 (row stride = ld)."""
     x, ldx = _mat(x, "x")
     f = x.shape[1] if f is None else int(f)
@@ -212,9 +212,8 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
         y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
     y, ldy = _mat(y, "y")
     v = a.view()
-    if slab_cols or block_nnz or warm:
+    if slab_cols or block_nnz:
         o = gsp_spmm_opts(slab_cols, block_nnz)
-        o.reserved[0] = warm
         st = lib().gsp_spmm_ex(ctypes.byref(v), _ptr(x), f, ldx, _ptr(y), ldy, ctypes.byref(o), _stream(stream))
         _check(st, "gsp_spmm_ex")
     else:

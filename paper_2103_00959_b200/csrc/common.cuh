@@ -116,9 +116,4 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 #endif
 }
 
-// TMA-driven L2 prefetch of a contiguous range (16-byte aligned, size % 16 == 0)
-__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
 }  // namespace gsp

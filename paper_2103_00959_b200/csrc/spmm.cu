@@ -100,15 +100,8 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
   return GSP_OK;
 }
 
-// L2 warm-up of one column slab of x: one TMA bulk prefetch per row (the
-// slab's bytes of that row), so the slab's random gathers that follow hit L2.
-__global__ void l2_warm_kernel(const float *__restrict__ x, int64_t n, int64_t ldx, uint32_t bytes) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-    bulk_prefetch_l2(x + r * ldx, bytes);
-}
-
 static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
-                                   float *y, int64_t ldy, gsp_reduce red, int warm, cudaStream_t s) {
+                                   float *y, int64_t ldy, gsp_reduce red, cudaStream_t s) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -126,25 +119,6 @@ static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, cons
   gsp_status st = engine_ldxv(p, L, a->n_cols, ldx);
   if (st) return st;
   p.mean = red == GSP_REDUCE_MEAN;
-  if (warm && L.V >= 4 && L.nslab > 0) {
-    // per-slab launches, each preceded by an L2 warm-up of its slab of x
-    EngineLaunch L1 = L;
-    L1.nslab = 1;
-    for (int64_t sl = 0; sl < L.nslab; ++sl) {
-      const int64_t c0 = sl * L.slab_cols, w = std::min<int64_t>(L.slab_cols, f - c0);
-      l2_warm_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(a->n_cols, 256), 1184)), 256, 0, s>>>(
-          x + c0, a->n_cols, ldx, (uint32_t)(((w + 3) & ~int64_t(3)) * 4));
-      if ((st = check_launch("l2_warm"))) return st;
-      EngineParams q = p;
-      q.x = x + c0;
-      q.y = y + c0;
-      q.f = w;
-      q.y_vec_ok = engine_y_vec_ok(L1, q.y, ldy);
-      st = a->val ? engine_launch(L1, q, WeightVal{a->val}, s) : engine_launch(L1, q, WeightOne{}, s);
-      if (st) return st;
-    }
-    return GSP_OK;
-  }
   switch (red) {
     case GSP_REDUCE_SUM:
     case GSP_REDUCE_MEAN:
@@ -174,10 +148,8 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
   SpmmPlan P;
   if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
-  // reserved[0] (experimental): 1 = per-slab launches, each after an L2 warm-up of its slab
-  const int warm = (opts && opts->reserved[0] == 1 && red == GSP_REDUCE_SUM) ? 1 : 0;
-  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, red, warm, s))) return st;
-  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, red, warm, s);
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, red, s))) return st;
+  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, red, s);
   return st;
 }
 
