@@ -261,6 +261,13 @@ gsp_status gsp_csr_slice(const gsp_csr *a, const int64_t *row_bounds, int32_t pa
                          float *val_out, gsp_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * Measurement helper (not part of the method): one launch that streams
+ * `bytes` of device memory `iters` times through L2 (ld.global.cg), used by
+ * bench.py to measure the L2 read ceiling live.  sink: device fp32
+ * [8 * SM count], never read. */
+gsp_status gsp_probe_l2_read(const void *buf, size_t bytes, int32_t iters, float *sink, gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
  * Misc. */
 const char *gsp_status_string(gsp_status st);
 const char *gsp_last_error_detail(void); /* thread-local; "" when none */

@@ -32,7 +32,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
 EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
-           "gsp_spmm_plan_info", "gsp_gspmm")
+           "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read")
 
 
 class GspError(RuntimeError):
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
             "gsp_spmm": [CP, P, I, I, P, I, P],
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
             "gsp_gspmm": [CP, ctypes.c_int, P, I, I, P, I, P],
+            "gsp_probe_l2_read": [P, ctypes.c_size_t, I32, P, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -357,6 +358,12 @@ def gsp_csr_slice(a: CSR, bounds, rank: int, rows_padded: int, stream=None) -> C
     _check(lib().gsp_csr_slice(ctypes.byref(v), hb, parts, rank, rows_padded, _ptr(rp), _ptr(col), _ptr(val),
                                _stream(stream)), "gsp_csr_slice")
     return CSR(rp, col[:k], None if val is None else val[:k], parts * rows_padded)
+
+
+def gsp_probe_l2_read(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None):
+    """Measurement helper: stream buf (L2-resident size) iters times."""
+    _check(lib().gsp_probe_l2_read(_ptr(buf), buf.numel() * buf.element_size(), iters, _ptr(sink), _stream(stream)),
+           "gsp_probe_l2_read")
 
 
 def version() -> int:

@@ -256,6 +256,7 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   p.head_dim = d;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
+  p.hpt = engine_hpt(L, d);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   WeightGat w{el, er, alpha_out, negative_slope, heads};
   return engine_launch(L, p, w, s);

@@ -20,15 +20,25 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
   int64_t SW = 0;
   if (head_dim > 0) {
     while (V > 1 && head_dim % V) V /= 2;
+    const int64_t heads = f / head_dim;
     if (slab_req > 0) {
       SW = slab_req;
-      if (SW % V || head_dim % SW || SW / V > 32 || (SW / V & (SW / V - 1)))
-        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must divide head_dim %lld and be V*2^k <= 32V", slab_req,
-                    (long long)head_dim);
+      const bool whole = SW % head_dim == 0 && (SW / head_dim) <= kMaxHpt && heads % (SW / head_dim) == 0;
+      if (SW % V || SW / V > 32 || (SW / V & (SW / V - 1)) || !(head_dim % SW == 0 || whole))
+        return fail(GSP_ERR_INVALID_ARG, "slab_cols %d must divide head_dim %lld or be up to %d whole heads",
+                    slab_req, (long long)head_dim, kMaxHpt);
     } else {
-      int64_t G = 32;
-      while (G > 1 && (head_dim % (G * V) || G * V > 128)) G /= 2;
-      SW = G * V;
+      // prefer a slab of hpt whole heads (hpt | heads, hpt <= kMaxHpt, <= 128 columns); else slabs inside a head
+      SW = 0;
+      for (int64_t hpt = std::min<int64_t>(kMaxHpt, heads); hpt >= 1 && !SW; --hpt) {
+        const int64_t sw = hpt * head_dim, g = sw / V;
+        if (heads % hpt == 0 && sw <= 128 && sw % V == 0 && g >= 1 && g <= 32 && (g & (g - 1)) == 0) SW = sw;
+      }
+      if (!SW) {
+        int64_t G = 32;
+        while (G > 1 && (head_dim % (G * V) || G * V > 128)) G /= 2;
+        SW = G * V;
+      }
     }
   } else {
     if (slab_req > 0) {
@@ -226,6 +236,7 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   p.head_dim = d;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
+  p.hpt = engine_hpt(L, d);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));
 }

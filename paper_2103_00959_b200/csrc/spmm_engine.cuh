@@ -48,6 +48,7 @@ constexpr int kHub = 512;          // degree above which a row is CTA-cooperativ
 constexpr int kVirt = 16;          // virtual ranges of a hub row
 constexpr int kMaxHubPerBlock = 64;
 constexpr int kStageChunks = 4;   // TMA bulk-copy chunks of the CSR window
+constexpr int kMaxHpt = 4;        // heads per team (multi-head modes)
 #ifndef GSP_MIN_BLOCKS
 #define GSP_MIN_BLOCKS 4
 #endif
@@ -195,17 +196,17 @@ struct WeightVal {  // SpMM with A's values
   struct Row {
     static constexpr bool kUnit = false, kComputed = false, kStagedVal = true;
     const float *val;
-    __device__ __forceinline__ float w(int64_t e, int /*c*/) const { return __ldcs(val + e); }
+    __device__ __forceinline__ float w(int64_t e, int /*c*/, int /*hh*/) const { return __ldcs(val + e); }
   };
-  __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{val}; }
+  __device__ __forceinline__ Row row(int64_t, int, bool, void *) const { return Row{val}; }
 };
 
 struct WeightOne {  // SpMM with val == NULL: psi = copy
   struct Row {
     static constexpr bool kUnit = true, kComputed = false, kStagedVal = false;
-    __device__ __forceinline__ float w(int64_t, int) const { return 1.0f; }
+    __device__ __forceinline__ float w(int64_t, int, int) const { return 1.0f; }
   };
-  __device__ __forceinline__ Row row(int64_t, int, bool) const { return Row{}; }
+  __device__ __forceinline__ Row row(int64_t, int, bool, void *) const { return Row{}; }
 };
 
 struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
@@ -214,10 +215,10 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   struct Row {
     static constexpr bool kUnit = false, kComputed = false, kStagedVal = false;
     const float *alpha;
-    int heads, h;
-    __device__ __forceinline__ float w(int64_t e, int) const { return __ldcs(alpha + e * heads + h); }
+    int heads, h;  // h: first head of the team's slab
+    __device__ __forceinline__ float w(int64_t e, int, int hh) const { return __ldcs(alpha + e * heads + h + hh); }
   };
-  __device__ __forceinline__ Row row(int64_t, int h, bool) const { return Row{alpha, heads, h}; }
+  __device__ __forceinline__ Row row(int64_t, int h, bool, void *) const { return Row{alpha, heads, h}; }
 };
 
 struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax)
@@ -228,7 +229,12 @@ struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax
 
 // Fused GAT weight (A13): s = LeakyReLU(el[u] + er[v]) in fp64,
 // alpha = exp(s - m) / S with the row statistics (m, S) computed inside the
-// aggregate kernel by the team that owns the (row, head) -- no stats pass.
+// aggregate kernel by the team that owns (row, heads h .. h+hpt-1) -- no
+// stats pass.  Per-head state lives in the team's shared memory.
+struct GatTeamStat {
+  double el_u, m;
+  float inv_s, pad;
+};
 struct WeightGat {
   const float *el, *er;
   float *alpha_out;
@@ -238,23 +244,25 @@ struct WeightGat {
     static constexpr bool kUnit = false, kComputed = true, kStagedVal = false;
     const float *er;
     float *alpha_out;
-    double el_u, m, slope;
-    float inv_s;
+    double slope;
     int heads, h;
-    __device__ __forceinline__ double score(int c) const {
-      const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
+    GatTeamStat *st;  // [kMaxHpt] in shared memory
+    __device__ __forceinline__ double score_of(double el_u, float er_v) const {
+      const double t = el_u + (double)er_v;
       return t >= 0.0 ? t : slope * t;
     }
-    __device__ __forceinline__ float finish(int64_t e, double s) const {
-      const float a = expf((float)(s - m)) * inv_s;
-      if (alpha_out) alpha_out[e * heads + h] = a;
+    __device__ __forceinline__ double score(int c, int hh) const {
+      return score_of(st[hh].el_u, __ldg(er + (int64_t)c * heads + h + hh));
+    }
+    __device__ __forceinline__ float finish(int64_t e, double s, int hh) const {
+      const float a = expf((float)(s - st[hh].m)) * st[hh].inv_s;
+      if (alpha_out) alpha_out[e * heads + h + hh] = a;
       return a;
     }
-    __device__ __forceinline__ float w(int64_t e, int c) const { return finish(e, score(c)); }
   };
   // first_slab: only the first slab of a head writes alpha_out (each entry once)
-  __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab) const {
-    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), 0.0, slope, 0.0f, heads, h};
+  __device__ __forceinline__ Row row(int64_t, int h, bool first_slab, void *st) const {
+    return Row{er, first_slab ? alpha_out : nullptr, slope, heads, h, reinterpret_cast<GatTeamStat *>(st)};
   }
 };
 
@@ -274,6 +282,7 @@ struct EngineParams {
   int stage;               // 1: stage col (and stage_val) in shared memory
   int win_cap;             // window capacity in entries (multiple of 4)
   int mean;                // GSpMM mean: divide the row sum by the row's entry count
+  int hpt;                 // heads per team (slab = hpt whole heads); 1 otherwise
 };
 
 // Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
@@ -392,8 +401,8 @@ template <int V, int G, bool kLong, class R, class Row, class Pro>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
                                              const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
-                                             unsigned tmask, int32_t *tc, float *tw, const double *cache, int ncache,
-                                             float (&out)[V], Pro &&prologue) {
+                                             unsigned tmask, int32_t *tc, float *tw, int hl, const double *cache,
+                                             int ncache, float (&out)[V], Pro &&prologue) {
   using TM = Team<G>;
   constexpr int T = TM::T, SPR = TM::SPR, NACC = TM::NACC, EPL = TM::EPL;
   float acc1[V], acc2[V];
@@ -405,7 +414,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     const int cnt = (int)(d - s * kSeg < kSeg ? d - s * kSeg : kSeg);
     const bool seg_in = win.in(e0) && e0 + cnt <= win.we;  // team-uniform
     const int32_t *sc;
-    const float *sw = tw;
+    const float *sw = tw + hl * kSeg;  // this lane's head's weights
     bool scratch = false;
     if (seg_in) {
       sc = win.scol + (e0 - win.wb);
@@ -433,11 +442,16 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
           const int j = tl + T * i;
           if (j < cnt) {
             const int c = sc[j];
-            if constexpr (Row::kComputed) {
-              const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
-              tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
-            } else {
-              tw[j] = wr.w(e0 + j, c);
+            const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
+#pragma unroll
+            for (int hh = 0; hh < kMaxHpt; ++hh) {
+              if (hh < p.hpt) {
+                if constexpr (Row::kComputed)
+                  tw[hh * kSeg + j] =
+                      wr.finish(e0 + j, (cache && q < ncache) ? cache[q * p.hpt + hh] : wr.score(c, hh), hh);
+                else
+                  tw[hh * kSeg + j] = wr.w(e0 + j, c, hh);
+              }
             }
           }
         }
@@ -505,9 +519,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   __shared__ int s_nhub, s_next;
   __shared__ __align__(16) float s_part[kVirt * SW];
   __shared__ __align__(8) uint64_t s_bar[kStageChunks];
-  __shared__ float s_tw[NT][kSeg];    // per-team scratch: weights
+  constexpr int kHptCap = G >= 2 ? kMaxHpt : 1;  // G == 1 slabs never hold more than one head
+  __shared__ float s_tw[NT][kHptCap * kSeg];     // per-team scratch: weights, per head
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
-  constexpr bool kGat = decltype(wf.row(0, 0, false))::kComputed;
+  constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kComputed;
+  __shared__ GatTeamStat s_gst[kGat ? NT : 1][kGat ? kHptCap : 1];
   constexpr int kCache = kGat ? 1024 / NT : 1;  // per-team fp64 score cache (GAT)
   __shared__ double s_cache[NT][kCache];
   __shared__ double s_red[kThreads / 32];
@@ -573,7 +589,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   const bool active = col0 < p.f;
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
   const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
-  const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;
+  const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
+  const int hl = p.hpt > 1 ? (int)((gl * V) / p.head_dim) : 0;         // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
 
   // 1. collect hub rows
@@ -604,35 +621,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
-    auto wr = wf.row(r, head, first_slab);
+    auto wr = wf.row(r, head, first_slab, kGat ? (void *)&s_gst[0][0] : nullptr);
     ensure(start + d);
     if constexpr (kGat) {
-      // CTA-wide softmax statistics of a hub row: thread tid takes edges
-      // tid + 256k; warp xor butterflies, then warps 0..7 in order (fixed)
-      double m = -INFINITY;
-      for (int64_t q = tid; q < d; q += kThreads) m = fmax(m, wr.score(win.col(p.col, start + q)));
-      m = team_max<32>(m, 0xffffffffu);
-      if (lane == 0) s_red[warp] = m;
-      __syncthreads();
-      m = s_red[0];
-      for (int w2 = 1; w2 < kThreads / 32; ++w2) m = fmax(m, s_red[w2]);
-      __syncthreads();
-      double S = 0.0;
-      for (int64_t q = tid; q < d; q += kThreads)
-        S += (double)expf((float)(wr.score(win.col(p.col, start + q)) - m));
-      S = team_sum<32>(S, 0xffffffffu);
-      if (lane == 0) s_red[warp] = S;
-      __syncthreads();
-      S = s_red[0];
-      for (int w2 = 1; w2 < kThreads / 32; ++w2) S += s_red[w2];
-      __syncthreads();
-      wr.m = m;
-      wr.inv_s = (float)(1.0 / S);
+      // CTA-wide softmax statistics of a hub row, head by head: thread tid
+      // takes edges tid + 256k; warp xor butterflies, then warps in order
+      for (int hh = 0; hh < p.hpt; ++hh) {
+        if (tid == 0) s_gst[0][hh].el_u = (double)__ldg(wf.el + r * wf.heads + head + hh);
+        __syncthreads();
+        double m = -INFINITY;
+        for (int64_t q = tid; q < d; q += kThreads) m = fmax(m, wr.score(win.col(p.col, start + q), hh));
+        m = team_max<32>(m, 0xffffffffu);
+        if (lane == 0) s_red[warp] = m;
+        __syncthreads();
+        m = s_red[0];
+        for (int w2 = 1; w2 < kThreads / 32; ++w2) m = fmax(m, s_red[w2]);
+        __syncthreads();
+        double S = 0.0;
+        for (int64_t q = tid; q < d; q += kThreads)
+          S += (double)expf((float)(wr.score(win.col(p.col, start + q), hh) - m));
+        S = team_sum<32>(S, 0xffffffffu);
+        if (lane == 0) s_red[warp] = S;
+        __syncthreads();
+        S = s_red[0];
+        for (int w2 = 1; w2 < kThreads / 32; ++w2) S += s_red[w2];
+        if (tid == 0) {
+          s_gst[0][hh].m = m;
+          s_gst[0][hh].inv_s = (float)(1.0 / S);
+        }
+        __syncthreads();
+      }
     }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
       row_segments<V, G, true, R>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
-                               s_tc[team], s_tw[team], nullptr, 0, part, [] {});
+                                  s_tc[team], s_tw[team], hl, nullptr, 0, part, [] {});
       if (sg == 0) {
 #pragma unroll
         for (int i = 0; i < V; ++i) s_part[v * SW + gl * V + i] = part[i];
@@ -667,33 +690,66 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     if (d > kHub) continue;
-    auto wr = wf.row(r, head, first_slab);
+    auto wr = wf.row(r, head, first_slab, kGat ? (void *)&s_gst[kGat ? team : 0][0] : nullptr);
     ensure(start + d);
     // GAT: the team's softmax statistics run inside the first segment, after
     // its first chunk of Z gathers has been issued; scores of the first kCache
     // edges are cached in fp64 by the lane that later turns them into alpha
     auto stats = [&]() {
       if constexpr (kGat) {
-        double m = -INFINITY;
-        for (int64_t q = tl; q < d; q += T) {
-          const double sc = wr.score(win.col(p.col, start + q));
-          if (q < kCache) s_cache[team][q] = sc;
-          m = fmax(m, sc);
+        // all hpt heads in one pass over the row; lane tl owns edges tl + T*k
+        const int H = p.hpt, nc = kCache / H;  // cached edges
+        double el_u[kMaxHpt], m[kMaxHpt], S[kMaxHpt];
+#pragma unroll
+        for (int hh = 0; hh < kMaxHpt; ++hh) {
+          el_u[hh] = hh < H ? (double)__ldg(wf.el + r * wf.heads + head + hh) : 0.0;
+          m[hh] = -INFINITY;
+          S[hh] = 0.0;
         }
-        m = team_max<T>(m, tmask);
-        double S = 0.0;
         for (int64_t q = tl; q < d; q += T) {
-          const double sc = q < kCache ? s_cache[team][q] : wr.score(win.col(p.col, start + q));
-          S += (double)expf((float)(sc - m));
+          const int c = win.col(p.col, start + q);
+          const float *erv = wf.er + (int64_t)c * wf.heads + head;
+#pragma unroll
+          for (int hh = 0; hh < kMaxHpt; ++hh) {
+            if (hh < H) {
+              const double sc = wr.score_of(el_u[hh], __ldg(erv + hh));
+              if (q < nc) s_cache[team][q * H + hh] = sc;
+              m[hh] = fmax(m[hh], sc);
+            }
+          }
         }
-        S = team_sum<T>(S, tmask);
-        wr.m = m;
-        wr.inv_s = (float)(1.0 / S);
+#pragma unroll
+        for (int hh = 0; hh < kMaxHpt; ++hh)
+          if (hh < H) m[hh] = team_max<T>(m[hh], tmask);
+        for (int64_t q = tl; q < d; q += T) {
+          const int c = q < nc ? 0 : win.col(p.col, start + q);
+#pragma unroll
+          for (int hh = 0; hh < kMaxHpt; ++hh) {
+            if (hh < H) {
+              const double sc = q < nc ? s_cache[team][q * H + hh]
+                                       : wr.score_of(el_u[hh], __ldg(wf.er + (int64_t)c * wf.heads + head + hh));
+              S[hh] += (double)expf((float)(sc - m[hh]));
+            }
+          }
+        }
+#pragma unroll
+        for (int hh = 0; hh < kMaxHpt; ++hh) {
+          if (hh < H) {
+            S[hh] = team_sum<T>(S[hh], tmask);
+            if (tl == 0) {
+              s_gst[team][hh].el_u = el_u[hh];
+              s_gst[team][hh].m = m[hh];
+              s_gst[team][hh].inv_s = (float)(1.0 / S[hh]);
+            }
+          }
+        }
+        __syncwarp(tmask);
       }
     };
     float out[V];
     row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask,
-                                 s_tc[team], s_tw[team], kGat ? &s_cache[team][0] : nullptr, kCache, out, stats);
+                                 s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr,
+                                 kGat ? kCache / p.hpt : 0, out, stats);
     finish_row<R, V>(out, d, p.mean);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
@@ -710,6 +766,11 @@ struct EngineLaunch {
 
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L);
+
+// heads per team for a multi-head launch planned with slab L.slab_cols
+inline int engine_hpt(const EngineLaunch &L, int64_t head_dim) {
+  return (head_dim > 0 && L.slab_cols > head_dim) ? (int)(L.slab_cols / head_dim) : 1;
+}
 
 // y may take the V-wide (at most float4) stores
 inline int engine_y_vec_ok(const EngineLaunch &L, const float *y, int64_t ldy) {
@@ -734,6 +795,7 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.stage_val = (p.stage && val && aligned16(val)) ? val : nullptr;
   p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
   p.mean = 0;
+  p.hpt = 1;
 }
 
 template <int V, int G, class W, class R>

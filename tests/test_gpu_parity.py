@@ -260,7 +260,7 @@ def test_attn_project_parity(H, D):
     assert_within(host(er), er_ref, erc, what="er")
 
 
-@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16)])
+@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 64), (4, 32), (4, 1)])
 def test_multihead_spmm_parity(built, H, D):
     for name in ("multi2", "cl4000", "hubs"):
         go, gg, _, _ = built[name]
@@ -278,7 +278,7 @@ def _gat_ref(go, el, er, z, H, D, slope):
     return y, cond, a
 
 
-@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16)])
+@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 64), (4, 32), (4, 1)])
 def test_gat_aggregate_parity(built, H, D):
     for name in ("multi0", "cl4000", "rmat3000", "hubs"):
         go, gg, _, _ = built[name]
