@@ -194,7 +194,7 @@ struct RedMin {
 struct WeightVal {  // SpMM with A's values
   const float *val;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = false, kStagedVal = true;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = true, kMultiHead = false;
     const float *val;
     __device__ __forceinline__ float w(int64_t e, int /*c*/, int /*hh*/) const { return __ldcs(val + e); }
   };
@@ -203,7 +203,7 @@ struct WeightVal {  // SpMM with A's values
 
 struct WeightOne {  // SpMM with val == NULL: psi = copy
   struct Row {
-    static constexpr bool kUnit = true, kComputed = false, kStagedVal = false;
+    static constexpr bool kUnit = true, kComputed = false, kStagedVal = false, kMultiHead = false;
     __device__ __forceinline__ float w(int64_t, int, int) const { return 1.0f; }
   };
   __device__ __forceinline__ Row row(int64_t, int, bool, void *) const { return Row{}; }
@@ -213,7 +213,7 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   const float *alpha;
   int heads;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true;
     const float *alpha;
     int heads, h;  // h: first head of the team's slab
     __device__ __forceinline__ float w(int64_t e, int, int hh) const { return __ldcs(alpha + e * heads + h + hh); }
@@ -241,7 +241,7 @@ struct WeightGat {
   double slope;
   int heads;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false;
+    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = true;
     const float *er;
     float *alpha_out;
     double slope;
@@ -443,9 +443,10 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
           if (j < cnt) {
             const int c = sc[j];
             const int64_t q = e0 + j - start;  // row-relative; cached by this same lane
+            constexpr int kHH = Row::kMultiHead ? kMaxHpt : 1;  // single-head modes: compile-time 1
 #pragma unroll
-            for (int hh = 0; hh < kMaxHpt; ++hh) {
-              if (hh < p.hpt) {
+            for (int hh = 0; hh < kHH; ++hh) {
+              if (hh == 0 || hh < p.hpt) {
                 if constexpr (Row::kComputed)
                   tw[hh * kSeg + j] =
                       wr.finish(e0 + j, (cache && q < ncache) ? cache[q * p.hpt + hh] : wr.score(c, hh), hh);
@@ -508,8 +509,15 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
   }
 }
 
+// register budget: 4 CTAs/SM (64 regs) for stored/unit weights; the fused
+// GAT weight keeps fp64 softmax state live and gets 3 CTAs/SM (85 regs)
+template <class W>
+struct MinBlocksFor {
+  static constexpr int value = W::Row::kComputed ? (kMinBlocks > 3 ? 3 : kMinBlocks) : kMinBlocks;
+};
+
 template <int V, int G, class W, class R>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const EngineParams p, const W wf) {
+__global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kernel(const EngineParams p, const W wf) {
   using TM = Team<G>;
   constexpr int T = TM::T;
   constexpr int NT = kThreads / T;  // teams per CTA
@@ -590,7 +598,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
   const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
-  const int hl = p.hpt > 1 ? (int)((gl * V) / p.head_dim) : 0;         // this lane's head offset
+  constexpr bool kMH = decltype(wf.row(0, 0, false, nullptr))::kMultiHead;
+  const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
 
   // 1. collect hub rows
@@ -697,50 +706,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) engine_kernel(const Engi
     // edges are cached in fp64 by the lane that later turns them into alpha
     auto stats = [&]() {
       if constexpr (kGat) {
-        // all hpt heads in one pass over the row; lane tl owns edges tl + T*k
+        // head by head (scalar fp64 state); lane tl owns edges tl + T*k; the
+        // scores of the first nc edges are cached as [q][hh]
         const int H = p.hpt, nc = kCache / H;  // cached edges
-        double el_u[kMaxHpt], m[kMaxHpt], S[kMaxHpt];
-#pragma unroll
-        for (int hh = 0; hh < kMaxHpt; ++hh) {
-          el_u[hh] = hh < H ? (double)__ldg(wf.el + r * wf.heads + head + hh) : 0.0;
-          m[hh] = -INFINITY;
-          S[hh] = 0.0;
-        }
-        for (int64_t q = tl; q < d; q += T) {
-          const int c = win.col(p.col, start + q);
-          const float *erv = wf.er + (int64_t)c * wf.heads + head;
-#pragma unroll
-          for (int hh = 0; hh < kMaxHpt; ++hh) {
-            if (hh < H) {
-              const double sc = wr.score_of(el_u[hh], __ldg(erv + hh));
-              if (q < nc) s_cache[team][q * H + hh] = sc;
-              m[hh] = fmax(m[hh], sc);
-            }
+        for (int hh = 0; hh < H; ++hh) {
+          const double el_u = (double)__ldg(wf.el + r * wf.heads + head + hh);
+          double m = -INFINITY;
+          for (int64_t q = tl; q < d; q += T) {
+            const double sc = wr.score_of(el_u, __ldg(wf.er + (int64_t)win.col(p.col, start + q) * wf.heads + head + hh));
+            if (q < nc) s_cache[team][q * H + hh] = sc;
+            m = fmax(m, sc);
           }
-        }
-#pragma unroll
-        for (int hh = 0; hh < kMaxHpt; ++hh)
-          if (hh < H) m[hh] = team_max<T>(m[hh], tmask);
-        for (int64_t q = tl; q < d; q += T) {
-          const int c = q < nc ? 0 : win.col(p.col, start + q);
-#pragma unroll
-          for (int hh = 0; hh < kMaxHpt; ++hh) {
-            if (hh < H) {
-              const double sc = q < nc ? s_cache[team][q * H + hh]
-                                       : wr.score_of(el_u[hh], __ldg(wf.er + (int64_t)c * wf.heads + head + hh));
-              S[hh] += (double)expf((float)(sc - m[hh]));
-            }
+          m = team_max<T>(m, tmask);
+          double S = 0.0;
+          for (int64_t q = tl; q < d; q += T) {
+            const double sc =
+                q < nc ? s_cache[team][q * H + hh]
+                       : wr.score_of(el_u, __ldg(wf.er + (int64_t)win.col(p.col, start + q) * wf.heads + head + hh));
+            S += (double)expf((float)(sc - m));
           }
-        }
-#pragma unroll
-        for (int hh = 0; hh < kMaxHpt; ++hh) {
-          if (hh < H) {
-            S[hh] = team_sum<T>(S[hh], tmask);
-            if (tl == 0) {
-              s_gst[team][hh].el_u = el_u[hh];
-              s_gst[team][hh].m = m[hh];
-              s_gst[team][hh].inv_s = (float)(1.0 / S[hh]);
-            }
+          S = team_sum<T>(S, tmask);
+          if (tl == 0) {
+            s_gst[team][hh].el_u = el_u;
+            s_gst[team][hh].m = m;
+            s_gst[team][hh].inv_s = (float)(1.0 / S);
           }
         }
         __syncwarp(tmask);
