@@ -527,8 +527,9 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   __shared__ int s_nhub, s_next;
   __shared__ __align__(16) float s_part[kVirt * SW];
   __shared__ __align__(8) uint64_t s_bar[kStageChunks];
-  constexpr int kHptCap = G >= 2 ? kMaxHpt : 1;  // G == 1 slabs never hold more than one head
-  __shared__ float s_tw[NT][kHptCap * kSeg];     // per-team scratch: weights, per head
+  constexpr bool kMH = W::Row::kMultiHead;
+  constexpr int kHptCap = (kMH && G >= 2) ? kMaxHpt : 1;  // G == 1 slabs never hold more than one head
+  __shared__ float s_tw[NT][kHptCap * kSeg];              // per-team scratch: weights, per head
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
   constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kComputed;
   __shared__ GatTeamStat s_gst[kGat ? NT : 1][kGat ? kHptCap : 1];
@@ -598,7 +599,6 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
   const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
-  constexpr bool kMH = decltype(wf.row(0, 0, false, nullptr))::kMultiHead;
   const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
 
