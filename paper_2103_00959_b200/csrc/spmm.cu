@@ -14,8 +14,12 @@ static int64_t pow2_floor(int64_t v) {
 // streamed CSR, Y and the next slab).  DESIGN.md §Kernels / slab sizing.
 static constexpr int64_t kL2SlabBudget = 48ll << 20;
 
+#ifndef GSP_MAX_HPT
+#define GSP_MAX_HPT kMaxHpt
+#endif
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L) {
+  const int64_t max_hpt = GSP_MAX_HPT;
   int V = vmax;
   int64_t SW = 0;
   if (head_dim > 0) {
@@ -30,7 +34,7 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
     } else {
       // prefer a slab of hpt whole heads (hpt | heads, hpt <= kMaxHpt, <= 128 columns); else slabs inside a head
       SW = 0;
-      for (int64_t hpt = std::min<int64_t>(kMaxHpt, heads); hpt >= 1 && !SW; --hpt) {
+      for (int64_t hpt = std::min<int64_t>(max_hpt, heads); hpt >= 1 && !SW; --hpt) {
         const int64_t sw = hpt * head_dim, g = sw / V;
         if (heads % hpt == 0 && sw <= 128 && sw % V == 0 && g >= 1 && g <= 32 && (g & (g - 1)) == 0) SW = sw;
       }

@@ -511,9 +511,12 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
 
 // register budget: 4 CTAs/SM (64 regs) for stored/unit weights; the fused
 // GAT weight keeps fp64 softmax state live and gets 3 CTAs/SM (85 regs)
+#ifndef GSP_GAT_MIN_BLOCKS
+#define GSP_GAT_MIN_BLOCKS 3
+#endif
 template <class W>
 struct MinBlocksFor {
-  static constexpr int value = W::Row::kComputed ? (kMinBlocks > 3 ? 3 : kMinBlocks) : kMinBlocks;
+  static constexpr int value = W::Row::kComputed ? GSP_GAT_MIN_BLOCKS : kMinBlocks;
 };
 
 template <int V, int G, class W, class R>

@@ -5,9 +5,9 @@ cd "$(dirname "$0")/.."
 mkdir -p variants
 rm -f variants/*.so
 build() { python paper_2103_00959_b200/_build.py --force --out=variants/libgsp_$1.so ${@:2} > /dev/null & }
-build base -DGSP_MIN_BLOCKS=4 -DGSP_UNROLL=8
-build pipe4 -DGSP_MIN_BLOCKS=4 -DGSP_UNROLL=4 -DGSP_PIPE=1
-build pipe8 -DGSP_MIN_BLOCKS=3 -DGSP_UNROLL=8 -DGSP_PIPE=1
-build pipe2 -DGSP_MIN_BLOCKS=4 -DGSP_UNROLL=2 -DGSP_PIPE=1
+build gat_h4_b3 -DGSP_MAX_HPT=4 -DGSP_GAT_MIN_BLOCKS=3
+build gat_h4_b4 -DGSP_MAX_HPT=4 -DGSP_GAT_MIN_BLOCKS=4
+build gat_h1_b4 -DGSP_MAX_HPT=1 -DGSP_GAT_MIN_BLOCKS=4
+build gat_h1_b3 -DGSP_MAX_HPT=1 -DGSP_GAT_MIN_BLOCKS=3
 wait
 ls variants
