@@ -240,7 +240,7 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
   EngineLaunch L;
-  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L);
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, 1);  // one head per team (fp64 state in registers)
   if (st) return st;
   EngineParams p;
   p.row_ptr = a->row_ptr;

@@ -14,12 +14,8 @@ static int64_t pow2_floor(int64_t v) {
 // streamed CSR, Y and the next slab).  DESIGN.md §Kernels / slab sizing.
 static constexpr int64_t kL2SlabBudget = 48ll << 20;
 
-#ifndef GSP_MAX_HPT
-#define GSP_MAX_HPT kMaxHpt
-#endif
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
-                       int32_t slab_req, int32_t block_req, EngineLaunch *L) {
-  const int64_t max_hpt = GSP_MAX_HPT;
+                       int32_t slab_req, int32_t block_req, EngineLaunch *L, int max_hpt) {
   int V = vmax;
   int64_t SW = 0;
   if (head_dim > 0) {
@@ -97,7 +93,7 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (ldx % 4 == 0 && aligned16(x)) vmax = 4;
   else if (ldx % 2 == 0 && aligned8(x)) vmax = 2;
   const int32_t slab_req = opts ? opts->slab_cols : 0, block_req = opts ? opts->block_nnz : 0;
-  gsp_status st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, slab_req, block_req, &P->main);
+  gsp_status st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, slab_req, block_req, &P->main, 1);
   if (st) return st;
   P->f_main = f;
   P->f_tail = 0;
@@ -105,7 +101,7 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (slab_req == 0 && P->main.V == 4 && f > SW && rem && rem <= SW / 2) {
     int64_t tw = 16;
     while (tw < rem) tw *= 2;
-    st = engine_plan(a->n_rows, a->n_cols, a->nnz, rem, 0, vmax, (int32_t)tw, block_req, &P->tail);
+    st = engine_plan(a->n_rows, a->n_cols, a->nnz, rem, 0, vmax, (int32_t)tw, block_req, &P->tail, 1);
     if (st) return st;
     P->f_main = f - rem;
     P->f_tail = rem;
@@ -224,7 +220,7 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
   EngineLaunch L;
-  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L);
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, kMaxHpt);
   if (st) return st;
   EngineParams p;
   p.row_ptr = a->row_ptr;

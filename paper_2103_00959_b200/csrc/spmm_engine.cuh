@@ -229,40 +229,34 @@ struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax
 
 // Fused GAT weight (A13): s = LeakyReLU(el[u] + er[v]) in fp64,
 // alpha = exp(s - m) / S with the row statistics (m, S) computed inside the
-// aggregate kernel by the team that owns (row, heads h .. h+hpt-1) -- no
-// stats pass.  Per-head state lives in the team's shared memory.
-struct GatTeamStat {
-  double el_u, m;
-  float inv_s, pad;
-};
+// aggregate kernel by the team that owns the (row, head) -- no stats pass.
+// One head per team: the fp64 row state stays in registers (measured faster
+// than several heads per team with the state in shared memory).
 struct WeightGat {
   const float *el, *er;
   float *alpha_out;
   double slope;
   int heads;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = true;
+    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = false;
     const float *er;
     float *alpha_out;
-    double slope;
+    double el_u, m, slope;
+    float inv_s;
     int heads, h;
-    GatTeamStat *st;  // [kMaxHpt] in shared memory
-    __device__ __forceinline__ double score_of(double el_u, float er_v) const {
-      const double t = el_u + (double)er_v;
+    __device__ __forceinline__ double score(int c, int = 0) const {
+      const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
       return t >= 0.0 ? t : slope * t;
     }
-    __device__ __forceinline__ double score(int c, int hh) const {
-      return score_of(st[hh].el_u, __ldg(er + (int64_t)c * heads + h + hh));
-    }
-    __device__ __forceinline__ float finish(int64_t e, double s, int hh) const {
-      const float a = expf((float)(s - st[hh].m)) * st[hh].inv_s;
-      if (alpha_out) alpha_out[e * heads + h + hh] = a;
+    __device__ __forceinline__ float finish(int64_t e, double s, int = 0) const {
+      const float a = expf((float)(s - m)) * inv_s;
+      if (alpha_out) alpha_out[e * heads + h] = a;
       return a;
     }
   };
   // first_slab: only the first slab of a head writes alpha_out (each entry once)
-  __device__ __forceinline__ Row row(int64_t, int h, bool first_slab, void *st) const {
-    return Row{er, first_slab ? alpha_out : nullptr, slope, heads, h, reinterpret_cast<GatTeamStat *>(st)};
+  __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab, void *) const {
+    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), 0.0, slope, 0.0f, heads, h};
   }
 };
 
@@ -448,8 +442,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
             for (int hh = 0; hh < kHH; ++hh) {
               if (hh == 0 || hh < p.hpt) {
                 if constexpr (Row::kComputed)
-                  tw[hh * kSeg + j] =
-                      wr.finish(e0 + j, (cache && q < ncache) ? cache[q * p.hpt + hh] : wr.score(c, hh), hh);
+                  tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
                 else
                   tw[hh * kSeg + j] = wr.w(e0 + j, c, hh);
               }
@@ -512,7 +505,7 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
 // register budget: 4 CTAs/SM (64 regs) for stored/unit weights; the fused
 // GAT weight keeps fp64 softmax state live and gets 3 CTAs/SM (85 regs)
 #ifndef GSP_GAT_MIN_BLOCKS
-#define GSP_GAT_MIN_BLOCKS 3
+#define GSP_GAT_MIN_BLOCKS 4
 #endif
 template <class W>
 struct MinBlocksFor {
@@ -535,7 +528,6 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   __shared__ float s_tw[NT][kHptCap * kSeg];              // per-team scratch: weights, per head
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
   constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kComputed;
-  __shared__ GatTeamStat s_gst[kGat ? NT : 1][kGat ? kHptCap : 1];
   constexpr int kCache = kGat ? 1024 / NT : 1;  // per-team fp64 score cache (GAT)
   __shared__ double s_cache[NT][kCache];
   __shared__ double s_red[kThreads / 32];
@@ -633,36 +625,30 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
-    auto wr = wf.row(r, head, first_slab, kGat ? (void *)&s_gst[0][0] : nullptr);
+    auto wr = wf.row(r, head, first_slab, nullptr);
     ensure(start + d);
     if constexpr (kGat) {
-      // CTA-wide softmax statistics of a hub row, head by head: thread tid
-      // takes edges tid + 256k; warp xor butterflies, then warps in order
-      for (int hh = 0; hh < p.hpt; ++hh) {
-        if (tid == 0) s_gst[0][hh].el_u = (double)__ldg(wf.el + r * wf.heads + head + hh);
-        __syncthreads();
-        double m = -INFINITY;
-        for (int64_t q = tid; q < d; q += kThreads) m = fmax(m, wr.score(win.col(p.col, start + q), hh));
-        m = team_max<32>(m, 0xffffffffu);
-        if (lane == 0) s_red[warp] = m;
-        __syncthreads();
-        m = s_red[0];
-        for (int w2 = 1; w2 < kThreads / 32; ++w2) m = fmax(m, s_red[w2]);
-        __syncthreads();
-        double S = 0.0;
-        for (int64_t q = tid; q < d; q += kThreads)
-          S += (double)expf((float)(wr.score(win.col(p.col, start + q), hh) - m));
-        S = team_sum<32>(S, 0xffffffffu);
-        if (lane == 0) s_red[warp] = S;
-        __syncthreads();
-        S = s_red[0];
-        for (int w2 = 1; w2 < kThreads / 32; ++w2) S += s_red[w2];
-        if (tid == 0) {
-          s_gst[0][hh].m = m;
-          s_gst[0][hh].inv_s = (float)(1.0 / S);
-        }
-        __syncthreads();
-      }
+      // CTA-wide softmax statistics of a hub row: thread tid takes edges
+      // tid + 256k; warp xor butterflies, then warps 0..7 in order (fixed)
+      double m = -INFINITY;
+      for (int64_t q = tid; q < d; q += kThreads) m = fmax(m, wr.score(win.col(p.col, start + q)));
+      m = team_max<32>(m, 0xffffffffu);
+      if (lane == 0) s_red[warp] = m;
+      __syncthreads();
+      m = s_red[0];
+      for (int w2 = 1; w2 < kThreads / 32; ++w2) m = fmax(m, s_red[w2]);
+      __syncthreads();
+      double S = 0.0;
+      for (int64_t q = tid; q < d; q += kThreads)
+        S += (double)expf((float)(wr.score(win.col(p.col, start + q)) - m));
+      S = team_sum<32>(S, 0xffffffffu);
+      if (lane == 0) s_red[warp] = S;
+      __syncthreads();
+      S = s_red[0];
+      for (int w2 = 1; w2 < kThreads / 32; ++w2) S += s_red[w2];
+      __syncthreads();
+      wr.m = m;
+      wr.inv_s = (float)(1.0 / S);
     }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
@@ -702,46 +688,37 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     if (d > kHub) continue;
-    auto wr = wf.row(r, head, first_slab, kGat ? (void *)&s_gst[kGat ? team : 0][0] : nullptr);
+    auto wr = wf.row(r, head, first_slab, nullptr);
     ensure(start + d);
     // GAT: the team's softmax statistics run inside the first segment, after
     // its first chunk of Z gathers has been issued; scores of the first kCache
     // edges are cached in fp64 by the lane that later turns them into alpha
     auto stats = [&]() {
       if constexpr (kGat) {
-        // head by head (scalar fp64 state); lane tl owns edges tl + T*k; the
-        // scores of the first nc edges are cached as [q][hh]
-        const int H = p.hpt, nc = kCache / H;  // cached edges
-        for (int hh = 0; hh < H; ++hh) {
-          const double el_u = (double)__ldg(wf.el + r * wf.heads + head + hh);
-          double m = -INFINITY;
-          for (int64_t q = tl; q < d; q += T) {
-            const double sc = wr.score_of(el_u, __ldg(wf.er + (int64_t)win.col(p.col, start + q) * wf.heads + head + hh));
-            if (q < nc) s_cache[team][q * H + hh] = sc;
-            m = fmax(m, sc);
-          }
-          m = team_max<T>(m, tmask);
-          double S = 0.0;
-          for (int64_t q = tl; q < d; q += T) {
-            const double sc =
-                q < nc ? s_cache[team][q * H + hh]
-                       : wr.score_of(el_u, __ldg(wf.er + (int64_t)win.col(p.col, start + q) * wf.heads + head + hh));
-            S += (double)expf((float)(sc - m));
-          }
-          S = team_sum<T>(S, tmask);
-          if (tl == 0) {
-            s_gst[team][hh].el_u = el_u;
-            s_gst[team][hh].m = m;
-            s_gst[team][hh].inv_s = (float)(1.0 / S);
-          }
+        // lane tl owns edges tl + T*k; the scores of the first kCache edges are
+        // cached in fp64 by the lane that later turns them into alpha
+        double m = -INFINITY;
+        for (int64_t q = tl; q < d; q += T) {
+          const double sc = wr.score(win.col(p.col, start + q));
+          if (q < kCache) s_cache[team][q] = sc;
+          m = fmax(m, sc);
         }
+        m = team_max<T>(m, tmask);
+        double S = 0.0;
+        for (int64_t q = tl; q < d; q += T) {
+          const double sc = q < kCache ? s_cache[team][q] : wr.score(win.col(p.col, start + q));
+          S += (double)expf((float)(sc - m));
+        }
+        S = team_sum<T>(S, tmask);
+        wr.m = m;
+        wr.inv_s = (float)(1.0 / S);
         __syncwarp(tmask);
       }
     };
     float out[V];
     row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask,
-                                 s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr,
-                                 kGat ? kCache / p.hpt : 0, out, stats);
+                                 s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr, kGat ? kCache : 0,
+                                 out, stats);
     finish_row<R, V>(out, d, p.mean);
     if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
   }
@@ -757,7 +734,7 @@ struct EngineLaunch {
 };
 
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
-                       int32_t slab_req, int32_t block_req, EngineLaunch *L);
+                       int32_t slab_req, int32_t block_req, EngineLaunch *L, int max_hpt);
 
 // heads per team for a multi-head launch planned with slab L.slab_cols
 inline int engine_hpt(const EngineLaunch &L, int64_t head_dim) {

@@ -5,9 +5,7 @@ cd "$(dirname "$0")/.."
 mkdir -p variants
 rm -f variants/*.so
 build() { python paper_2103_00959_b200/_build.py --force --out=variants/libgsp_$1.so ${@:2} > /dev/null & }
-build gat_h4_b3 -DGSP_MAX_HPT=4 -DGSP_GAT_MIN_BLOCKS=3
-build gat_h4_b4 -DGSP_MAX_HPT=4 -DGSP_GAT_MIN_BLOCKS=4
-build gat_h1_b4 -DGSP_MAX_HPT=1 -DGSP_GAT_MIN_BLOCKS=4
-build gat_h1_b3 -DGSP_MAX_HPT=1 -DGSP_GAT_MIN_BLOCKS=3
+build gat_b4 -DGSP_GAT_MIN_BLOCKS=4
+build gat_b3 -DGSP_GAT_MIN_BLOCKS=3
 wait
 ls variants
