@@ -49,13 +49,15 @@ def lib():
         L.orc_sym_norm.argtypes = [I, P, P, P, P, P, P]
         L.orc_spmm.argtypes = [I, I, P, P, P, P, I, I, P, P, I]
         L.orc_gspmm.argtypes = [I, I, P, P, P, P, I, I, ctypes.c_int, P, I]
+        L.orc_propagate.argtypes = [I, P, P, P, P, I, I, I, P, P, P, I]
+        L.orc_ppr_coeffs.argtypes = [ctypes.c_double, I, P]
         L.orc_edge_softmax.argtypes = [I, I, P, I, P, P]
         L.orc_gat_scores.argtypes = [I, I, P, P, I, P, P, ctypes.c_double, P]
         L.orc_multihead_spmm.argtypes = [I, I, P, P, I, P, P, I, I, P, P, I]
         L.orc_attn_project.argtypes = [I, I, I, I, P, I, P, P, P, P, P, P]
         L.orc_partition_rows.argtypes = [I, P, I, P]
         L.orc_csr_slice.argtypes = [I, P, P, P, P, I, I, I, P, P, P]
-        for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_edge_softmax", "orc_gat_scores",
+        for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_propagate", "orc_ppr_coeffs", "orc_edge_softmax", "orc_gat_scores",
                   "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice"):
             getattr(L, f).restype = ctypes.c_int
     return _lib
@@ -159,6 +161,28 @@ def gspmm(row_ptr, col, a, x, reduce="sum", f=None, r0=0, r1=None):
     _chk(lib().orc_gspmm(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], REDUCE[reduce], _p(y),
                          y.shape[1]))
     return y[:, :f]
+
+
+def propagate(row_ptr, col, a, x, theta, f=None, want_cond=True):
+    """(y, cond) fp64 [n, f] = sum_k theta_k A^k x (oracle.c §3c)."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    a = _c(a, np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    n = row_ptr.size - 1
+    f = x.shape[1] if f is None else f
+    y = np.zeros((n, max(f, 1)), np.float64)
+    cond = np.zeros_like(y) if want_cond else None
+    _chk(lib().orc_propagate(n, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], theta.size - 1, _p(theta), _p(y),
+                             _p(cond), y.shape[1]))
+    return y[:, :f], (cond[:, :f] if want_cond else None)
+
+
+def ppr_coeffs(alpha, K):
+    th = np.zeros(K + 1, np.float64)
+    _chk(lib().orc_ppr_coeffs(float(alpha), K, _p(th)))
+    return th
 
 
 def edge_softmax(row_ptr, logits, heads=1, r0=0, r1=None):

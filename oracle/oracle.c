@@ -213,6 +213,61 @@ int orc_gspmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col
 }
 
 /* ---------------------------------------------------------------------------
+ * 3c. K-step graph propagation (NEXT-4): y = sum_{k=0..K} theta_k A^k x.
+ *    P:297 [graph diffusion matrix A_bar = sum_i alpha_i A^i "to collect
+ *    information of distant neighbors"], P:255 [APPNP: personalized-PageRank
+ *    propagation], S:171-188 [diffusion_matrix, ppr_coeffs].  Computed the
+ *    plain way: t_0 = x, t_k = A t_{k-1}, y = sum_k theta_k t_k (fp64).
+ *    cond (nullable) = the same recursion on |A|, |x|, |theta| (error scale).
+ *    Works on all n rows (the recursion needs every row).
+ * ------------------------------------------------------------------------- */
+int orc_propagate(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *a, const float *x,
+                  int64_t f, int64_t ldx, int64_t K, const double *theta, double *y, double *cond, int64_t ldy) {
+  if (n < 0 || f < 0 || ldx < f || ldy < f || K < 0 || !row_ptr || !x || !theta || !y) return ORC_ERR_ARG;
+  const size_t sz = (size_t)(n > 0 ? n : 1) * (size_t)(f > 0 ? f : 1);
+  double *t = (double *)malloc(sizeof(double) * sz), *t2 = (double *)malloc(sizeof(double) * sz);
+  double *ta = (double *)malloc(sizeof(double) * sz), *ta2 = (double *)malloc(sizeof(double) * sz);
+  if (!t || !t2 || !ta || !ta2) { free(t); free(t2); free(ta); free(ta2); return ORC_ERR_NOMEM; }
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t k = 0; k < f; ++k) {
+      t[u * f + k] = (double)x[u * ldx + k];
+      ta[u * f + k] = fabs((double)x[u * ldx + k]);
+      y[u * ldy + k] = theta[0] * t[u * f + k];
+      if (cond) cond[u * ldy + k] = fabs(theta[0]) * ta[u * f + k];
+    }
+  for (int64_t step = 1; step <= K; ++step) {
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t k = 0; k < f; ++k) {
+        double s = 0.0, sa = 0.0;
+        for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+          const double ae = a ? a[e] : 1.0;
+          s += ae * t[(int64_t)col[e] * f + k];
+          sa += fabs(ae) * ta[(int64_t)col[e] * f + k];
+        }
+        t2[u * f + k] = s;
+        ta2[u * f + k] = sa;
+      }
+    double *sw = t; t = t2; t2 = sw;
+    sw = ta; ta = ta2; ta2 = sw;
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t k = 0; k < f; ++k) {
+        y[u * ldy + k] += theta[step] * t[u * f + k];
+        if (cond) cond[u * ldy + k] += fabs(theta[step]) * ta[u * f + k];
+      }
+  }
+  free(t); free(t2); free(ta); free(ta2);
+  return ORC_OK;
+}
+
+/* PPR (APPNP) coefficients: theta_k = alpha (1 - alpha)^k, k = 0..K. */
+int orc_ppr_coeffs(double alpha, int64_t K, double *theta) {
+  if (!(alpha > 0.0 && alpha <= 1.0) || K < 0 || !theta) return ORC_ERR_ARG;
+  double p = alpha;
+  for (int64_t k = 0; k <= K; ++k) { theta[k] = p; p *= (1.0 - alpha); }
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * 4. Edge-wise softmax, per head.
  *    P:653-656 [§4.1: alpha'_uv = exp(alpha_uv) / sum_{w in N(u)} exp(alpha_uw);
  *    "first apply the scan to find the max value ... subtract this maximum ...

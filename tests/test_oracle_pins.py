@@ -469,3 +469,50 @@ def test_gspmm_vs_dense_numpy():
                 np.testing.assert_allclose(y[u], ref, rtol=1e-13, atol=1e-15, err_msg=red)
         ys, _ = orc.spmm(g.row_ptr, g.col, w, x)
         np.testing.assert_array_equal(orc.gspmm(g.row_ptr, g.col, w, x, "sum"), ys)
+
+
+# ---------------------------------------------------------------------------
+# 3c. K-step propagation (oracle.c §3c, NEXT-4)
+# ---------------------------------------------------------------------------
+
+def test_ppr_coeffs_spec_examples():
+    """S:185-187: alpha=1,K=3 -> [1,0,0,0]; alpha=0.5,K=2 -> [0.5,0.25,0.125];
+    sum = 1-(1-alpha)^(K+1)."""
+    np.testing.assert_array_equal(orc.ppr_coeffs(1.0, 3), [1, 0, 0, 0])
+    np.testing.assert_array_equal(orc.ppr_coeffs(0.5, 2), [0.5, 0.25, 0.125])
+    th = orc.ppr_coeffs(0.1, 10)
+    assert abs(th.sum() - (1 - 0.9 ** 11)) < 1e-15
+
+
+def test_propagate_vs_dense_matrix_polynomial():
+    """sum_k theta_k A^k X against numpy.linalg.matrix_power on small graphs;
+    K = 0 gives theta_0 X; theta = e_1 gives the single SpMM."""
+    rng = np.random.default_rng(31)
+    for t in range(25):
+        n = int(rng.integers(1, 40))
+        m = int(rng.integers(0, 3 * n + 1))
+        g = orc.build_csr(n, rng.integers(0, n, m), rng.integers(0, n, m), None, bool(t % 2), 1.0)
+        _, a64, _ = orc.sym_norm(g)
+        A = g.dense(a64)
+        x = uniform((n, 4), seed=t)
+        K = int(rng.integers(0, 6))
+        th = uniform(K + 1, seed=50 + t).astype(np.float64)
+        y, cond = orc.propagate(g.row_ptr, g.col, a64, x, th)
+        ref = sum(th[k] * np.linalg.matrix_power(A, k) @ x.astype(np.float64) for k in range(K + 1))
+        np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-13)
+        assert np.all(np.abs(y) <= cond * (1 + 1e-12) + 1e-300)
+    y1, _ = orc.propagate(g.row_ptr, g.col, a64, x, [0.0, 1.0])
+    ys, _ = orc.spmm(g.row_ptr, g.col, a64, x)
+    np.testing.assert_allclose(y1, ys, rtol=1e-15, atol=0)
+
+
+def test_propagate_sqrt_degree_eigenvector():
+    """A^ sqrt(d) = sqrt(d) => sum_k theta_k A^k sqrt(d) = (sum theta) sqrt(d)
+    on a power-law graph (PPR coefficients)."""
+    s, d = chung_lu(2000, 16000, seed=9)
+    g = orc.build_csr(2000, s, d, None, True, 1.0)
+    deg, a64, _ = orc.sym_norm(g)
+    x = np.sqrt(deg).astype(np.float32)[:, None]
+    th = orc.ppr_coeffs(0.1, 10)
+    y, _ = orc.propagate(g.row_ptr, g.col, a64, x, th)
+    np.testing.assert_allclose(y[:, 0], th.sum() * np.sqrt(deg), rtol=3e-7)
