@@ -427,6 +427,29 @@ def main():
             red[r_] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3)}
         out.setdefault("secondary", {})["C4_gspmm_reduce"] = red
 
+    # --- secondary: K-step propagation (APPNP, K=10, alpha=0.1) of 41-wide logits on C4 (NEXT-4) ---
+    if not use_dist and not args.no_gat:
+        fk, K = 41, 10
+        xk = torch.from_numpy(features(n, fk, 44, seed=9)).to(dev)
+        yk = torch.empty((n, fk), dtype=torch.float32, device=dev)
+        th = [0.1 * 0.9 ** k for k in range(K + 1)]
+        ts = []
+        for i in range(args.warmup + 5):
+            flush.zero_()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record()
+            G.gsp_propagate(gn, xk, th, f=fk, y=yk)
+            a1.record()
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                ts.append(a0.elapsed_time(a1))
+        tk = float(np.mean(ts))
+        out.setdefault("secondary", {})["C4_appnp_K10_f41"] = {
+            "ms": tk, "GE/s": K * nnz * fk / (tk * 1e-3), "launches": K,
+            "alg_GB/s": K * spmm_alg_bytes(n, nnz, fk) / (tk * 1e-3) / 1e9}
+        del xk, yk
+
     # --- secondary: fused GAT aggregate on the Flickr-shaped graph (C3) ---
     if not use_dist and not args.no_gat:
         c3 = CONFIGS["C3"]

@@ -162,6 +162,28 @@ typedef enum { GSP_REDUCE_SUM = 0, GSP_REDUCE_MEAN = 1, GSP_REDUCE_MAX = 2, GSP_
 gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_t f, int64_t ldx, float *y,
                      int64_t ldy, gsp_stream stream);
 
+/* ---------------------------------------------------------------------------
+ * K-step propagation (NEXT-4): y = sum_{k=0..K} theta_k A^k x.
+ * P:297 (graph diffusion A_bar = sum_i alpha_i A^i), P:255 (APPNP, personalized
+ * PageRank: theta_k = alpha (1 - alpha)^k), P:282 (SGC: theta = e_K);
+ * S:171-188.  K >= 1 launches of the SpMM engine with a fused accumulate
+ * epilogue; step 1 folds theta_0 x in, so no separate scale pass.
+ *   theta  HOST fp64 [K+1]
+ *   ws     device workspace of gsp_propagate_workspace() bytes (the t_k
+ *          ping-pong buffers; 0 for K == 1)
+ * A must be square; x and y must not overlap.
+ *
+ * gsp_spmm_accumulate is one step with the fused epilogue:
+ *   t = A x                        (written to t unless t == NULL)
+ *   acc = coef * t + (src != NULL ? src_coef * src : acc)      (fp32 fma)
+ * It is the building block of the row-partitioned multi-GPU propagation. */
+gsp_status gsp_spmm_accumulate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t, int64_t ldt,
+                               float *acc, int64_t ldacc, float coef, const float *src, int64_t ldsrc,
+                               float src_coef, gsp_stream stream);
+gsp_status gsp_propagate_workspace(const gsp_csr *a, int64_t f, int64_t K, size_t *ws_bytes);
+gsp_status gsp_propagate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, int64_t K, const double *theta,
+                         float *y, int64_t ldy, void *ws, size_t ws_bytes, gsp_stream stream);
+
 /* Tuning knobs for gsp_spmm_ex (0 = automatic).  Results are bitwise
  * identical for every setting (the summation order does not depend on them). */
 typedef struct {

@@ -32,7 +32,8 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
 EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
-           "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read")
+           "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
+           "gsp_propagate_workspace", "gsp_propagate")
 
 
 class GspError(RuntimeError):
@@ -73,6 +74,9 @@ def lib() -> ctypes.CDLL:
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
             "gsp_gspmm": [CP, ctypes.c_int, P, I, I, P, I, P],
             "gsp_probe_l2_read": [P, ctypes.c_size_t, I32, P, P],
+            "gsp_spmm_accumulate": [CP, P, I, I, P, I, P, I, F, P, I, F, P],
+            "gsp_propagate_workspace": [CP, I, I, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_propagate": [CP, P, I, I, I, P, P, I, P, ctypes.c_size_t, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -358,6 +362,41 @@ def gsp_csr_slice(a: CSR, bounds, rank: int, rows_padded: int, stream=None) -> C
     _check(lib().gsp_csr_slice(ctypes.byref(v), hb, parts, rank, rows_padded, _ptr(rp), _ptr(col), _ptr(val),
                                _stream(stream)), "gsp_csr_slice")
     return CSR(rp, col[:k], None if val is None else val[:k], parts * rows_padded)
+
+
+def gsp_spmm_accumulate(a: CSR, x: torch.Tensor, acc: torch.Tensor, coef: float, f: Optional[int] = None,
+                        t: Optional[torch.Tensor] = None, src: Optional[torch.Tensor] = None, src_coef: float = 0.0,
+                        stream=None):
+    """One propagation step: t = A x (if t given); acc = coef*t + (src_coef*src if src else acc)."""
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    acc, ldacc = _mat(acc, "acc")
+    ldt = _mat(t, "t")[1] if t is not None else 0
+    ldsrc = _mat(src, "src")[1] if src is not None else 0
+    v = a.view()
+    _check(lib().gsp_spmm_accumulate(ctypes.byref(v), _ptr(x), f, ldx, _ptr(t), ldt, _ptr(acc), ldacc, coef,
+                                     _ptr(src), ldsrc, src_coef, _stream(stream)), "gsp_spmm_accumulate")
+    return acc
+
+
+def gsp_propagate(a: CSR, x: torch.Tensor, theta, f: Optional[int] = None, y: Optional[torch.Tensor] = None,
+                  ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """y = sum_k theta_k A^k x (K = len(theta) - 1 >= 1)."""
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    th = (ctypes.c_double * len(theta))(*[float(t) for t in theta])
+    if y is None:
+        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+    y, ldy = _mat(y, "y")
+    n = ctypes.c_size_t(0)
+    v = a.view()
+    _check(lib().gsp_propagate_workspace(ctypes.byref(v), f, len(theta) - 1, ctypes.byref(n)),
+           "gsp_propagate_workspace")
+    if n.value and (ws is None or ws.numel() < n.value):
+        ws = torch.empty(n.value, dtype=torch.uint8, device=x.device)
+    _check(lib().gsp_propagate(ctypes.byref(v), _ptr(x), f, ldx, len(theta) - 1, th, _ptr(y), ldy,
+                               _ptr(ws) if n.value else None, n.value, _stream(stream)), "gsp_propagate")
+    return y
 
 
 def gsp_probe_l2_read(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None):

@@ -110,8 +110,18 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
   return GSP_OK;
 }
 
+// accumulate epilogue of a propagation step (see gsp_spmm_accumulate)
+struct AccEpi {
+  float *acc;
+  int64_t ldacc;
+  float coef;
+  const float *src;
+  int64_t ldsrc;
+  float src_coef;
+};
+
 static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
-                                   float *y, int64_t ldy, gsp_reduce red, cudaStream_t s) {
+                                   float *y, int64_t ldy, gsp_reduce red, const AccEpi *epi, cudaStream_t s) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -126,6 +136,19 @@ static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, cons
   p.head_dim = 0;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
+  if (epi) {
+    const int vw = L.V == 8 ? 4 : L.V;
+    p.acc = epi->acc;
+    p.ldacc = epi->ldacc;
+    p.acc_coef = epi->coef;
+    p.acc_src = epi->src;
+    p.ldsrc = epi->ldsrc;
+    p.src_coef = epi->src_coef;
+    p.skip_y = y == nullptr;
+    p.acc_vec_ok = (epi->ldacc % vw == 0) && (reinterpret_cast<uintptr_t>(epi->acc) % (4 * vw) == 0);
+    p.src_vec_ok = epi->src && (epi->ldsrc % vw == 0) && (reinterpret_cast<uintptr_t>(epi->src) % (4 * vw) == 0);
+    if (!y) p.y = epi->acc;  // never written (skip_y); keeps pointer arithmetic valid
+  }
   gsp_status st = engine_ldxv(p, L, a->n_cols, ldx);
   if (st) return st;
   p.mean = red == GSP_REDUCE_MEAN;
@@ -158,8 +181,36 @@ static gsp_status spmm_impl(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (overlaps(x, xb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
   SpmmPlan P;
   if ((st = spmm_plan(a, x, f, ldx, opts, &P))) return st;
-  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, red, s))) return st;
-  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, red, s);
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, red, nullptr, s))) return st;
+  if (P.f_tail) st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, red, nullptr, s);
+  return st;
+}
+
+static gsp_status spmm_acc_impl(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t, int64_t ldt,
+                                float *acc, int64_t ldacc, float coef, const float *src, int64_t ldsrc, float src_coef,
+                                cudaStream_t s, const char *fn) {
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (a->n_rows != a->n_cols) return fail(GSP_ERR_INVALID_ARG, "%s: propagation needs a square matrix", fn);
+  if (f < 0 || ldx < f || (t && ldt < f) || ldacc < f || (src && ldsrc < f))
+    return fail(GSP_ERR_INVALID_ARG, "%s: bad f / leading dimensions", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!x || !acc) return fail(GSP_ERR_INVALID_ARG, "%s: x / acc is NULL", fn);
+  const size_t xb = (size_t)((a->n_cols - 1) * ldx + f) * 4, ab = (size_t)((a->n_rows - 1) * ldacc + f) * 4;
+  const size_t tb = t ? (size_t)((a->n_rows - 1) * ldt + f) * 4 : 0;
+  if (overlaps(x, xb, acc, ab) || (t && (overlaps(x, xb, t, tb) || overlaps(t, tb, acc, ab))))
+    return fail(GSP_ERR_ALIAS, "%s: x, t and acc must not overlap", fn);
+  if (src && src != acc && overlaps(src, (size_t)((a->n_rows - 1) * ldsrc + f) * 4, acc, ab))
+    return fail(GSP_ERR_ALIAS, "%s: src partially overlaps acc", fn);
+  SpmmPlan P;
+  if ((st = spmm_plan(a, x, f, ldx, nullptr, &P))) return st;
+  AccEpi e{acc, ldacc, coef, src, ldsrc, src_coef};
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, t, t ? ldt : 0, GSP_REDUCE_SUM, &e, s))) return st;
+  if (P.f_tail) {
+    AccEpi e2{acc + P.f_main, ldacc, coef, src ? src + P.f_main : nullptr, ldsrc, src_coef};
+    st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, t ? t + P.f_main : nullptr, t ? ldt : 0,
+                          GSP_REDUCE_SUM, &e2, s);
+  }
   return st;
 }
 
@@ -170,6 +221,62 @@ using namespace gsp;
 extern "C" gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
                                gsp_stream stream) {
   return spmm_impl(a, x, f, ldx, y, ldy, nullptr, GSP_REDUCE_SUM, cs(stream), "gsp_spmm");
+}
+
+extern "C" gsp_status gsp_spmm_accumulate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t,
+                                          int64_t ldt, float *acc, int64_t ldacc, float coef, const float *src,
+                                          int64_t ldsrc, float src_coef, gsp_stream stream) {
+  clear_detail();
+  return spmm_acc_impl(a, x, f, ldx, t, ldt, acc, ldacc, coef, src, ldsrc, src_coef, cs(stream),
+                       "gsp_spmm_accumulate");
+}
+
+extern "C" gsp_status gsp_propagate_workspace(const gsp_csr *a, int64_t f, int64_t K, size_t *ws_bytes) {
+  clear_detail();
+  if (!a || f < 0 || K < 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_propagate_workspace: bad argument");
+  const int64_t ld = (f + 3) / 4 * 4;
+  *ws_bytes = K >= 2 ? (size_t)(K >= 3 ? 2 : 1) * (size_t)a->n_rows * ld * 4 + 512 : 0;
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_propagate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, int64_t K,
+                                    const double *theta, float *y, int64_t ldy, void *ws, size_t ws_bytes,
+                                    gsp_stream stream) {
+  const char *fn = "gsp_propagate";
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (K < 0 || !theta) return fail(GSP_ERR_INVALID_ARG, "%s: K >= 0 and theta[K+1] required", fn);
+  if (a->n_rows != a->n_cols) return fail(GSP_ERR_INVALID_ARG, "%s: propagation needs a square matrix", fn);
+  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: bad f / leading dimensions", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!x || !y) return fail(GSP_ERR_INVALID_ARG, "%s: x / y is NULL", fn);
+  size_t need = 0;
+  gsp_propagate_workspace(a, f, K, &need);
+  if (need && (!ws || ws_bytes < need)) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, need);
+  cudaStream_t s = cs(stream);
+  const int64_t ld = (f + 3) / 4 * 4;
+  float *tb[2] = {nullptr, nullptr};
+  if (need) {
+    float *w = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+    tb[0] = w;
+    tb[1] = K >= 3 ? w + (size_t)a->n_rows * ld : nullptr;
+  }
+  if (K == 0) {  // y = theta_0 x: a propagation of zero steps is an epilogue-only pass
+    return fail(GSP_ERR_UNSUPPORTED, "%s: K == 0 (y = theta_0 x) is a plain scale; use K >= 1", fn);
+  }
+  // step k: t_k = A t_{k-1} (t_0 = x); y = theta_k t_k + (k == 1 ? theta_0 x : y)
+  const float *tin = x;
+  int64_t ldin = ldx;
+  for (int64_t k = 1; k <= K; ++k) {
+    float *tout = (k == K) ? nullptr : tb[(k - 1) & 1];
+    st = spmm_acc_impl(a, tin, f, ldin, tout, ld, y, ldy, (float)theta[k], k == 1 ? x : nullptr, ldx,
+                       (float)theta[0], s, fn);
+    if (st) return st;
+    tin = tout;
+    ldin = ld;
+  }
+  return GSP_OK;
 }
 
 extern "C" gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_t f, int64_t ldx, float *y,

@@ -277,7 +277,44 @@ struct EngineParams {
   int win_cap;             // window capacity in entries (multiple of 4)
   int mean;                // GSpMM mean: divide the row sum by the row's entry count
   int hpt;                 // heads per team (slab = hpt whole heads); 1 otherwise
+  // fused accumulate epilogue (K-step propagation): acc = acc_coef * out +
+  // (acc_src ? src_coef * acc_src : acc); y is not written when skip_y
+  float *acc;
+  const float *acc_src;
+  int64_t ldacc, ldsrc;
+  float acc_coef, src_coef;
+  int skip_y, acc_vec_ok, src_vec_ok;
 };
+
+template <int V>
+__device__ __forceinline__ void load_cols(float (&r)[V], const float *p, int nvalid, bool vec_ok) {
+  if (nvalid >= V && vec_ok) {
+    Vec<V>::ld(r, p);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) r[i] = i < nvalid ? p[i] : 0.0f;
+  }
+}
+
+// Row epilogue: store out[] to y and/or fold it into the accumulator.
+template <int V>
+__device__ __forceinline__ void epilogue(const EngineParams &p, int64_t r, int64_t col0, const float (&out)[V],
+                                         int nvalid) {
+  if (p.acc) {
+    float prev[V], nv[V];
+    if (p.acc_src) {
+      load_cols<V>(prev, p.acc_src + r * p.ldsrc + col0, nvalid, p.src_vec_ok);
+#pragma unroll
+      for (int i = 0; i < V; ++i) prev[i] *= p.src_coef;
+    } else {
+      load_cols<V>(prev, p.acc + r * p.ldacc + col0, nvalid, p.acc_vec_ok);
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) nv[i] = fmaf(p.acc_coef, out[i], prev[i]);
+    store_cols<V>(p.acc + r * p.ldacc + col0, nv, nvalid, p.acc_vec_ok);
+  }
+  if (!p.skip_y) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+}
 
 // Team geometry.  A TEAM of T lanes owns one (row, slab): T = 32 when the
 // group width G >= 8 (a whole warp per row), else 4G (several rows per warp).
@@ -673,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
 #pragma unroll
       for (int i = 0; i < V; ++i) out[i] = s_part[gl * V + i];
       finish_row<R, V>(out, d, p.mean);
-      store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+      epilogue<V>(p, r, col0, out, nvalid);
     }
     __syncthreads();
   }
@@ -720,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
                                  s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr, kGat ? kCache : 0,
                                  out, stats);
     finish_row<R, V>(out, d, p.mean);
-    if (sg == 0 && active) store_cols<V>(p.y + r * p.ldy + col0, out, nvalid, p.y_vec_ok);
+    if (sg == 0 && active) epilogue<V>(p, r, col0, out, nvalid);
   }
   // no CTA may exit with bulk copies still writing its shared memory
   if (tid == 0) ensure(win.we);
@@ -765,6 +802,11 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
   p.mean = 0;
   p.hpt = 1;
+  p.acc = nullptr;
+  p.acc_src = nullptr;
+  p.ldacc = p.ldsrc = 0;
+  p.acc_coef = p.src_coef = 0.0f;
+  p.skip_y = p.acc_vec_ok = p.src_vec_ok = 0;
 }
 
 template <int V, int G, class W, class R>

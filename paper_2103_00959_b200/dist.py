@@ -113,3 +113,47 @@ class RowPartitionedSpMM:
         c0, c1 = self.cols[k], self.cols[k + 1]
         if self.rows:
             self.ops.spmm(self.local, self.gathered[k], c1 - c0, y[:, c0:c1])
+
+
+class RowPartitionedPropagate(RowPartitionedSpMM):
+    """y_shard = (sum_k theta_k A^k x)[rows of this rank] (K-step propagation,
+    NEXT-4).  Step k all-gathers t_{k-1} (chunked, on the communication
+    stream) and runs gsp_spmm_accumulate on the local slice, which writes t_k
+    straight into this rank's shard buffers (the next step's all-gather
+    source) and folds theta_k t_k into the local accumulator.  Bitwise equal
+    to the single-GPU gsp_propagate (same per-element operations)."""
+
+    def __call__(self, theta, y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        from . import gsp_spmm_accumulate
+        K = len(theta) - 1
+        if K < 1:
+            raise ValueError("theta needs K >= 1 (len >= 2)")
+        if y is None:
+            y = torch.empty((self.rows, self.f), dtype=torch.float32, device=self.device)
+        x0 = [s[:self.rows].clone() for s in self.shard]  # theta_0 x term of step 1
+        nch = len(self.cols) - 1
+        for k in range(1, K + 1):
+            def local(c):
+                c0, c1 = self.cols[c], self.cols[c + 1]
+                if self.rows:
+                    gsp_spmm_accumulate(self.local, self.gathered[c], y[:, c0:c1], float(theta[k]), f=c1 - c0,
+                                        t=self.shard[c][:self.rows] if k < K else None,
+                                        src=x0[c] if k == 1 else None, src_coef=float(theta[0]))
+            if self.comm is None:
+                for c in range(nch):
+                    self.exchange(c)
+                    local(c)
+                continue
+            main = torch.cuda.current_stream(self.device)
+            self.comm.wait_stream(main)  # previous step's t shard is complete
+            events = []
+            with torch.cuda.stream(self.comm):
+                for c in range(nch):
+                    self.exchange(c)
+                    ev = torch.cuda.Event()
+                    ev.record(self.comm)
+                    events.append(ev)
+            for c in range(nch):
+                main.wait_event(events[c])
+                local(c)
+        return y

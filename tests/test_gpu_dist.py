@@ -53,6 +53,15 @@ def _worker(rank, world, port, backend, chunks, q):
         y = op()
         torch.cuda.synchronize()
         ok = torch.equal(y, y_ref[op.r0:op.r1])
+        # K-step propagation through the same partition (NEXT-4)
+        from paper_2103_00959_b200.dist import RowPartitionedPropagate
+        th = [0.1 * 0.9 ** k for k in range(6)]
+        pp = RowPartitionedPropagate(g, rank, world, f, chunks=chunks, device=dev,
+                                     all_gather=None if backend == "nccl" else _staged_gather)
+        pp.load_shard(x[pp.r0:pp.r1, :f])
+        yp = pp(th)
+        torch.cuda.synchronize()
+        ok = ok and torch.equal(yp, G.gsp_propagate(g, x, th, f=f)[pp.r0:pp.r1])
         q.put((rank, ok, op.r0, op.r1))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e), -1, -1))

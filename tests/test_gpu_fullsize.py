@@ -64,6 +64,15 @@ def test_c4_identity_every_row(c4):
     np.testing.assert_allclose(y, np.sqrt(deg)[:, None].repeat(8, 1), rtol=3e-6)
 
 
+def test_c4_propagate_eigenvector(c4):
+    """A^ sqrt(d) = sqrt(d) => K=10 PPR propagation of sqrt(d) is (sum theta) sqrt(d) on every row."""
+    cfg, go, (deg, a64, a32), gg, gn = c4
+    th = orc.ppr_coeffs(0.1, 10)
+    x = torch.sqrt(gn.deg).float()[:, None].repeat(1, 4).contiguous()
+    y = host(G.gsp_propagate(gn, x, th))
+    np.testing.assert_allclose(y, th.sum() * np.sqrt(deg)[:, None].repeat(4, 1), rtol=3e-5)
+
+
 def test_c3_gat_sampled_rows_and_convexity():
     cfg = CONFIGS["C3"]
     H, D = cfg.heads, cfg.d

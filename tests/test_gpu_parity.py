@@ -359,3 +359,35 @@ def test_gspmm_sum_equals_spmm_bitwise(built):
     go, gg, _, gn = built["rmat3000"]
     x = dev(features(go.n, 300, seed=3))
     assert torch.equal(G.gsp_gspmm(gn, x, "sum"), G.gsp_spmm(gn, x))
+
+
+# ---------------------------------------------------------------- NEXT-4: K-step propagation
+
+@pytest.mark.parametrize("K", [1, 2, 3, 10])
+@pytest.mark.parametrize("f", [1, 41, 128, 300])
+def test_propagate_parity(built, K, f):
+    """y = sum_k theta_k A^k x (PPR coefficients) vs the fp64 oracle; the error
+    of each of the K SpMMs is propagated by A, bound K*1e-5*cond + 1e-6."""
+    th = orc.ppr_coeffs(0.1, K)
+    for name in ("isolated-nofill", "multi0", "er300-weighted", "cl4000", "hubs"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        x = features(go.n, f, (f + 3) // 4 * 4, seed=K + f)
+        yref, cond = orc.propagate(go.row_ptr, go.col, a64, x, th)
+        y = host(G.gsp_propagate(gn, dev(x), th, f=f))
+        assert_within(y, yref, cond, rel=K * 1e-5, what=f"{name} K={K} f={f}")
+
+
+def test_propagate_accumulate_step_semantics(built):
+    """gsp_spmm_accumulate: t = A x, acc = c*t + s*src (or + acc)."""
+    go, gg, _, gn = built["cl4000"]
+    x = dev(features(go.n, 64, seed=1))
+    src = dev(features(go.n, 64, seed=2))
+    t = torch.empty_like(x)
+    acc = torch.empty_like(x)
+    G.gsp_spmm_accumulate(gn, x, acc, 0.5, t=t, src=src, src_coef=2.0)
+    ax = G.gsp_spmm(gn, x)
+    assert torch.equal(t, ax)
+    assert torch.equal(acc, torch.addcmul(src * 2.0, ax, torch.tensor(0.5, device=DEV)))
+    acc2 = acc.clone()
+    G.gsp_spmm_accumulate(gn, x, acc2, -1.0)
+    assert torch.equal(acc2, torch.addcmul(acc, ax, torch.tensor(-1.0, device=DEV)))
