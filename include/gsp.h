@@ -176,7 +176,8 @@ gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_
  * gsp_spmm_accumulate is one step with the fused epilogue:
  *   t = A x                        (written to t unless t == NULL)
  *   acc = coef * t + (src != NULL ? src_coef * src : acc)      (fp32 fma)
- * It is the building block of the row-partitioned multi-GPU propagation. */
+ * It is the building block of the row-partitioned multi-GPU propagation
+ * (A may be a rectangular slice there: x has n_cols rows, t/acc/src n_rows). */
 gsp_status gsp_spmm_accumulate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t, int64_t ldt,
                                float *acc, int64_t ldacc, float coef, const float *src, int64_t ldsrc,
                                float src_coef, gsp_stream stream);

@@ -191,12 +191,12 @@ static gsp_status spmm_acc_impl(const gsp_csr *a, const float *x, int64_t f, int
                                 cudaStream_t s, const char *fn) {
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
-  if (a->n_rows != a->n_cols) return fail(GSP_ERR_INVALID_ARG, "%s: propagation needs a square matrix", fn);
   if (f < 0 || ldx < f || (t && ldt < f) || ldacc < f || (src && ldsrc < f))
     return fail(GSP_ERR_INVALID_ARG, "%s: bad f / leading dimensions", fn);
   if (a->n_rows == 0 || f == 0) return GSP_OK;
   if (!x || !acc) return fail(GSP_ERR_INVALID_ARG, "%s: x / acc is NULL", fn);
-  const size_t xb = (size_t)((a->n_cols - 1) * ldx + f) * 4, ab = (size_t)((a->n_rows - 1) * ldacc + f) * 4;
+  const size_t xb = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 4 : 0;
+  const size_t ab = (size_t)((a->n_rows - 1) * ldacc + f) * 4;
   const size_t tb = t ? (size_t)((a->n_rows - 1) * ldt + f) * 4 : 0;
   if (overlaps(x, xb, acc, ab) || (t && (overlaps(x, xb, t, tb) || overlaps(t, tb, acc, ab))))
     return fail(GSP_ERR_ALIAS, "%s: x, t and acc must not overlap", fn);
