@@ -372,7 +372,7 @@ def test_propagate_parity(built, K, f):
     for name in ("isolated-nofill", "multi0", "er300-weighted", "cl4000", "hubs"):
         go, gg, (deg, a64, a32), gn = built[name]
         x = features(go.n, f, (f + 3) // 4 * 4, seed=K + f)
-        yref, cond = orc.propagate(go.row_ptr, go.col, a64, x, th)
+        yref, cond = orc.propagate(go.row_ptr, go.col, a64, x, th, f=f)
         y = host(G.gsp_propagate(gn, dev(x), th, f=f))
         assert_within(y, yref, cond, rel=K * 1e-5, what=f"{name} K={K} f={f}")
 
