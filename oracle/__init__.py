@@ -56,9 +56,14 @@ def lib():
         L.orc_multihead_spmm.argtypes = [I, I, P, P, I, P, P, I, I, P, P, I]
         L.orc_attn_project.argtypes = [I, I, I, I, P, I, P, P, P, P, P, P]
         L.orc_partition_rows.argtypes = [I, P, I, P]
+        L.orc_sddmm.argtypes = [I, P, P, I, I, P, I, P, I, P]
+        L.orc_csr_transpose.argtypes = [I, I, P, P, P, P, P]
+        L.orc_edge_softmax_backward.argtypes = [I, P, I, P, P, P]
+        L.orc_gat_backward.argtypes = [I, P, P, I, P, P, ctypes.c_double, P, I, I, P, I, P, P, P, P]
         L.orc_csr_slice.argtypes = [I, P, P, P, P, I, I, I, P, P, P]
         for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_propagate", "orc_ppr_coeffs", "orc_edge_softmax", "orc_gat_scores",
-                  "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice"):
+                  "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice", "orc_sddmm",
+                  "orc_csr_transpose", "orc_edge_softmax_backward", "orc_gat_backward"):
             getattr(L, f).restype = ctypes.c_int
     return _lib
 
@@ -257,3 +262,55 @@ def csr_slice(row_ptr, col, val, bounds, rank, rows_padded):
     _chk(lib().orc_csr_slice(row_ptr.size - 1, _p(row_ptr), _p(col), _p(val), _p(bounds), parts, rank,
                              rows_padded, _p(rp), _p(co), _p(vo)))
     return rp, co[:k], vo[:k]
+
+
+def sddmm(row_ptr, col, p, q, heads=1, d=None):
+    """out fp64 [nnz, heads] = per-edge per-head dot(p[u], q[v]) (oracle.c §10a)."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    p = np.ascontiguousarray(p, dtype=np.float32)
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    d = p.shape[1] // heads if d is None else d
+    out = np.zeros(max(int(row_ptr[-1]) * heads, 1), np.float64)
+    _chk(lib().orc_sddmm(row_ptr.size - 1, _p(row_ptr), _p(col), heads, d, _p(p), p.shape[1], _p(q), q.shape[1],
+                         _p(out)))
+    return out[:int(row_ptr[-1]) * heads].reshape(-1, heads)
+
+
+def csr_transpose(row_ptr, col, n_cols):
+    """(row_ptr_t, col_t, perm) of A^T (oracle.c §10b)."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    nnz = int(row_ptr[-1])
+    rp = np.zeros(n_cols + 1, np.int64)
+    ct = np.zeros(max(nnz, 1), np.int32)
+    pm = np.zeros(max(nnz, 1), np.int64)
+    _chk(lib().orc_csr_transpose(row_ptr.size - 1, n_cols, _p(row_ptr), _p(col), _p(rp), _p(ct), _p(pm)))
+    return rp, ct[:nnz], pm[:nnz]
+
+
+def edge_softmax_backward(row_ptr, alpha, dalpha, heads=1):
+    row_ptr = _c(row_ptr, np.int64)
+    a = np.ascontiguousarray(alpha, dtype=np.float64).reshape(-1)
+    da = np.ascontiguousarray(dalpha, dtype=np.float64).reshape(-1)
+    ds = np.zeros(max(a.size, 1), np.float64)
+    _chk(lib().orc_edge_softmax_backward(row_ptr.size - 1, _p(row_ptr), heads, _p(a), _p(da), _p(ds)))
+    return ds[:a.size].reshape(-1, heads)
+
+
+def gat_backward(row_ptr, col, el, er, z, dy, heads, d, slope=0.2):
+    """(dz [n, H*D], d_el [n, H], d_er [n, H], dt [nnz, H]) fp64 (oracle.c §10d)."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    el = np.ascontiguousarray(el, dtype=np.float32)
+    er = np.ascontiguousarray(er, dtype=np.float32)
+    z = np.ascontiguousarray(z, dtype=np.float32)
+    dy = np.ascontiguousarray(dy, dtype=np.float32)
+    n = row_ptr.size - 1
+    dz = np.zeros((n, heads * d), np.float64)
+    d_el = np.zeros((n, heads), np.float64)
+    d_er = np.zeros((n, heads), np.float64)
+    dt = np.zeros(max(int(row_ptr[-1]) * heads, 1), np.float64)
+    _chk(lib().orc_gat_backward(n, _p(row_ptr), _p(col), heads, _p(el), _p(er), float(slope), _p(z), d, z.shape[1],
+                                _p(dy), dy.shape[1], _p(dz), _p(d_el), _p(d_er), _p(dt)))
+    return dz, d_el, d_er, dt[:int(row_ptr[-1]) * heads].reshape(-1, heads)

@@ -367,6 +367,111 @@ int orc_attn_project(int64_t r0, int64_t r1, int64_t heads, int64_t d, const flo
 }
 
 /* ---------------------------------------------------------------------------
+ * 10. GAT backward (NEXT-3).  P:652 [§4.1: SDDMM T = A (.) (P Q^T) "is used
+ *     for back-propagating the gradients to the sparse adjacency matrix since
+ *     the adjacency matrix of the GAT model is computed by the attention
+ *     mechanism"]; S:153-161 (sddmm), S:237-245 (spmm_var backward).
+ *
+ * 10a. Multi-head SDDMM: out[e,h] = sum_k p[u,h,k] q[v,h,k], e = (u,v).
+ *      Structural: A's values are not multiplied in.
+ * ------------------------------------------------------------------------- */
+int orc_sddmm(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t heads, int64_t d, const float *p,
+              int64_t ldp, const float *q, int64_t ldq, double *out) {
+  if (n < 0 || heads <= 0 || d < 0 || ldp < heads * d || ldq < heads * d || !row_ptr || !p || !q || !out)
+    return ORC_ERR_ARG;
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e)
+      for (int64_t h = 0; h < heads; ++h) {
+        double s = 0.0;
+        for (int64_t k = 0; k < d; ++k)
+          s += (double)p[u * ldp + h * d + k] * (double)q[(int64_t)col[e] * ldq + h * d + k];
+        out[e * heads + h] = s;
+      }
+  return ORC_OK;
+}
+
+/* 10b. Transpose of a CSR with n_cols columns: rows of A^T are A's columns,
+ *      entries in increasing original row; perm[e'] = index in A of entry e'
+ *      of A^T.  Plain counting by column. */
+int orc_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t *row_ptr, const int32_t *col,
+                      int64_t *rp_t, int32_t *col_t, int64_t *perm) {
+  if (n_rows < 0 || n_cols < 0 || !row_ptr || !rp_t) return ORC_ERR_ARG;
+  const int64_t nnz = row_ptr[n_rows];
+  for (int64_t c = 0; c <= n_cols; ++c) rp_t[c] = 0;
+  for (int64_t e = 0; e < nnz; ++e) rp_t[col[e] + 1] += 1;
+  for (int64_t c = 0; c < n_cols; ++c) rp_t[c + 1] += rp_t[c];
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_cols > 0 ? n_cols : 1));
+  if (!fill) return ORC_ERR_NOMEM;
+  for (int64_t c = 0; c < n_cols; ++c) fill[c] = rp_t[c];
+  for (int64_t u = 0; u < n_rows; ++u)
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      const int64_t k = fill[col[e]]++;
+      col_t[k] = (int32_t)u;
+      perm[k] = e;
+    }
+  free(fill);
+  return ORC_OK;
+}
+
+/* 10c. Edge-softmax backward (the Jacobian of §4 per row and head):
+ *      ds[e] = alpha[e] * (dalpha[e] - sum_{e' in row} alpha[e'] dalpha[e']). */
+int orc_edge_softmax_backward(int64_t n, const int64_t *row_ptr, int64_t heads, const double *alpha,
+                              const double *dalpha, double *ds) {
+  if (n < 0 || heads <= 0 || !row_ptr || !alpha || !dalpha || !ds) return ORC_ERR_ARG;
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t h = 0; h < heads; ++h) {
+      double dot = 0.0;
+      for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) dot += alpha[e * heads + h] * dalpha[e * heads + h];
+      for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e)
+        ds[e * heads + h] = alpha[e * heads + h] * (dalpha[e * heads + h] - dot);
+    }
+  return ORC_OK;
+}
+
+/* 10d. Backward of the fused GAT aggregate (§5 scores, §4 softmax, §6 SpMM)
+ *      given dY [n][H][D]:
+ *        dalpha[e,h] = sum_k dY[u,h,k] z[v,h,k]                (SDDMM)
+ *        dz[v,h,:]  += alpha[e,h] dY[u,h,:]                     (A^T SpMM)
+ *        ds = softmax backward;  dt = ds * (t >= 0 ? 1 : slope),  t = el[u]+er[v]
+ *        d_el[u,h] = sum_{e in row u} dt[e,h];  d_er[v,h] = sum_{e=(u,v)} dt[e,h]
+ *      alpha is recomputed here from el, er (fp64).  dt (nullable) [nnz][H]. */
+int orc_gat_backward(int64_t n, const int64_t *row_ptr, const int32_t *col, int64_t heads, const float *el,
+                     const float *er, double slope, const float *z, int64_t d, int64_t ldz, const float *dy,
+                     int64_t lddy, double *dz, double *d_el, double *d_er, double *dt_out) {
+  if (n < 0 || heads <= 0 || d < 0 || !row_ptr || !el || !er || !z || !dy || !dz || !d_el || !d_er)
+    return ORC_ERR_ARG;
+  const int64_t nnz = row_ptr[n], H = heads;
+  double *s = (double *)malloc(sizeof(double) * (size_t)(nnz * H > 0 ? nnz * H : 1));
+  double *al = (double *)malloc(sizeof(double) * (size_t)(nnz * H > 0 ? nnz * H : 1));
+  double *da = (double *)malloc(sizeof(double) * (size_t)(nnz * H > 0 ? nnz * H : 1));
+  double *ds = (double *)malloc(sizeof(double) * (size_t)(nnz * H > 0 ? nnz * H : 1));
+  if (!s || !al || !da || !ds) { free(s); free(al); free(da); free(ds); return ORC_ERR_NOMEM; }
+  int rc = orc_gat_scores(0, n, row_ptr, col, H, el, er, slope, s);
+  if (!rc) rc = orc_edge_softmax(0, n, row_ptr, H, s, al);
+  if (!rc) rc = orc_sddmm(n, row_ptr, col, H, d, dy, lddy, z, ldz, da);
+  if (!rc) rc = orc_edge_softmax_backward(n, row_ptr, H, al, da, ds);
+  if (!rc) {
+    for (int64_t v = 0; v < n; ++v)
+      for (int64_t k = 0; k < H * d; ++k) dz[v * H * d + k] = 0.0;
+    for (int64_t v = 0; v < n * H; ++v) { d_el[v] = 0.0; d_er[v] = 0.0; }
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+        const int64_t v = col[e];
+        for (int64_t h = 0; h < H; ++h) {
+          const double t = (double)el[u * H + h] + (double)er[v * H + h];
+          const double dt = ds[e * H + h] * (t >= 0.0 ? 1.0 : slope);
+          if (dt_out) dt_out[e * H + h] = dt;
+          d_el[u * H + h] += dt;
+          d_er[v * H + h] += dt;
+          for (int64_t k = 0; k < d; ++k) dz[v * H * d + h * d + k] += al[e * H + h] * (double)dy[u * lddy + h * d + k];
+        }
+      }
+  }
+  free(s); free(al); free(da); free(ds);
+  return rc;
+}
+
+/* ---------------------------------------------------------------------------
  * 8. Row partition balanced by nnz (DESIGN.md multi-GPU):
  *    bound_p = lower_bound(row_ptr[0..n], ceil(p * nnz / P)) for 0 < p < P,
  *    bound_0 = 0, bound_P = n.  lower_bound = first r with row_ptr[r] >= t.

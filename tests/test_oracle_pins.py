@@ -516,3 +516,107 @@ def test_propagate_sqrt_degree_eigenvector():
     th = orc.ppr_coeffs(0.1, 10)
     y, _ = orc.propagate(g.row_ptr, g.col, a64, x, th)
     np.testing.assert_allclose(y[:, 0], th.sum() * np.sqrt(deg), rtol=3e-7)
+
+
+# ---------------------------------------------------------------------------
+# 10. GAT backward pieces (oracle.c §10, NEXT-3)
+# ---------------------------------------------------------------------------
+
+def test_sddmm_spec_examples(golden):
+    for case in golden["spec_examples"]["sddmm"]:
+        e = np.array(case["edges"], np.int64).reshape(-1, 2)
+        g = orc.build_csr(case["n"], e[:, 0], e[:, 1], None, False, 0.0)
+        t = orc.sddmm(g.row_ptr, g.col, np.array(case["p"], np.float32), np.array(case["q"], np.float32))
+        np.testing.assert_array_equal(t[:, 0], case["t"]), case["cite"]
+    # self-loops only, p = q -> ||p[u]||^2
+    p = uniform((7, 5), seed=3)
+    g = orc.build_csr(7, [], [], None, False, 1.0)
+    t = orc.sddmm(g.row_ptr, g.col, p, p)
+    np.testing.assert_allclose(t[:, 0], (p.astype(np.float64) ** 2).sum(1), rtol=1e-15)
+
+
+def test_sddmm_equals_masked_dense_product():
+    """masking dense P Q^T by A's pattern equals sddmm (per head)."""
+    s, d = chung_lu(300, 2000, seed=4)
+    g = orc.build_csr(300, s, d, None, True, 1.0)
+    H, D = 3, 5
+    p = uniform((300, H * D), seed=5)
+    q = uniform((300, H * D), seed=6)
+    t = orc.sddmm(g.row_ptr, g.col, p, q, heads=H)
+    rows = np.repeat(np.arange(300), np.diff(g.row_ptr))
+    for h in range(H):
+        PQ = p[:, h * D:(h + 1) * D].astype(np.float64) @ q[:, h * D:(h + 1) * D].astype(np.float64).T
+        np.testing.assert_allclose(t[:, h], PQ[rows, g.col], rtol=1e-12, atol=1e-14)
+
+
+def test_csr_transpose_vs_scipy():
+    import scipy.sparse as sp
+    rng = np.random.default_rng(8)
+    for t in range(10):
+        n, m = int(rng.integers(1, 60)), int(rng.integers(0, 300))
+        g = orc.build_csr(n, rng.integers(0, n, m), rng.integers(0, n, m), None, False, 0.0)
+        vals = np.arange(1, g.nnz + 1, dtype=np.float64)  # distinct values track the permutation
+        rp, ct, pm = orc.csr_transpose(g.row_ptr, g.col, n)
+        T = sp.csr_matrix((vals, g.col, g.row_ptr), shape=(n, n)).T.tocsr()
+        T.sort_indices()
+        np.testing.assert_array_equal(rp, T.indptr)
+        np.testing.assert_array_equal(ct, T.indices)
+        np.testing.assert_array_equal(vals[pm], T.data)
+        rp2, ct2, pm2 = orc.csr_transpose(rp, ct, n)  # (A^T)^T = A
+        np.testing.assert_array_equal(rp2, g.row_ptr)
+        np.testing.assert_array_equal(ct2, g.col)
+        np.testing.assert_array_equal(pm[pm2], np.arange(g.nnz))
+
+
+def test_edge_softmax_backward_vs_dense_jacobian():
+    """ds = J^T dalpha with the dense softmax Jacobian J = diag(a) - a a^T per row."""
+    s, d = chung_lu(200, 900, seed=2)
+    g = orc.build_csr(200, s, d, None, True, 1.0)
+    H = 2
+    lg = uniform((g.nnz, H), seed=3, low=-3, high=3).astype(np.float64)
+    a = orc.edge_softmax(g.row_ptr, lg, H)
+    da = uniform((g.nnz, H), seed=4).astype(np.float64)
+    ds = orc.edge_softmax_backward(g.row_ptr, a, da, H)
+    for u in range(0, 200, 7):
+        b, e = g.row_ptr[u], g.row_ptr[u + 1]
+        for h in range(H):
+            al = a[b:e, h]
+            J = np.diag(al) - np.outer(al, al)
+            np.testing.assert_allclose(ds[b:e, h], J.T @ da[b:e, h], rtol=1e-12, atol=1e-15)
+
+
+def test_gat_backward_vs_finite_differences():
+    """Central differences of L = <dY, Y(el, er, z)> through the FORWARD oracle
+    (gat_scores -> edge_softmax -> multihead_spmm).  Inputs are multiples of
+    2^-6 and eps = 2^-12, so x +- eps is exact in fp32; the O(eps^2) remainder
+    is far below the 1e-5 tolerance."""
+    rng = np.random.default_rng(12)
+    n, H, D = 40, 2, 3
+    s, d = erdos_renyi(n, 120, seed=5)
+    g = orc.build_csr(n, s, d, None, True, 1.0)
+    q = lambda shape: (rng.integers(-128, 128, shape) / 64.0).astype(np.float32)
+    el, er, z, dy = q((n, H)), q((n, H)), q((n, H * D)), q((n, H * D))
+
+    def loss(el_, er_, z_):
+        sc = orc.gat_scores(g.row_ptr, g.col, el_, er_, H, 0.2)
+        al = orc.edge_softmax(g.row_ptr, sc, H)
+        y, _ = orc.multihead_spmm(g.row_ptr, g.col, al, z_, H, D)
+        return float((y * dy.astype(np.float64)).sum())
+
+    dz, d_el, d_er, dt = orc.gat_backward(g.row_ptr, g.col, el, er, z, dy, H, D, 0.2)
+    eps = 2.0 ** -12
+    for arr, grad in ((el, d_el), (er, d_er), (z, dz)):
+        for _ in range(12):
+            i, j = int(rng.integers(0, arr.shape[0])), int(rng.integers(0, arr.shape[1]))
+            orig = arr[i, j]
+            arr[i, j] = orig + eps
+            lp = loss(el, er, z)
+            arr[i, j] = orig - eps
+            lm = loss(el, er, z)
+            arr[i, j] = orig
+            fd = (lp - lm) / (2 * eps)
+            assert abs(fd - grad[i, j]) <= 1e-5 * max(1.0, abs(fd)), (fd, grad[i, j])
+    # d_el is the row sum and d_er the column sum of dt
+    rows = np.repeat(np.arange(n), np.diff(g.row_ptr))
+    np.testing.assert_allclose(d_el, np.stack([np.bincount(rows, dt[:, h], n) for h in range(H)], 1), rtol=1e-12)
+    np.testing.assert_allclose(d_er, np.stack([np.bincount(g.col, dt[:, h], n) for h in range(H)], 1), rtol=1e-12)
