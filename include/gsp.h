@@ -261,6 +261,51 @@ gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const float *el, c
                              gsp_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-3: GAT backward.  P:652 (§4.1: SDDMM T = A (.) (P Q^T) "is used for
+ * back-propagating the gradients to the sparse adjacency matrix since the
+ * adjacency matrix of the GAT model is computed by the attention mechanism"),
+ * P:653-656 (edge softmax).
+ *
+ * gsp_csr_transpose: A^T in canonical form (n_cols rows) and perm[e'] = the
+ *   index in A of entry e' of A^T (so per-entry arrays of A can be read in A^T
+ *   order).  Outputs: row_ptr_t int64 [n_cols+1], col_t int32 [nnz],
+ *   perm int32 [nnz]; nnz < 2^31; ws >= gsp_csr_transpose_workspace bytes,
+ *   256-byte aligned.  Bit-exact (integer work).
+ * gsp_sddmm: out[e,h] = sum_k p[u,h,k] q[v,h,k] for e = (u,v) (structural:
+ *   A's values are not multiplied in).  p [n_rows][ldp], q [n_cols][ldq]
+ *   viewed as [H][D]; out fp32 [nnz][H].
+ * gsp_edge_softmax_backward: ds = alpha (dalpha - sum_row alpha dalpha) per
+ *   head (fp64 row dot); heads must divide 32.  ds may equal dalpha.
+ * gsp_gat_aggregate_backward: given dY of gsp_gat_aggregate (same a, el, er,
+ *   z, slope), writes dz [n][lddz] (= A^T_alpha dY, overwritten),
+ *   d_el [n][H] and d_er [n][H] (the LeakyReLU-score gradients; the score's
+ *   dependence on Z goes through gsp_attn_project_backward).  at/perm from
+ *   gsp_csr_transpose(a).  alpha is recomputed from el, er.  ws >=
+ *   gsp_gat_backward_workspace bytes.  Launches: softmax, SDDMM, fused
+ *   softmax/LeakyReLU backward with row sums, column sums, A^T SpMM.
+ * gsp_attn_project_backward: dz[u,h,:] += d_el[u,h] a_l[h,:] + d_er[u,h] a_r[h,:];
+ *   d_al[h,:] = sum_u d_el[u,h] z[u,h,:], d_ar likewise (fixed-order
+ *   reduction, fp64 partials in ws >= gsp_attn_project_backward_workspace). */
+gsp_status gsp_csr_transpose_workspace(const gsp_csr *a, size_t *ws_bytes);
+gsp_status gsp_csr_transpose(const gsp_csr *a, int64_t *row_ptr_t, int32_t *col_t, int32_t *perm, void *ws,
+                             size_t ws_bytes, gsp_stream stream);
+gsp_status gsp_sddmm(const gsp_csr *a, int32_t heads, const float *p, int64_t d, int64_t ldp, const float *q,
+                     int64_t ldq, float *out, gsp_stream stream);
+gsp_status gsp_edge_softmax_backward(const gsp_csr *a, int32_t heads, const float *alpha, const float *dalpha,
+                                     float *ds, gsp_stream stream);
+gsp_status gsp_gat_backward_workspace(const gsp_csr *a, int32_t heads, size_t *ws_bytes);
+gsp_status gsp_gat_aggregate_backward(const gsp_csr *a, const gsp_csr *at, const int32_t *perm, int32_t heads,
+                                      const float *el, const float *er, double negative_slope, const float *z,
+                                      int64_t d, int64_t ldz, const float *dy, int64_t lddy, float *dz,
+                                      int64_t lddz, float *d_el, float *d_er, void *ws, size_t ws_bytes,
+                                      gsp_stream stream);
+gsp_status gsp_attn_project_backward_workspace(int64_t n, int32_t heads, int64_t d, size_t *ws_bytes);
+gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const float *z, int64_t ldz,
+                                     const float *a_l, const float *a_r, const float *d_el, const float *d_er,
+                                     float *dz, int64_t lddz, float *d_al, float *d_ar, void *ws, size_t ws_bytes,
+                                     gsp_stream stream);
+
+/* ---------------------------------------------------------------------------
  * Multi-GPU row partition.
  * gsp_partition_rows: row_bounds[p] = first row r with row_ptr[r] >=
  *   ceil(p * nnz / parts) for 0 < p < parts; row_bounds[0] = 0,

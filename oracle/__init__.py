@@ -60,10 +60,11 @@ def lib():
         L.orc_csr_transpose.argtypes = [I, I, P, P, P, P, P]
         L.orc_edge_softmax_backward.argtypes = [I, P, I, P, P, P]
         L.orc_gat_backward.argtypes = [I, P, P, I, P, P, ctypes.c_double, P, I, I, P, I, P, P, P, P]
+        L.orc_attn_project_backward.argtypes = [I, I, I, P, I, P, P, P, P, P, P, P]
         L.orc_csr_slice.argtypes = [I, P, P, P, P, I, I, I, P, P, P]
         for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_propagate", "orc_ppr_coeffs", "orc_edge_softmax", "orc_gat_scores",
                   "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice", "orc_sddmm",
-                  "orc_csr_transpose", "orc_edge_softmax_backward", "orc_gat_backward"):
+                  "orc_csr_transpose", "orc_edge_softmax_backward", "orc_gat_backward", "orc_attn_project_backward"):
             getattr(L, f).restype = ctypes.c_int
     return _lib
 
@@ -314,3 +315,19 @@ def gat_backward(row_ptr, col, el, er, z, dy, heads, d, slope=0.2):
     _chk(lib().orc_gat_backward(n, _p(row_ptr), _p(col), heads, _p(el), _p(er), float(slope), _p(z), d, z.shape[1],
                                 _p(dy), dy.shape[1], _p(dz), _p(d_el), _p(d_er), _p(dt)))
     return dz, d_el, d_er, dt[:int(row_ptr[-1]) * heads].reshape(-1, heads)
+
+
+def attn_project_backward(z, a_l, a_r, d_el, d_er, heads, d):
+    """(dz [n, H*D], d_al [H*D], d_ar [H*D]) fp64 (oracle.c §10e)."""
+    z = np.ascontiguousarray(z, dtype=np.float32)
+    a_l = np.ascontiguousarray(a_l, dtype=np.float32).reshape(-1)
+    a_r = np.ascontiguousarray(a_r, dtype=np.float32).reshape(-1)
+    d_el = np.ascontiguousarray(d_el, dtype=np.float64)
+    d_er = np.ascontiguousarray(d_er, dtype=np.float64)
+    n = z.shape[0]
+    dz = np.zeros((n, heads * d), np.float64)
+    d_al = np.zeros(heads * d, np.float64)
+    d_ar = np.zeros(heads * d, np.float64)
+    _chk(lib().orc_attn_project_backward(n, heads, d, _p(z), z.shape[1], _p(a_l), _p(a_r), _p(d_el), _p(d_er),
+                                         _p(dz), _p(d_al), _p(d_ar)))
+    return dz, d_al, d_ar

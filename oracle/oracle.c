@@ -471,6 +471,26 @@ int orc_gat_backward(int64_t n, const int64_t *row_ptr, const int32_t *col, int6
   return rc;
 }
 
+/* 10e. Backward of the attention projection (§7): el = z.a_l, er = z.a_r per
+ *      head, so dz[u,h,:] = d_el[u,h] a_l[h,:] + d_er[u,h] a_r[h,:] and
+ *      d_al[h,:] = sum_u d_el[u,h] z[u,h,:] (d_ar likewise). */
+int orc_attn_project_backward(int64_t n, int64_t heads, int64_t d, const float *z, int64_t ldz, const float *a_l,
+                              const float *a_r, const double *d_el, const double *d_er, double *dz, double *d_al,
+                              double *d_ar) {
+  if (n < 0 || heads <= 0 || d < 0 || ldz < heads * d || !z || !a_l || !a_r || !d_el || !d_er || !dz || !d_al || !d_ar)
+    return ORC_ERR_ARG;
+  for (int64_t k = 0; k < heads * d; ++k) { d_al[k] = 0.0; d_ar[k] = 0.0; }
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t h = 0; h < heads; ++h)
+      for (int64_t k = 0; k < d; ++k) {
+        const int64_t c = h * d + k;
+        dz[u * heads * d + c] = d_el[u * heads + h] * (double)a_l[c] + d_er[u * heads + h] * (double)a_r[c];
+        d_al[c] += d_el[u * heads + h] * (double)z[u * ldz + c];
+        d_ar[c] += d_er[u * heads + h] * (double)z[u * ldz + c];
+      }
+  return ORC_OK;
+}
+
 /* ---------------------------------------------------------------------------
  * 8. Row partition balanced by nnz (DESIGN.md multi-GPU):
  *    bound_p = lower_bound(row_ptr[0..n], ceil(p * nnz / P)) for 0 < p < P,

@@ -33,7 +33,9 @@ EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "g
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
            "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
-           "gsp_propagate_workspace", "gsp_propagate")
+           "gsp_propagate_workspace", "gsp_propagate", "gsp_csr_transpose_workspace", "gsp_csr_transpose",
+           "gsp_sddmm", "gsp_edge_softmax_backward", "gsp_gat_backward_workspace", "gsp_gat_aggregate_backward",
+           "gsp_attn_project_backward_workspace", "gsp_attn_project_backward")
 
 
 class GspError(RuntimeError):
@@ -77,6 +79,14 @@ def lib() -> ctypes.CDLL:
             "gsp_spmm_accumulate": [CP, P, I, I, P, I, P, I, F, P, I, F, P],
             "gsp_propagate_workspace": [CP, I, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_propagate": [CP, P, I, I, I, P, P, I, P, ctypes.c_size_t, P],
+            "gsp_csr_transpose_workspace": [CP, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_csr_transpose": [CP, P, P, P, P, ctypes.c_size_t, P],
+            "gsp_sddmm": [CP, I32, P, I, I, P, I, P, P],
+            "gsp_edge_softmax_backward": [CP, I32, P, P, P, P],
+            "gsp_gat_backward_workspace": [CP, I32, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_gat_aggregate_backward": [CP, CP, P, I32, P, P, D, P, I, I, P, I, P, I, P, P, P, ctypes.c_size_t, P],
+            "gsp_attn_project_backward_workspace": [I, I32, I, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_attn_project_backward": [I, I32, I, P, I, P, P, P, P, P, I, P, P, P, ctypes.c_size_t, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -397,6 +407,93 @@ def gsp_propagate(a: CSR, x: torch.Tensor, theta, f: Optional[int] = None, y: Op
     _check(lib().gsp_propagate(ctypes.byref(v), _ptr(x), f, ldx, len(theta) - 1, th, _ptr(y), ldy,
                                _ptr(ws) if n.value else None, n.value, _stream(stream)), "gsp_propagate")
     return y
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: GAT backward
+# ---------------------------------------------------------------------------
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1) + 256, dtype=torch.uint8, device=device)
+
+
+def _aligned(t: torch.Tensor):
+    return ctypes.c_void_p((t.data_ptr() + 255) // 256 * 256)
+
+
+def gsp_csr_transpose(a: CSR, stream=None):
+    """(A^T as CSR, perm int32 [nnz]): entry e' of A^T is entry perm[e'] of A."""
+    n = ctypes.c_size_t(0)
+    v = a.view()
+    _check(lib().gsp_csr_transpose_workspace(ctypes.byref(v), ctypes.byref(n)), "gsp_csr_transpose_workspace")
+    dev = a.row_ptr.device
+    ws = _ws(n.value, dev)
+    rp = torch.empty(a.n_cols + 1, dtype=torch.int64, device=dev)
+    ct = torch.empty(max(a.nnz, 1), dtype=torch.int32, device=dev)
+    pm = torch.empty(max(a.nnz, 1), dtype=torch.int32, device=dev)
+    _check(lib().gsp_csr_transpose(ctypes.byref(v), _ptr(rp), _ptr(ct), _ptr(pm), _aligned(ws), n.value,
+                                   _stream(stream)), "gsp_csr_transpose")
+    return CSR(rp, ct[:a.nnz], None, a.n_rows), pm[:a.nnz]
+
+
+def gsp_sddmm(a: CSR, p: torch.Tensor, q: torch.Tensor, heads: int = 1, d: Optional[int] = None,
+              out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out [nnz, heads]: out[e,h] = <p[u,h,:], q[v,h,:]>."""
+    p, ldp = _mat(p, "p")
+    q, ldq = _mat(q, "q")
+    d = p.shape[1] // heads if d is None else d
+    out = torch.empty((a.nnz, heads), dtype=torch.float32, device=p.device) if out is None else out
+    v = a.view()
+    _check(lib().gsp_sddmm(ctypes.byref(v), heads, _ptr(p), d, ldp, _ptr(q), ldq, _ptr(out), _stream(stream)),
+           "gsp_sddmm")
+    return out
+
+
+def gsp_edge_softmax_backward(a: CSR, alpha: torch.Tensor, dalpha: torch.Tensor, heads: int,
+                              ds: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    ds = torch.empty_like(dalpha) if ds is None else ds
+    v = a.view()
+    _check(lib().gsp_edge_softmax_backward(ctypes.byref(v), heads, _ptr(alpha), _ptr(dalpha), _ptr(ds),
+                                           _stream(stream)), "gsp_edge_softmax_backward")
+    return ds
+
+
+def gsp_gat_aggregate_backward(a: CSR, at: CSR, perm: torch.Tensor, el: torch.Tensor, er: torch.Tensor,
+                               z: torch.Tensor, dy: torch.Tensor, heads: int, d: int, negative_slope: float = 0.2,
+                               stream=None):
+    """(dz, d_el, d_er) of gsp_gat_aggregate's output gradient dy."""
+    z, ldz = _mat(z, "z")
+    dy, lddy = _mat(dy, "dy")
+    dz = torch.empty((a.n_cols, heads * d), dtype=torch.float32, device=z.device)
+    d_el = torch.empty((a.n_rows, heads), dtype=torch.float32, device=z.device)
+    d_er = torch.empty((a.n_cols, heads), dtype=torch.float32, device=z.device)
+    n = ctypes.c_size_t(0)
+    v, vt = a.view(), at.view()
+    _check(lib().gsp_gat_backward_workspace(ctypes.byref(v), heads, ctypes.byref(n)), "gsp_gat_backward_workspace")
+    ws = _ws(n.value, z.device)
+    _check(lib().gsp_gat_aggregate_backward(ctypes.byref(v), ctypes.byref(vt), _ptr(perm), heads, _ptr(el),
+                                            _ptr(er), float(negative_slope), _ptr(z), d, ldz, _ptr(dy), lddy,
+                                            _ptr(dz), heads * d, _ptr(d_el), _ptr(d_er), _aligned(ws), n.value,
+                                            _stream(stream)), "gsp_gat_aggregate_backward")
+    return dz, d_el, d_er
+
+
+def gsp_attn_project_backward(z: torch.Tensor, a_l: torch.Tensor, a_r: torch.Tensor, d_el: torch.Tensor,
+                              d_er: torch.Tensor, dz: torch.Tensor, heads: int, d: int, stream=None):
+    """dz += d_el a_l + d_er a_r (in place); returns (d_al, d_ar) [heads*d]."""
+    z, ldz = _mat(z, "z")
+    dz, lddz = _mat(dz, "dz")
+    n = z.shape[0]
+    d_al = torch.empty(heads * d, dtype=torch.float32, device=z.device)
+    d_ar = torch.empty(heads * d, dtype=torch.float32, device=z.device)
+    nb = ctypes.c_size_t(0)
+    _check(lib().gsp_attn_project_backward_workspace(n, heads, d, ctypes.byref(nb)),
+           "gsp_attn_project_backward_workspace")
+    ws = _ws(nb.value, z.device)
+    _check(lib().gsp_attn_project_backward(n, heads, d, _ptr(z), ldz, _ptr(a_l), _ptr(a_r), _ptr(d_el), _ptr(d_er),
+                                           _ptr(dz), lddz, _ptr(d_al), _ptr(d_ar), _aligned(ws), nb.value,
+                                           _stream(stream)), "gsp_attn_project_backward")
+    return d_al, d_ar
 
 
 def gsp_probe_l2_read(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None):

@@ -263,6 +263,32 @@ __global__ void fill_i64_kernel(int64_t *p, int64_t count, int64_t v) {
     p[i] = v;
 }
 
+// Stable LSD radix sort of (key, value) pairs on the low `bits` bits of the
+// keys, 8 bits per pass, ping-ponging between the two buffer pairs; on
+// return keys/vals point at the sorted arrays.  counts: radix_counts_bytes(N),
+// scan_ws: radix_scan_ws_bytes(N).
+size_t radix_counts_bytes(int64_t N) { return (size_t)256 * std::max<int64_t>(1, ceil_div(N, kRadixTile)) * 4; }
+size_t radix_scan_ws_bytes(int64_t N) { return scan_ws_bytes(256 * std::max<int64_t>(1, ceil_div(N, kRadixTile))); }
+gsp_status radix_sort_pairs(uint64_t *&keys, uint32_t *&vals, uint64_t *keys_alt, uint32_t *vals_alt, int64_t N,
+                            int bits, uint32_t *counts, uint8_t *scan_ws, cudaStream_t s) {
+  const int64_t ntiles = ceil_div(N, kRadixTile);
+  uint64_t *ka = keys, *kb = keys_alt;
+  uint32_t *va = vals, *vb = vals_alt;
+  gsp_status st = GSP_OK;
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_hist_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, N, shift, counts, ntiles);
+    if ((st = check_launch("radix_hist"))) return st;
+    if ((st = scan_exclusive(counts, counts, 256 * ntiles, scan_ws, s))) return st;  // digit-major offsets
+    radix_scatter_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, va, kb, vb, N, shift, counts, ntiles);
+    if ((st = check_launch("radix_scatter"))) return st;
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  keys = ka;
+  vals = va;
+  return GSP_OK;
+}
+
 struct BuildLayout {
   size_t keys_a, keys_b, vals_a, vals_b, counts, head, idx, scan, scalars, total;
 };
@@ -390,17 +416,7 @@ extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, cons
   if (st) return st;
 
   // stable LSD radix sort over the bits of EMPTY = n*n
-  const int bits = key_bits(n);
-  const int64_t ntiles = ceil_div(S, kRadixTile);
-  for (int shift = 0; shift < bits; shift += 8) {
-    radix_hist_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, S, shift, counts, ntiles);
-    if ((st = check_launch("radix_hist"))) return st;
-    if ((st = scan_exclusive(counts, counts, 256 * ntiles, scan_ws, s))) return st;  // digit-major offsets
-    radix_scatter_kernel<<<(unsigned)ntiles, kRadixThreads, 0, s>>>(ka, va, kb, vb, S, shift, counts, ntiles);
-    if ((st = check_launch("radix_scatter"))) return st;
-    std::swap(ka, kb);
-    std::swap(va, vb);
-  }
+  if ((st = radix_sort_pairs(ka, va, kb, vb, S, key_bits(n), counts, scan_ws, s))) return st;
   const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
   head_flags_kernel<<<gb, 256, 0, s>>>(ka, S, EMPTY, head);
   if ((st = check_launch("head_flags"))) return st;

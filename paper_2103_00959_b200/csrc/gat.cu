@@ -106,6 +106,13 @@ static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *e
   return check_launch("row_stats");
 }
 
+// alpha = softmax_row(LeakyReLU(el[u] + er[v])) written per entry and head
+// (the GAT backward recomputes alpha with the same reductions as the forward)
+gsp_status launch_row_softmax_scores(const gsp_csr *a, const float *el, const float *er, double slope, int H,
+                                     float *alpha, cudaStream_t s) {
+  return launch_stats<true, true>(a, el, er, nullptr, slope, H, nullptr, alpha, s);
+}
+
 // ------------------------------------------------------------------------
 // Attention projection el/er (a4).  One warp per row.  When a head's D/V
 // vectors tile the warp (32 % (D/V) == 0) lanes cover several heads at once

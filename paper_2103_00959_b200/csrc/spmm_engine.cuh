@@ -773,6 +773,10 @@ struct EngineLaunch {
 gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, int64_t head_dim, int vmax,
                        int32_t slab_req, int32_t block_req, EngineLaunch *L, int max_hpt);
 
+// gat.cu: alpha = row softmax of the GAT scores (fp64 statistics)
+gsp_status launch_row_softmax_scores(const gsp_csr *a, const float *el, const float *er, double slope, int H,
+                                     float *alpha, cudaStream_t s);
+
 // heads per team for a multi-head launch planned with slab L.slab_cols
 inline int engine_hpt(const EngineLaunch &L, int64_t head_dim) {
   return (head_dim > 0 && L.slab_cols > head_dim) ? (int)(L.slab_cols / head_dim) : 1;

@@ -391,3 +391,95 @@ def test_propagate_accumulate_step_semantics(built):
     acc2 = acc.clone()
     G.gsp_spmm_accumulate(gn, x, acc2, -1.0)
     assert torch.equal(acc2, torch.addcmul(acc, ax, torch.tensor(-1.0, device=DEV)))
+
+
+# ---------------------------------------------------------------- NEXT-3: GAT backward
+
+def test_csr_transpose_bit_exact(built):
+    for name in ("n1-empty", "isolated-nofill", "multi0", "multi4", "cl4000", "rmat3000", "hubs", "star100k"):
+        go, gg, _, _ = built[name]
+        rp, ct, pm = orc.csr_transpose(go.row_ptr, go.col, go.n)
+        at, perm = G.gsp_csr_transpose(gg)
+        np.testing.assert_array_equal(host(at.row_ptr), rp, err_msg=name)
+        np.testing.assert_array_equal(host(at.col), ct, err_msg=name)
+        np.testing.assert_array_equal(host(perm).astype(np.int64), pm, err_msg=name)
+
+
+@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 64), (3, 16), (1, 602)])
+def test_sddmm_parity(built, H, D):
+    """|t - t_ref| <= 1e-5 * sum_k |p q| + 1e-6 (D-term dot products)."""
+    for name in ("multi1", "cl4000", "hubs"):
+        go, gg, _, _ = built[name]
+        p = uniform((go.n, H * D), seed=1)
+        q = uniform((go.n, H * D), seed=2)
+        tref = orc.sddmm(go.row_ptr, go.col, p, q, heads=H)
+        cond = orc.sddmm(go.row_ptr, go.col, np.abs(p), np.abs(q), heads=H)
+        t = host(G.gsp_sddmm(gg, dev(p), dev(q), heads=H))
+        assert_within(t, tref, cond, what=f"{name} H={H} D={D}")
+
+
+def test_edge_softmax_backward_parity(built):
+    """|ds - ds_ref| <= 1e-5 * alpha (|dalpha| + sum_row alpha |dalpha|) + 1e-9."""
+    for H in (1, 2, 4, 8):
+        go, gg, _, _ = built["cl4000"]
+        lg = uniform((go.nnz, H), seed=H, low=-3, high=3)
+        a = G.gsp_edge_softmax(gg, dev(lg), H)
+        da = uniform((go.nnz, H), seed=10 + H)
+        ds = host(G.gsp_edge_softmax_backward(gg, a, dev(da), H))
+        a64 = host(a).astype(np.float64)
+        dsref = orc.edge_softmax_backward(go.row_ptr, a64, da.astype(np.float64), H)
+        rows = np.repeat(np.arange(go.n), np.diff(go.row_ptr))
+        rs = np.stack([np.bincount(rows, a64[:, h] * np.abs(da[:, h]), go.n) for h in range(H)], 1)
+        cond = a64 * (np.abs(da) + rs[rows])
+        assert_within(ds, dsref, cond, abs_=1e-9, what=f"H={H}")
+
+
+@pytest.mark.parametrize("H,D", [(1, 64), (4, 8), (8, 64), (2, 3)])
+def test_gat_aggregate_backward_parity(built, H, D):
+    """dz, d_el, d_er vs the fp64 oracle.  Bounds from the arithmetic: dz is an
+    A^T SpMM (1e-5 * sum alpha |dy|); dt = alpha (dalpha - <alpha, dalpha>)
+    with dalpha an SDDMM, so |d dt| <= 1e-5 * alpha (c + sum_row alpha c),
+    c = sddmm(|dy|, |z|); d_el / d_er sum those over rows / columns."""
+    for name in ("multi0", "cl4000", "hubs"):
+        go, gg, _, _ = built[name]
+        n = go.n
+        el = uniform((n, H), seed=4, low=-3, high=3)
+        er = uniform((n, H), seed=5, low=-3, high=3)
+        z = uniform((n, H * D), seed=6)
+        dy = uniform((n, H * D), seed=7)
+        at, perm = G.gsp_csr_transpose(gg)
+        dz, d_el, d_er = [host(t) for t in G.gsp_gat_aggregate_backward(gg, at, perm, dev(el), dev(er), dev(z),
+                                                                         dev(dy), H, D)]
+        dz_r, del_r, der_r, dt_r = orc.gat_backward(go.row_ptr, go.col, el, er, z, dy, H, D)
+        sc = orc.gat_scores(go.row_ptr, go.col, el, er, H)
+        al = orc.edge_softmax(go.row_ptr, sc, H)
+        rp_t, ct, pm = orc.csr_transpose(go.row_ptr, go.col, n)
+        dz_c, _ = orc.multihead_spmm(rp_t, ct, al[pm], np.abs(dy), H, D)
+        assert_within(dz, dz_r, dz_c, what=f"dz {name}")
+        c = orc.sddmm(go.row_ptr, go.col, np.abs(dy), np.abs(z), heads=H)
+        rows = np.repeat(np.arange(n), np.diff(go.row_ptr))
+        rs = np.stack([np.bincount(rows, al[:, h] * c[:, h], n) for h in range(H)], 1)
+        cdt = al * (c + rs[rows])
+        cel = np.stack([np.bincount(rows, cdt[:, h], n) for h in range(H)], 1)
+        cer = np.stack([np.bincount(go.col, cdt[:, h], n) for h in range(H)], 1)
+        assert_within(d_el, del_r, cel, what=f"d_el {name}")
+        assert_within(d_er, der_r, cer, what=f"d_er {name}")
+
+
+def test_attn_project_backward_parity():
+    n, H, D = 3000, 8, 64
+    z = uniform((n, H * D), seed=1)
+    al = uniform((H, D), seed=2)
+    ar = uniform((H, D), seed=3)
+    gl = uniform((n, H), seed=4)
+    gr = uniform((n, H), seed=5)
+    dz0 = uniform((n, H * D), seed=6)
+    dz = dev(dz0)
+    d_al, d_ar = G.gsp_attn_project_backward(dev(z), dev(al.reshape(-1)), dev(ar.reshape(-1)), dev(gl), dev(gr), dz,
+                                             H, D)
+    dz_r, dal_r, dar_r = orc.attn_project_backward(z, al, ar, gl, gr, H, D)
+    _, dal_c, dar_c = orc.attn_project_backward(np.abs(z), al, ar, np.abs(gl), np.abs(gr), H, D)
+    assert_within(host(d_al), dal_r, dal_c, what="d_al")
+    assert_within(host(d_ar), dar_r, dar_c, what="d_ar")
+    dzc, _, _ = orc.attn_project_backward(z, np.abs(al), np.abs(ar), np.abs(gl), np.abs(gr), H, D)
+    assert_within(host(dz), dz0.astype(np.float64) + dz_r, np.abs(dz0) + dzc, what="dz")

@@ -620,3 +620,30 @@ def test_gat_backward_vs_finite_differences():
     rows = np.repeat(np.arange(n), np.diff(g.row_ptr))
     np.testing.assert_allclose(d_el, np.stack([np.bincount(rows, dt[:, h], n) for h in range(H)], 1), rtol=1e-12)
     np.testing.assert_allclose(d_er, np.stack([np.bincount(g.col, dt[:, h], n) for h in range(H)], 1), rtol=1e-12)
+
+
+def test_attn_project_backward_vs_finite_differences():
+    """Central differences of L = <g_l, el> + <g_r, er> through orc.attn_project
+    (linear: exact up to rounding) for z, a_l, a_r."""
+    rng = np.random.default_rng(3)
+    n, H, D = 30, 2, 4
+    q = lambda shape: (rng.integers(-64, 64, shape) / 32.0).astype(np.float32)
+    z, al, ar = q((n, H * D)), q((H, D)), q((H, D))
+    gl, gr = rng.standard_normal((n, H)), rng.standard_normal((n, H))
+
+    def loss(z_, al_, ar_):
+        el, er, _, _ = orc.attn_project(z_, al_, ar_, H, D)
+        return float((el * gl).sum() + (er * gr).sum())
+
+    dz, d_al, d_ar = orc.attn_project_backward(z, al, ar, gl, gr, H, D)
+    eps = 2.0 ** -10
+    for arr, grad in ((z, dz), (al, d_al.reshape(H, D)), (ar, d_ar.reshape(H, D))):
+        for _ in range(10):
+            i, j = int(rng.integers(0, arr.shape[0])), int(rng.integers(0, arr.shape[1]))
+            o = arr[i, j]
+            arr[i, j] = o + eps
+            lp = loss(z, al, ar)
+            arr[i, j] = o - eps
+            lm = loss(z, al, ar)
+            arr[i, j] = o
+            assert abs((lp - lm) / (2 * eps) - grad[i, j]) <= 1e-9 * max(1.0, abs(grad[i, j]))
