@@ -61,10 +61,14 @@ def lib():
         L.orc_edge_softmax_backward.argtypes = [I, P, I, P, P, P]
         L.orc_gat_backward.argtypes = [I, P, P, I, P, P, ctypes.c_double, P, I, I, P, I, P, P, P, P]
         L.orc_attn_project_backward.argtypes = [I, I, I, P, I, P, P, P, P, P, P, P]
+        L.orc_linear.argtypes = [I, I, P, I, I, P, I, P, P, P, I]
+        L.orc_gcn_layer.argtypes = [I, I, P, P, P, P, I, I, P, I, P, ctypes.c_int, P, P, I]
+        L.orc_bias_act.argtypes = [I, I, P, I, P, ctypes.c_int]
         L.orc_csr_slice.argtypes = [I, P, P, P, P, I, I, I, P, P, P]
         for f in ("orc_build_csr", "orc_sym_norm", "orc_spmm", "orc_gspmm", "orc_propagate", "orc_ppr_coeffs", "orc_edge_softmax", "orc_gat_scores",
                   "orc_multihead_spmm", "orc_attn_project", "orc_partition_rows", "orc_csr_slice", "orc_sddmm",
-                  "orc_csr_transpose", "orc_edge_softmax_backward", "orc_gat_backward", "orc_attn_project_backward"):
+                  "orc_csr_transpose", "orc_edge_softmax_backward", "orc_gat_backward", "orc_attn_project_backward",
+                  "orc_linear", "orc_gcn_layer", "orc_bias_act"):
             getattr(L, f).restype = ctypes.c_int
     return _lib
 
@@ -331,3 +335,44 @@ def attn_project_backward(z, a_l, a_r, d_el, d_er, heads, d):
     _chk(lib().orc_attn_project_backward(n, heads, d, _p(z), z.shape[1], _p(a_l), _p(a_r), _p(d_el), _p(d_er),
                                          _p(dz), _p(d_al), _p(d_ar)))
     return dz, d_al, d_ar
+
+
+ACT = {"none": 0, "relu": 1, "elu": 2}
+
+
+def linear(x, w, bias=None, r0=0, r1=None):
+    """(y, cond) fp64 = x W (+ bias) on rows [r0, r1) (oracle.c §11a)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    bias = _c(bias, np.float32)
+    r1 = x.shape[0] if r1 is None else r1
+    f_in, f_out = w.shape
+    y = np.zeros((r1 - r0, max(f_out, 1)), np.float64)
+    cond = np.zeros_like(y)
+    _chk(lib().orc_linear(r0, r1, _p(x), x.shape[1], f_in, _p(w), f_out, _p(bias), _p(y), _p(cond), y.shape[1]))
+    return y[:, :f_out], cond[:, :f_out]
+
+
+def gcn_layer(row_ptr, col, a, x, w, bias=None, act="relu", r0=0, r1=None):
+    """(y, cond) fp64 = act(sum_e a_e x[v] W + b) on rows [r0, r1) (oracle.c §11b)."""
+    row_ptr = _c(row_ptr, np.int64)
+    col = _c(col, np.int32)
+    a = _c(a, np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    bias = _c(bias, np.float32)
+    n = row_ptr.size - 1
+    r1 = n if r1 is None else r1
+    f_in, f_out = w.shape
+    y = np.zeros((r1 - r0, max(f_out, 1)), np.float64)
+    cond = np.zeros_like(y)
+    _chk(lib().orc_gcn_layer(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), x.shape[1], f_in, _p(w), f_out, _p(bias),
+                             ACT[act], _p(y), _p(cond), y.shape[1]))
+    return y[:, :f_out], cond[:, :f_out]
+
+
+def bias_act(y, bias=None, act="none"):
+    y = np.array(y, dtype=np.float64, order="C", copy=True)
+    bias = _c(bias, np.float32)
+    _chk(lib().orc_bias_act(y.shape[0], y.shape[1], _p(y), y.shape[1], _p(bias), ACT[act]))
+    return y

@@ -492,6 +492,76 @@ int orc_attn_project_backward(int64_t n, int64_t heads, int64_t d, const float *
 }
 
 /* ---------------------------------------------------------------------------
+ * 11. Layers for 2-layer inference (NEXT-1).  P:239-246 [Eq. gcn_layer:
+ *     H^(l+1) = sigma(A^ H^(l) W^(l))]; P:253 (GAT); P:661-663 [Table
+ *     spmm_time: 2-layer GCN / GAT inference, hidden 128, GAT 4 heads].
+ *     act: 0 none, 1 ReLU (GCN hidden layers), 2 ELU alpha=1 (GAT hidden).
+ * 11a. y = x W (+ bias) on rows [r0, r1); W row-major [f_in][f_out].
+ * ------------------------------------------------------------------------- */
+static double orc_act(double v, int act) {
+  if (act == 1) return v > 0.0 ? v : 0.0;
+  if (act == 2) return v > 0.0 ? v : expm1(v);
+  return v;
+}
+
+int orc_linear(int64_t r0, int64_t r1, const float *x, int64_t ldx, int64_t f_in, const float *w, int64_t f_out,
+               const float *bias, double *y, double *cond, int64_t ldy) {
+  if (r0 < 0 || r1 < r0 || f_in < 0 || f_out < 0 || ldx < f_in || ldy < f_out || !x || !w || !y) return ORC_ERR_ARG;
+  for (int64_t u = r0; u < r1; ++u)
+    for (int64_t j = 0; j < f_out; ++j) {
+      double s = bias ? (double)bias[j] : 0.0, c = bias ? fabs((double)bias[j]) : 0.0;
+      for (int64_t k = 0; k < f_in; ++k) {
+        const double t = (double)x[u * ldx + k] * (double)w[k * f_out + j];
+        s += t;
+        c += fabs(t);
+      }
+      y[(u - r0) * ldy + j] = s;
+      if (cond) cond[(u - r0) * ldy + j] = c;
+    }
+  return ORC_OK;
+}
+
+/* 11b. GCN layer on rows [r0, r1): y[u] = act(sum_e a_e (x[col_e] W) + bias),
+ *      the product computed per neighbour (Eq. gcn_layer written out).
+ *      cond[u] = sum_e |a_e| (|x[col_e]| |W|) + |bias| (error scale, before act). */
+int orc_gcn_layer(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col, const double *a,
+                  const float *x, int64_t ldx, int64_t f_in, const float *w, int64_t f_out, const float *bias, int act,
+                  double *y, double *cond, int64_t ldy) {
+  if (r0 < 0 || r1 < r0 || f_in < 0 || f_out < 0 || ldx < f_in || ldy < f_out || !row_ptr || !x || !w || !y)
+    return ORC_ERR_ARG;
+  double *t = (double *)malloc(sizeof(double) * (size_t)(f_out > 0 ? f_out : 1));
+  double *tc = (double *)malloc(sizeof(double) * (size_t)(f_out > 0 ? f_out : 1));
+  if (!t || !tc) { free(t); free(tc); return ORC_ERR_NOMEM; }
+  for (int64_t u = r0; u < r1; ++u) {
+    double *yu = y + (u - r0) * ldy;
+    double *cu = cond ? cond + (u - r0) * ldy : NULL;
+    for (int64_t j = 0; j < f_out; ++j) {
+      yu[j] = bias ? (double)bias[j] : 0.0;
+      if (cu) cu[j] = bias ? fabs((double)bias[j]) : 0.0;
+    }
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      const double ae = a ? a[e] : 1.0;
+      orc_linear(col[e], col[e] + 1, x, ldx, f_in, w, f_out, NULL, t, tc, f_out);
+      for (int64_t j = 0; j < f_out; ++j) {
+        yu[j] += ae * t[j];
+        if (cu) cu[j] += fabs(ae) * tc[j];
+      }
+    }
+    for (int64_t j = 0; j < f_out; ++j) yu[j] = orc_act(yu[j], act);
+  }
+  free(t); free(tc);
+  return ORC_OK;
+}
+
+/* 11c. Elementwise act(x + bias) (for composing layers in tests). */
+int orc_bias_act(int64_t n, int64_t f, double *y, int64_t ldy, const float *bias, int act) {
+  if (n < 0 || f < 0 || ldy < f || !y) return ORC_ERR_ARG;
+  for (int64_t u = 0; u < n; ++u)
+    for (int64_t j = 0; j < f; ++j) y[u * ldy + j] = orc_act(y[u * ldy + j] + (bias ? (double)bias[j] : 0.0), act);
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * 8. Row partition balanced by nnz (DESIGN.md multi-GPU):
  *    bound_p = lower_bound(row_ptr[0..n], ceil(p * nnz / P)) for 0 < p < P,
  *    bound_0 = 0, bound_P = n.  lower_bound = first r with row_ptr[r] >= t.

@@ -647,3 +647,42 @@ def test_attn_project_backward_vs_finite_differences():
             lm = loss(z, al, ar)
             arr[i, j] = o
             assert abs((lp - lm) / (2 * eps) - grad[i, j]) <= 1e-9 * max(1.0, abs(grad[i, j]))
+
+
+# ---------------------------------------------------------------------------
+# 11. inference layers (oracle.c §11, NEXT-1)
+# ---------------------------------------------------------------------------
+
+def test_linear_vs_numpy_and_activations():
+    x = uniform((50, 17), seed=1)
+    w = uniform((17, 9), seed=2)
+    b = uniform(9, seed=3)
+    y, cond = orc.linear(x, w, b)
+    np.testing.assert_allclose(y, x.astype(np.float64) @ w.astype(np.float64) + b, rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(cond, np.abs(x.astype(np.float64)) @ np.abs(w.astype(np.float64)) + np.abs(b),
+                               rtol=1e-13)
+    import torch
+    v = uniform((6, 7), seed=4, low=-3, high=3).astype(np.float64)
+    np.testing.assert_array_equal(orc.bias_act(v, None, "relu"), torch.relu(torch.from_numpy(v)).numpy())
+    np.testing.assert_allclose(orc.bias_act(v, None, "elu"), torch.nn.functional.elu(torch.from_numpy(v)).numpy(),
+                               rtol=1e-15, atol=1e-300)
+
+
+def test_gcn_layer_vs_dense_eq_gcn_layer():
+    """Eq. gcn_layer: act(A^ X W + b) against dense NumPy; the SPEC
+    example S:496 (K2, X=[[1],[0]], W=[1], A^ all 0.5 -> [[0.5],[0.5]])."""
+    s, d = chung_lu(200, 800, seed=6)
+    g = orc.build_csr(200, s, d, None, True, 1.0)
+    _, a64, _ = orc.sym_norm(g)
+    x = uniform((200, 12), seed=7)
+    w = uniform((12, 5), seed=8)
+    b = uniform(5, seed=9)
+    for act in ("none", "relu", "elu"):
+        y, _ = orc.gcn_layer(g.row_ptr, g.col, a64, x, w, b, act)
+        ref = orc.bias_act(g.dense(a64) @ (x.astype(np.float64) @ w.astype(np.float64)), b, act)
+        np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-13)
+    g2 = orc.build_csr(2, [0], [1], None, True, 1.0)
+    _, a2, _ = orc.sym_norm(g2)
+    y2, _ = orc.gcn_layer(g2.row_ptr, g2.col, a2, np.array([[1.0], [0.0]], np.float32), np.array([[1.0]], np.float32),
+                          None, "none")
+    np.testing.assert_array_equal(y2, [[0.5], [0.5]])
