@@ -484,6 +484,49 @@ def main():
             "alg_GB/s": gb / (tgm * 1e-3) / 1e9, "frac_of_hbm_peak": gb / (tgm * 1e-3) / 1e9 / peak,
             "launches": "one engine_kernel<4,16,WeightGat> per aggregate (softmax statistics fused)"}
 
+    # --- NEXT-1: the paper's Table spmm_time workload (2-layer GCN / GAT inference,
+    #     hidden 128, GAT 4 heads), with the paper's RTX 3090 times ---
+    if not use_dist and not args.no_gat:
+        from paper_2103_00959_b200.inference import GATParams, GCNParams, gat_inference, gcn_inference
+        paper = {"C3": ("Flickr", 500, 7, 0.002, 0.009), "C4": ("Reddit", 602, 41, 0.022, 0.080),
+                 "C5": ("Yelp", 300, 100, 0.023, 0.081)}  # (name, feats, classes, GCN s, GAT s) P:24-26
+        table = {}
+        for key, (dname, fin, ncls, t_gcn, t_gat) in paper.items():
+            cfg_k = CONFIGS[key]
+            if key == args.config:
+                gk = gn
+            else:
+                sk, dk = graph_for(cfg_k, seed=1)
+                gk = G.gsp_sym_normalize(G.gsp_coo_to_csr(cfg_k.n, torch.from_numpy(sk).to(dev),
+                                                          torch.from_numpy(dk).to(dev), None, True, 1.0))
+            xk = torch.from_numpy(features(cfg_k.n, fin, (fin + 3) // 4 * 4, seed=2)).to(dev)[:, :fin]
+            pg = GCNParams.init(fin, 128, ncls, dev, seed=1)
+            pa = GATParams.init(fin, 128, 4, ncls, dev, seed=1)
+            res = {}
+            for mname, fn_ in (("gcn", lambda: gcn_inference(gk, xk, pg)), ("gat", lambda: gat_inference(gk, xk, pa))):
+                ts = []
+                for i in range(args.warmup + 10):
+                    flush.zero_()
+                    a0 = torch.cuda.Event(enable_timing=True)
+                    a1 = torch.cuda.Event(enable_timing=True)
+                    a0.record()
+                    fn_()
+                    a1.record()
+                    torch.cuda.synchronize()
+                    if i >= args.warmup:
+                        ts.append(a0.elapsed_time(a1))
+                res[mname + "_ms"] = float(np.mean(ts))
+            res["paper_3090_gcn_ms"] = 1e3 * t_gcn
+            res["paper_3090_gat_ms"] = 1e3 * t_gat
+            res["nnz"] = gk.nnz
+            table[f"{key}-{dname}"] = res
+            del xk
+        out.setdefault("secondary", {})["next1_table_spmm_time"] = {
+            "workload": "2-layer GCN (hidden 128, ReLU) and GAT (4 heads x 32, ELU; 1 output head) inference, "
+                        "random weights, synthetic graphs with the paper's node/edge/feature/class counts",
+            "note": "paper times are CogDL on an RTX 3090 (P:678-693), fp32, context only (other hardware)",
+            "results": table}
+
     # --- cpu_baseline: the oracle as it stands, bounded sample, rank 0 at N=1 ---
     if not use_dist and rank == 0 and not args.no_cpu_baseline:
         try:

@@ -35,7 +35,8 @@ EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "g
            "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
            "gsp_propagate_workspace", "gsp_propagate", "gsp_csr_transpose_workspace", "gsp_csr_transpose",
            "gsp_sddmm", "gsp_edge_softmax_backward", "gsp_gat_backward_workspace", "gsp_gat_aggregate_backward",
-           "gsp_attn_project_backward_workspace", "gsp_attn_project_backward")
+           "gsp_attn_project_backward_workspace", "gsp_attn_project_backward", "gsp_linear", "gsp_spmm_bias_act",
+           "gsp_gcn_layer_workspace", "gsp_gcn_layer", "gsp_gat_aggregate_bias_act")
 
 
 class GspError(RuntimeError):
@@ -87,6 +88,11 @@ def lib() -> ctypes.CDLL:
             "gsp_gat_aggregate_backward": [CP, CP, P, I32, P, P, D, P, I, I, P, I, P, I, P, P, P, ctypes.c_size_t, P],
             "gsp_attn_project_backward_workspace": [I, I32, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_attn_project_backward": [I, I32, I, P, I, P, P, P, P, P, I, P, P, P, ctypes.c_size_t, P],
+            "gsp_linear": [I, I, P, I, P, I, I, P, I, P],
+            "gsp_spmm_bias_act": [CP, P, I, I, P, ctypes.c_int, P, I, P],
+            "gsp_gcn_layer_workspace": [I, I, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_gcn_layer": [CP, P, I, I, P, I, P, ctypes.c_int, P, I, P, ctypes.c_size_t, P],
+            "gsp_gat_aggregate_bias_act": [CP, I32, P, P, D, P, I, I, P, ctypes.c_int, P, I, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -494,6 +500,67 @@ def gsp_attn_project_backward(z: torch.Tensor, a_l: torch.Tensor, a_r: torch.Ten
                                            _ptr(dz), lddz, _ptr(d_al), _ptr(d_ar), _aligned(ws), nb.value,
                                            _stream(stream)), "gsp_attn_project_backward")
     return d_al, d_ar
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: inference layers
+# ---------------------------------------------------------------------------
+
+ACT = {"none": 0, "relu": 1, "elu": 2}
+
+
+def gsp_linear(x: torch.Tensor, w: torch.Tensor, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """y = x w (row-major, fp32 cuBLAS GEMM)."""
+    x, ldx = _mat(x, "x")
+    w, ldw = _mat(w, "w")
+    n, f_in = x.shape
+    f_out = w.shape[1]
+    y = torch.empty((n, f_out), dtype=torch.float32, device=x.device) if y is None else y
+    y, ldy = _mat(y, "y")
+    _check(lib().gsp_linear(n, f_in, _ptr(x), ldx, _ptr(w), ldw, f_out, _ptr(y), ldy, _stream(stream)), "gsp_linear")
+    return y
+
+
+def gsp_spmm_bias_act(a: CSR, x: torch.Tensor, bias: Optional[torch.Tensor] = None, act: str = "none",
+                      f: Optional[int] = None, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    x, ldx = _mat(x, "x")
+    f = x.shape[1] if f is None else int(f)
+    y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device) if y is None else y
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    _check(lib().gsp_spmm_bias_act(ctypes.byref(v), _ptr(x), f, ldx, _ptr(bias), ACT[act], _ptr(y), ldy,
+                                   _stream(stream)), "gsp_spmm_bias_act")
+    return y
+
+
+def gsp_gcn_layer(a: CSR, x: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None, act: str = "relu",
+                  y: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """y = act(A (x w) + bias)  (Eq. gcn_layer)."""
+    x, ldx = _mat(x, "x")
+    f_in, f_out = w.shape
+    y = torch.empty((a.n_rows, f_out), dtype=torch.float32, device=x.device) if y is None else y
+    y, ldy = _mat(y, "y")
+    nb = ctypes.c_size_t(0)
+    _check(lib().gsp_gcn_layer_workspace(a.n_cols, f_out, ctypes.byref(nb)), "gsp_gcn_layer_workspace")
+    if ws is None or ws.numel() < nb.value:
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=x.device)
+    v = a.view()
+    _check(lib().gsp_gcn_layer(ctypes.byref(v), _ptr(x), f_in, ldx, _ptr(w.contiguous()), f_out, _ptr(bias),
+                               ACT[act], _ptr(y), ldy, _ptr(ws), ws.numel(), _stream(stream)), "gsp_gcn_layer")
+    return y
+
+
+def gsp_gat_aggregate_bias_act(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tensor, heads: int, d: int,
+                               bias: Optional[torch.Tensor] = None, act: str = "none", negative_slope: float = 0.2,
+                               y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    z, ldz = _mat(z, "z")
+    y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device) if y is None else y
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    _check(lib().gsp_gat_aggregate_bias_act(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope),
+                                            _ptr(z), d, ldz, _ptr(bias), ACT[act], _ptr(y), ldy, _stream(stream)),
+           "gsp_gat_aggregate_bias_act")
+    return y
 
 
 def gsp_probe_l2_read(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None):

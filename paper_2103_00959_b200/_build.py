@@ -53,7 +53,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, def
         if verbose and out:
             sys.stderr.write(out.decode(errors="replace"))
     tmp = lib + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lcublas", "-Xlinker",
+                           "-rpath=/usr/local/cuda/lib64", "-lrt", "-ldl", "-lpthread"])
     os.replace(tmp, lib)
     return lib
 

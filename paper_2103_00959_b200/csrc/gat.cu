@@ -224,13 +224,11 @@ extern "C" gsp_status gsp_gat_workspace(const gsp_csr *a, int32_t heads, size_t 
   return GSP_OK;
 }
 
-extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const float *el, const float *er,
-                                        double negative_slope, const float *z, int64_t d, int64_t ldz, float *y,
-                                        int64_t ldy, float *alpha_out, void *ws, size_t ws_bytes, gsp_stream stream) {
-  const char *fn = "gsp_gat_aggregate";
+static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const float *el, const float *er,
+                                     double negative_slope, const float *z, int64_t d, int64_t ldz, float *y,
+                                     int64_t ldy, float *alpha_out, const float *bias, int act, cudaStream_t s,
+                                     const char *fn) {
   clear_detail();
-  (void)ws;
-  (void)ws_bytes;
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
   if (heads <= 0 || d < 0) return fail(GSP_ERR_INVALID_ARG, "%s: heads >= 1 and d >= 0 required", fn);
@@ -242,7 +240,6 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   const size_t zb = a->n_cols ? (size_t)((a->n_cols - 1) * ldz + f) * 4 : 0;
   const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
   if (overlaps(z, zb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: z and y overlap", fn);
-  cudaStream_t s = cs(stream);
   int vmax = 1;
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
@@ -264,7 +261,27 @@ extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const f
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
   p.hpt = engine_hpt(L, d);
+  p.bias = bias;
+  p.act = act;
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   WeightGat w{el, er, alpha_out, negative_slope, heads};
   return engine_launch(L, p, w, s);
+}
+
+extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const float *el, const float *er,
+                                        double negative_slope, const float *z, int64_t d, int64_t ldz, float *y,
+                                        int64_t ldy, float *alpha_out, void *ws, size_t ws_bytes, gsp_stream stream) {
+  (void)ws;
+  (void)ws_bytes;
+  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, alpha_out, nullptr, 0, cs(stream),
+                            "gsp_gat_aggregate");
+}
+
+extern "C" gsp_status gsp_gat_aggregate_bias_act(const gsp_csr *a, int32_t heads, const float *el, const float *er,
+                                                 double negative_slope, const float *z, int64_t d, int64_t ldz,
+                                                 const float *bias, gsp_act act, float *y, int64_t ldy,
+                                                 gsp_stream stream) {
+  if (act < GSP_ACT_NONE || act > GSP_ACT_ELU) return fail(GSP_ERR_INVALID_ARG, "gsp_gat_aggregate_bias_act: bad act");
+  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, nullptr, bias, (int)act, cs(stream),
+                            "gsp_gat_aggregate_bias_act");
 }

@@ -1,0 +1,72 @@
+// linear.cu -- NEXT-1: the dense step of a GNN layer, Y = X W (Eq. gcn_layer,
+// P:242 H W), and the GCN layer act(A^ (X W) + b).  X W is a plain dense GEMM,
+// delegated to cuBLAS (fp32 compute, CUBLAS_COMPUTE_32F: no TF32 rounding, so
+// fp32 parity holds); the sparse aggregation, bias and activation run in the
+// SpMM engine (fused epilogue).
+#include <cublas_v2.h>
+
+#include <algorithm>
+
+#include "spmm_engine.cuh"
+
+namespace gsp {
+
+// one cuBLAS handle per (thread, device), created on first use
+static cublasHandle_t blas_handle() {
+  static thread_local cublasHandle_t h[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!h[dev] && cublasCreate(&h[dev]) != CUBLAS_STATUS_SUCCESS) h[dev] = nullptr;
+  return h[dev];
+}
+
+}  // namespace gsp
+
+using namespace gsp;
+
+extern "C" gsp_status gsp_linear(int64_t n, int64_t f_in, const float *x, int64_t ldx, const float *w, int64_t ldw,
+                                 int64_t f_out, float *y, int64_t ldy, gsp_stream stream) {
+  const char *fn = "gsp_linear";
+  clear_detail();
+  if (n < 0 || f_in < 0 || f_out < 0 || ldx < f_in || ldw < f_out || ldy < f_out)
+    return fail(GSP_ERR_INVALID_ARG, "%s: bad sizes", fn);
+  if (n == 0 || f_out == 0) return GSP_OK;
+  if (!x || !w || !y) return fail(GSP_ERR_INVALID_ARG, "%s: null pointer", fn);
+  if (n >= (int64_t(1) << 31) || f_in >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "%s: too large", fn);
+  if (overlaps(x, (size_t)((n - 1) * ldx + f_in) * 4, y, (size_t)((n - 1) * ldy + f_out) * 4))
+    return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+  cublasHandle_t h = blas_handle();
+  if (!h) return fail(GSP_ERR_CUDA, "%s: cublasCreate failed", fn);
+  if (cublasSetStream(h, cs(stream)) != CUBLAS_STATUS_SUCCESS) return fail(GSP_ERR_CUDA, "%s: cublasSetStream", fn);
+  const float one = 1.0f, zero = 0.0f;
+  // row-major Y[n x f_out] = X[n x f_in] W[f_in x f_out]  <=>  column-major Y^T = W^T X^T
+  const cublasStatus_t r = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)f_out, (int)n, (int)f_in, &one, w,
+                                        CUDA_R_32F, (int)ldw, x, CUDA_R_32F, (int)ldx, &zero, y, CUDA_R_32F, (int)ldy,
+                                        CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  if (r != CUBLAS_STATUS_SUCCESS) return fail(GSP_ERR_CUDA, "%s: cublasGemmEx status %d", fn, (int)r);
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_gcn_layer_workspace(int64_t n, int64_t f_out, size_t *ws_bytes) {
+  clear_detail();
+  if (n < 0 || f_out < 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_gcn_layer_workspace: bad argument");
+  *ws_bytes = (size_t)n * ((f_out + 3) / 4 * 4) * 4 + 256;
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_gcn_layer(const gsp_csr *a, const float *x, int64_t f_in, int64_t ldx, const float *w,
+                                    int64_t f_out, const float *bias, gsp_act act, float *y, int64_t ldy, void *ws,
+                                    size_t ws_bytes, gsp_stream stream) {
+  const char *fn = "gsp_gcn_layer";
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  size_t need = 0;
+  gsp_gcn_layer_workspace(a->n_cols, f_out, &need);
+  if (!ws || ws_bytes < need) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, need);
+  float *h = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  const int64_t ldh = (f_out + 3) / 4 * 4;
+  if ((st = gsp_linear(a->n_cols, f_in, x, ldx, w, f_out, f_out, h, ldh, stream))) return st;
+  return gsp_spmm_bias_act(a, h, f_out, ldh, bias, act, y, ldy, stream);
+}

@@ -121,7 +121,8 @@ struct AccEpi {
 };
 
 static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, const float *x, int64_t f, int64_t ldx,
-                                   float *y, int64_t ldy, gsp_reduce red, const AccEpi *epi, cudaStream_t s) {
+                                   float *y, int64_t ldy, gsp_reduce red, const AccEpi *epi, cudaStream_t s,
+                                   const float *bias = nullptr, int act = 0) {
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -136,6 +137,8 @@ static gsp_status spmm_launch_part(const gsp_csr *a, const EngineLaunch &L, cons
   p.head_dim = 0;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, a->val);
+  p.bias = bias;
+  p.act = act;
   if (epi) {
     const int vw = L.V == 8 ? 4 : L.V;
     p.acc = epi->acc;
@@ -277,6 +280,28 @@ extern "C" gsp_status gsp_propagate(const gsp_csr *a, const float *x, int64_t f,
     ldin = ld;
   }
   return GSP_OK;
+}
+
+extern "C" gsp_status gsp_spmm_bias_act(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, const float *bias,
+                                        gsp_act act, float *y, int64_t ldy, gsp_stream stream) {
+  const char *fn = "gsp_spmm_bias_act";
+  clear_detail();
+  if (act < GSP_ACT_NONE || act > GSP_ACT_ELU) return fail(GSP_ERR_INVALID_ARG, "%s: bad activation", fn);
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!y || (a->n_cols > 0 && !x)) return fail(GSP_ERR_INVALID_ARG, "%s: null pointer", fn);
+  const size_t xb = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 4 : 0;
+  if (overlaps(x, xb, y, (size_t)((a->n_rows - 1) * ldy + f) * 4)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+  SpmmPlan P;
+  if ((st = spmm_plan(a, x, f, ldx, nullptr, &P))) return st;
+  cudaStream_t s = cs(stream);
+  if ((st = spmm_launch_part(a, P.main, x, P.f_main, ldx, y, ldy, GSP_REDUCE_SUM, nullptr, s, bias, act))) return st;
+  if (P.f_tail)
+    st = spmm_launch_part(a, P.tail, x + P.f_main, P.f_tail, ldx, y + P.f_main, ldy, GSP_REDUCE_SUM, nullptr, s,
+                          bias ? bias + P.f_main : nullptr, act);
+  return st;
 }
 
 extern "C" gsp_status gsp_gspmm(const gsp_csr *a, gsp_reduce reduce, const float *x, int64_t f, int64_t ldx, float *y,

@@ -284,6 +284,9 @@ struct EngineParams {
   int64_t ldacc, ldsrc;
   float acc_coef, src_coef;
   int skip_y, acc_vec_ok, src_vec_ok;
+  // fused layer epilogue (NEXT-1): out = act(out + bias[col]); act 0 none, 1 ReLU, 2 ELU
+  const float *bias;
+  int act;
 };
 
 template <int V>
@@ -298,8 +301,17 @@ __device__ __forceinline__ void load_cols(float (&r)[V], const float *p, int nva
 
 // Row epilogue: store out[] to y and/or fold it into the accumulator.
 template <int V>
-__device__ __forceinline__ void epilogue(const EngineParams &p, int64_t r, int64_t col0, const float (&out)[V],
+__device__ __forceinline__ void epilogue(const EngineParams &p, int64_t r, int64_t col0, const float (&out_in)[V],
                                          int nvalid) {
+  float out[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    float v = out_in[i];
+    if (p.bias && i < nvalid) v += __ldg(p.bias + col0 + i);
+    if (p.act == 1) v = fmaxf(v, 0.0f);
+    else if (p.act == 2) v = v > 0.0f ? v : expm1f(v);
+    out[i] = v;
+  }
   if (p.acc) {
     float prev[V], nv[V];
     if (p.acc_src) {
@@ -811,6 +823,8 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.ldacc = p.ldsrc = 0;
   p.acc_coef = p.src_coef = 0.0f;
   p.skip_y = p.acc_vec_ok = p.src_vec_ok = 0;
+  p.bias = nullptr;
+  p.act = 0;
 }
 
 template <int V, int G, class W, class R>

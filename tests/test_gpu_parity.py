@@ -483,3 +483,73 @@ def test_attn_project_backward_parity():
     assert_within(host(d_ar), dar_r, dar_c, what="d_ar")
     dzc, _, _ = orc.attn_project_backward(z, np.abs(al), np.abs(ar), np.abs(gl), np.abs(gr), H, D)
     assert_within(host(dz), dz0.astype(np.float64) + dz_r, np.abs(dz0) + dzc, what="dz")
+
+
+# ---------------------------------------------------------------- NEXT-1: inference layers
+
+def _lin_rel(f_in):
+    """Bound for y = act(A (x W) + b) with an fp32 GEMM of f_in terms (any
+    summation order: gamma_{f_in} <= f_in * 2^-24) followed by the SpMM bound
+    1e-5 (north_star); ReLU / ELU are 1-Lipschitz."""
+    return 1e-5 + f_in * 2.0 ** -24
+
+
+@pytest.mark.parametrize("f_in,f_out", [(3, 5), (33, 7), (128, 41), (602, 128)])
+def test_linear_parity(f_in, f_out):
+    x = uniform((5000, f_in), seed=1)
+    w = uniform((f_in, f_out), seed=2)
+    y = host(G.gsp_linear(dev(x), dev(w)))
+    yr, c = orc.linear(x, w)
+    assert_within(y, yr, c, rel=f_in * 2.0 ** -24 + 1e-7, what=f"linear {f_in}x{f_out}")
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "elu"])
+def test_gcn_layer_parity(built, act):
+    for name in ("isolated-nofill", "cl4000", "hubs"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        x = uniform((go.n, 37), seed=3)
+        w = uniform((37, 20), seed=4)
+        b = uniform(20, seed=5)
+        y = host(G.gsp_gcn_layer(gn, dev(x), dev(w), dev(b), act))
+        yr, c = orc.gcn_layer(go.row_ptr, go.col, a64, x, w, b, act)
+        assert_within(y, yr, c, rel=_lin_rel(37), what=f"{name} {act}")
+
+
+@pytest.mark.parametrize("H,D", [(4, 32), (1, 41), (8, 8)])
+def test_gat_aggregate_bias_act_parity(built, H, D):
+    go, gg, _, _ = built["cl4000"]
+    n = go.n
+    z = uniform((n, H * D), seed=3)
+    el = uniform((n, H), seed=4, low=-3, high=3)
+    er = uniform((n, H), seed=5, low=-3, high=3)
+    b = uniform(H * D, seed=6)
+    y = host(G.gsp_gat_aggregate_bias_act(gg, dev(el), dev(er), dev(z), H, D, dev(b), "elu"))
+    s = orc.gat_scores(go.row_ptr, go.col, el, er, H)
+    al = orc.edge_softmax(go.row_ptr, s, H)
+    yr, c = orc.multihead_spmm(go.row_ptr, go.col, al, z, H, D)
+    assert_within(y, orc.bias_act(yr, b, "elu"), c + np.abs(b), what=f"H={H} D={D}")
+
+
+def test_gcn_inference_sampled_rows_c4():
+    """2-layer GCN on C4 through paper_2103_00959_b200.inference: layer 1 vs the
+    oracle on sampled rows; layer 2 from the GPU's own layer-1 output."""
+    from paper_2103_00959_b200.inference import GCNParams, gcn_inference
+    cfg = CONFIGS["C4"]
+    from synth import graph_for
+    s, d = graph_for(cfg, seed=1)
+    gn = G.gsp_sym_normalize(gpu_build(cfg.n, s, d))
+    go = orc.CSR(cfg.n, host(gn.row_ptr), host(gn.col), host(gn.val))
+    a = go.val.astype(np.float64)
+    x = features(cfg.n, cfg.f, cfg.ld, seed=2)
+    p = GCNParams.init(cfg.f, 128, 41, DEV, seed=1)
+    h1 = host(G.gsp_gcn_layer(gn, dev(x), p.w1, p.b1, "relu"))
+    out = host(gcn_inference(gn, dev(x), p))
+    rng = np.random.default_rng(0)
+    rows = rng.choice(cfg.n, 60, replace=False)
+    x602 = np.ascontiguousarray(x[:, :cfg.f])
+    w1, b1, w2, b2 = host(p.w1), host(p.b1), host(p.w2), host(p.b2)
+    for r in rows:
+        yr, c = orc.gcn_layer(go.row_ptr, go.col, a, x602, w1, b1, "relu", r0=r, r1=r + 1)
+        assert_within(h1[r:r + 1], yr, c, rel=_lin_rel(cfg.f), what=f"layer1 row {r}")
+        y2, c2 = orc.gcn_layer(go.row_ptr, go.col, a, h1, w2, b2, "none", r0=r, r1=r + 1)
+        assert_within(out[r:r + 1], y2, c2, rel=_lin_rel(128), what=f"layer2 row {r}")
