@@ -18,6 +18,7 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
                        int32_t slab_req, int32_t block_req, EngineLaunch *L, int max_hpt) {
   int V = vmax;
   int64_t SW = 0;
+  if (head_dim > 0 && head_dim == f && slab_req <= 0) head_dim = 0;  // one head cannot be straddled: plain plan
   if (head_dim > 0) {
     while (V > 1 && head_dim % V) V /= 2;
     const int64_t heads = f / head_dim;

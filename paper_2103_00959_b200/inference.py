@@ -23,6 +23,12 @@ import torch
 from . import (CSR, gsp_attn_project, gsp_gat_aggregate_bias_act, gsp_gcn_layer, gsp_linear)
 
 
+def _padded(n: int, cols: int, device) -> torch.Tensor:
+    """[n, cols] view of an [n, round_up(cols, 4)] buffer: rows stay 16-byte
+    aligned so the engine's float4 path applies to any width."""
+    return torch.empty((n, (cols + 3) // 4 * 4), dtype=torch.float32, device=device)[:, :cols]
+
+
 def _glorot(shape, rng):
     lim = np.sqrt(6.0 / (shape[0] + shape[-1]))
     return (rng.uniform(-lim, lim, shape)).astype(np.float32)
@@ -45,8 +51,8 @@ class GCNParams:
 
 def gcn_inference(a: CSR, x: torch.Tensor, p: GCNParams) -> torch.Tensor:
     """Two GCN layers on the normalised adjacency a (2 GEMM + 2 SpMM launches)."""
-    h1 = gsp_gcn_layer(a, x, p.w1, p.b1, "relu")
-    return gsp_gcn_layer(a, h1, p.w2, p.b2, "none")
+    h1 = gsp_gcn_layer(a, x, p.w1, p.b1, "relu", y=_padded(a.n_rows, p.w1.shape[1], x.device))
+    return gsp_gcn_layer(a, h1, p.w2, p.b2, "none", y=_padded(a.n_rows, p.w2.shape[1], x.device))
 
 
 @dataclass
@@ -77,9 +83,12 @@ class GATParams:
 
 def gat_inference(a: CSR, x: torch.Tensor, p: GATParams, negative_slope: float = 0.2) -> torch.Tensor:
     """Two GAT layers on the self-looped graph a (values unused)."""
-    z1 = gsp_linear(x, p.w1)
+    dev = x.device
+    z1 = gsp_linear(x, p.w1, y=_padded(a.n_cols, p.w1.shape[1], dev))
     el1, er1 = gsp_attn_project(z1, p.al1, p.ar1, p.heads1, p.d1)
-    h1 = gsp_gat_aggregate_bias_act(a, el1, er1, z1, p.heads1, p.d1, p.b1, "elu", negative_slope)
-    z2 = gsp_linear(h1, p.w2)
+    h1 = gsp_gat_aggregate_bias_act(a, el1, er1, z1, p.heads1, p.d1, p.b1, "elu", negative_slope,
+                                    y=_padded(a.n_rows, p.heads1 * p.d1, dev))
+    z2 = gsp_linear(h1, p.w2, y=_padded(a.n_cols, p.classes, dev))
     el2, er2 = gsp_attn_project(z2, p.al2, p.ar2, 1, p.classes)
-    return gsp_gat_aggregate_bias_act(a, el2, er2, z2, 1, p.classes, p.b2, "none", negative_slope)
+    return gsp_gat_aggregate_bias_act(a, el2, er2, z2, 1, p.classes, p.b2, "none", negative_slope,
+                                      y=_padded(a.n_rows, p.classes, dev))

@@ -553,3 +553,24 @@ def test_gcn_inference_sampled_rows_c4():
         assert_within(h1[r:r + 1], yr, c, rel=_lin_rel(cfg.f), what=f"layer1 row {r}")
         y2, c2 = orc.gcn_layer(go.row_ptr, go.col, a, h1, w2, b2, "none", r0=r, r1=r + 1)
         assert_within(out[r:r + 1], y2, c2, rel=_lin_rel(128), what=f"layer2 row {r}")
+
+
+def test_gat_inference_end_to_end_small(built):
+    """2-layer GAT through inference.gat_inference vs the oracle composed from
+    the GPU's own layer-1 intermediates (linear, attention projection, fused
+    aggregate with ELU; output layer with one 41-wide head)."""
+    from paper_2103_00959_b200.inference import GATParams, gat_inference, _padded
+    go, gg, _, _ = built["cl4000"]
+    n = go.n
+    x = uniform((n, 50), seed=1)
+    p = GATParams.init(50, 128, 4, 41, DEV, seed=2)
+    out = host(gat_inference(gg, dev(x), p))
+    z1 = G.gsp_linear(dev(x), p.w1, y=_padded(n, 128, DEV))
+    el1, er1 = G.gsp_attn_project(z1, p.al1, p.ar1, 4, 32)
+    h1 = G.gsp_gat_aggregate_bias_act(gg, el1, er1, z1, 4, 32, p.b1, "elu", y=_padded(n, 128, DEV))
+    z2 = G.gsp_linear(h1, p.w2, y=_padded(n, 41, DEV))
+    el2, er2 = G.gsp_attn_project(z2, p.al2, p.ar2, 1, 41)
+    s = orc.gat_scores(go.row_ptr, go.col, host(el2), host(er2), 1)
+    al = orc.edge_softmax(go.row_ptr, s, 1)
+    yr, c = orc.multihead_spmm(go.row_ptr, go.col, al, host(z2), 1, 41)
+    assert_within(out, orc.bias_act(yr, host(p.b2), "none"), c, what="gat output layer")
