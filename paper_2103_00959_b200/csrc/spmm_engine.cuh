@@ -361,9 +361,6 @@ __device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor b
 
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
-#ifndef GSP_PIPE
-#define GSP_PIPE 0
-#endif
 template <int V, int G, class Row, class R, bool kFull, class Pre>
 __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
                                            const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
@@ -397,24 +394,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       }
     }
   };
-  if constexpr (GSP_PIPE && EPS / U >= 2) {
-    // software pipeline: the gathers of chunk k+1 are issued before chunk k is
-    // consumed, so each lane keeps U..2U gathers in flight continuously
-    float xa[U][V], xc[U][V];
-    load(0, xa);
-    pre();
-#pragma unroll
-    for (int t0 = 0; t0 < EPS; t0 += 2 * U) {
-      const bool more1 = t0 + U < EPS && (kFull || SPR * (t0 + U) < cnt);
-      if (more1) load(t0 + U, xc);
-      fma(t0, xa);
-      if (!more1) break;
-      const bool more2 = t0 + 2 * U < EPS && (kFull || SPR * (t0 + 2 * U) < cnt);
-      if (more2) load(t0 + 2 * U, xa);
-      fma(t0 + U, xc);
-      if (!more2) break;
-    }
-  } else {
+  {
 #pragma unroll
     for (int t0 = 0; t0 < EPS; t0 += U) {
       if (!kFull && SPR * t0 >= cnt) break;
