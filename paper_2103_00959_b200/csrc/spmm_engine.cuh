@@ -363,7 +363,7 @@ __device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor b
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
 template <int V, int G, class Row, class R, bool kFull, class Pre>
 __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
-                                           const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, bool active,
+                                           const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, int nact,
                                            int sg, float (&a)[Team<G>::NACC][V], Pre &&pre) {
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
@@ -374,8 +374,12 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       const int j = sg + SPR * (t0 + u);
       const bool ok = kFull || j < cnt;
       const uint32_t cj = ok ? (uint32_t)sc[j] : 0u;
-      if (ok && active) {
+      if (ok && nact == V) {
         vld<V>(xv[u], xb + cj * ldxv);
+      } else if (ok && nact > 0) {  // last vector of the row-slab: only columns < f are read
+        const float *src = reinterpret_cast<const float *>(xb + cj * ldxv);
+#pragma unroll
+        for (int i = 0; i < V; ++i) xv[u][i] = i < nact ? __ldg(src + i) : 0.0f;
       } else {
 #pragma unroll
         for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
@@ -423,7 +427,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 template <int V, int G, bool kLong, class R, class Row, class Pro>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
-                                             const typename VecT<V>::T *__restrict__ xb, bool active, int tl, int sg,
+                                             const typename VecT<V>::T *__restrict__ xb, int nact, int tl, int sg,
                                              unsigned tmask, int32_t *tc, float *tw, int hl, const double *cache,
                                              int ncache, float (&out)[V], Pro &&prologue) {
   using TM = Team<G>;
@@ -486,8 +490,8 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < V; ++i) a[q][i] = R::init();
-    if (cnt == kSeg) seg_gather<V, G, Row, R, true>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
-    else seg_gather<V, G, Row, R, false>(sc, sw, cnt, xb, p.ldxv, active, sg, a, pre);
+    if (cnt == kSeg) seg_gather<V, G, Row, R, true>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
+    else seg_gather<V, G, Row, R, false>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
     if (scratch) __syncwarp(tmask);  // scratch is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
@@ -621,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   const int64_t col0 = slab * SW + (int64_t)gl * V;
   const bool active = col0 < p.f;
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
+  const int nact = active ? nvalid : 0;  // columns this lane gathers
   const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
   const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
@@ -639,6 +644,12 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   const Window win{s_col, p.stage_val ? s_val : nullptr, s_win[0], s_win[1]};
   const int64_t wchunk = s_win[2];
   int ready = 0;  // chunks this thread has seen complete
+#ifdef GSP_DEBUG_WINDOW_BARRIER
+  // debug builds: every thread waits for the whole window, then a CTA barrier
+  if (p.stage)
+    for (; ready < kStageChunks && win.wb + ready * wchunk < win.we; ++ready) mbar_wait(&s_bar[ready], 0);
+  __syncthreads();
+#endif
   // wait until the window covers [.., e_end) (or all of it)
   auto ensure = [&](int64_t e_end) {
     if (!p.stage) return;
@@ -681,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G, true, R>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, active, tl, sg, tmask,
+      row_segments<V, G, true, R>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, nact, tl, sg, tmask,
                                   s_tc[team], s_tw[team], hl, nullptr, 0, part, [] {});
       if (sg == 0) {
 #pragma unroll
@@ -745,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
       }
     };
     float out[V];
-    row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, active, tl, sg, tmask,
+    row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, nact, tl, sg, tmask,
                                  s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr, kGat ? kCache : 0,
                                  out, stats);
     finish_row<R, V>(out, d, p.mean);
