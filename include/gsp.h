@@ -138,7 +138,10 @@ gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, 
  * a3. SpMM  Y = A X  (GSpMM, phi = sum, psi = multiply).
  * P:640-645 (§4.1 Eq. formula:1; "SpMM operator H^(l+1) <- A H^(l)"),
  * P:646-648 (kernel design: CSR, coalesced feature access, cached indices).
- *   x  device fp32 [a->n_cols][ldx], columns [0, f) used
+ *   x  device fp32 [a->n_cols][ldx], columns [0, f) used; the whole
+ *      [n_cols][ldx] extent must be readable: padding columns [f, ldx) that
+ *      share a 16-byte vector with column f-1 may be read, their values are
+ *      never used (any bits, including NaN, are fine)
  *   y  device fp32 [a->n_rows][ldy], columns [0, f) written
  *   f >= 0, ldx >= f, ldy >= f.  x and y must not overlap (GSP_ERR_ALIAS).
  * fp32 multiply-add; error bound per element in DESIGN.md §Summation order
@@ -241,16 +244,21 @@ gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, const float *z,
  *   s[e,h]  = LeakyReLU(el[u,h] + er[v,h]; negative_slope)     e = (u,v), A13
  *   alpha   = edge softmax of s over row u, per head
  *   Y[u,h,:] = sum_e alpha[e,h] Z[v,h,:]
- * ONE launch: the team that owns a (row, head) first reduces the row's
- * softmax statistics (max and sum of exp, fp64, warp-shuffle butterflies;
- * hub rows: the whole CTA) and then runs the fused score -> softmax ->
- * aggregate pass.  Per-edge scores and alpha are never materialised unless
- * alpha_out is non-NULL.
+ * Two schedules, same result up to fp rounding of the statistics:
+ *  - ws given (>= gsp_gat_workspace bytes, 16-byte aligned, heads | 32): a
+ *    statistics launch (one warp per row for all heads: max and sum of exp
+ *    in fp64 with warp-shuffle xor trees) writes (m, 1/S) per (row,
+ *    head) into ws, then the aggregate launch forms alpha on the fly;
+ *  - ws NULL (or too small): ONE launch; the team that owns a (row, head)
+ *    first reduces the row's statistics (hub rows: the whole CTA) and then
+ *    runs the fused score -> softmax -> aggregate pass.
+ * Per-edge scores and alpha are never materialised unless alpha_out is
+ * non-NULL.
  *   el  device fp32 [a->n_rows][heads];  er device fp32 [a->n_cols][heads]
  *   z   device fp32 [a->n_cols][ldz] ([H][D]);  y device fp32 [a->n_rows][ldy]
  *   alpha_out  device fp32 [nnz][heads] or NULL
- *   ws  device workspace of gsp_gat_workspace(a, heads) bytes (currently 0:
- *       ws may be NULL; the parameter is kept for ABI stability)
+ *   ws  NULL, or device workspace of gsp_gat_workspace(a, heads) bytes
+ *       (= n_rows * heads * 16: fp64 max + fp32 1/S per (row, head))
  * The score is formed in fp64 (el + er, slope multiply, minus the row max) and
  * rounded once before the fp32 exponential.
  */
@@ -316,7 +324,7 @@ gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const 
  * gsp_gcn_layer: y = act(A (x w) + bias): gsp_linear into ws, then
  *   gsp_spmm_bias_act.  ws >= gsp_gcn_layer_workspace(a->n_cols, f_out).
  * gsp_gat_aggregate_bias_act: gsp_gat_aggregate with y = act(Y + bias[H*D])
- *   fused (ELU for hidden GAT layers). */
+ *   fused (ELU for hidden GAT layers); ws as for gsp_gat_aggregate. */
 typedef enum { GSP_ACT_NONE = 0, GSP_ACT_RELU = 1, GSP_ACT_ELU = 2 } gsp_act;
 gsp_status gsp_linear(int64_t n, int64_t f_in, const float *x, int64_t ldx, const float *w, int64_t ldw,
                       int64_t f_out, float *y, int64_t ldy, gsp_stream stream);
@@ -328,7 +336,8 @@ gsp_status gsp_gcn_layer(const gsp_csr *a, const float *x, int64_t f_in, int64_t
                          size_t ws_bytes, gsp_stream stream);
 gsp_status gsp_gat_aggregate_bias_act(const gsp_csr *a, int32_t heads, const float *el, const float *er,
                                       double negative_slope, const float *z, int64_t d, int64_t ldz,
-                                      const float *bias, gsp_act act, float *y, int64_t ldy, gsp_stream stream);
+                                      const float *bias, gsp_act act, float *y, int64_t ldy, void *ws,
+                                      size_t ws_bytes, gsp_stream stream);
 
 /* ---------------------------------------------------------------------------
  * Multi-GPU row partition.

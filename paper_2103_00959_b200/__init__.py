@@ -92,7 +92,7 @@ def lib() -> ctypes.CDLL:
             "gsp_spmm_bias_act": [CP, P, I, I, P, ctypes.c_int, P, I, P],
             "gsp_gcn_layer_workspace": [I, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_gcn_layer": [CP, P, I, I, P, I, P, ctypes.c_int, P, I, P, ctypes.c_size_t, P],
-            "gsp_gat_aggregate_bias_act": [CP, I32, P, P, D, P, I, I, P, ctypes.c_int, P, I, P],
+            "gsp_gat_aggregate_bias_act": [CP, I32, P, P, D, P, I, I, P, ctypes.c_int, P, I, P, ctypes.c_size_t, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
             "gsp_edge_softmax": [CP, I32, P, P, P],
@@ -325,11 +325,20 @@ def gsp_gat_workspace(a: CSR, heads: int) -> int:
     return n.value
 
 
+def _gat_ws(a: CSR, heads: int, device, ws: Optional[torch.Tensor]) -> torch.Tensor:
+    need = gsp_gat_workspace(a, heads)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
+    return ws
+
+
 def gsp_gat_aggregate(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tensor, heads: int, d: int,
                       negative_slope: float = 0.2, y: Optional[torch.Tensor] = None, alpha_out=None,
-                      ws: Optional[torch.Tensor] = None, stream=None):
+                      ws: Optional[torch.Tensor] = None, single_launch: bool = False, stream=None):
     """Fused LeakyReLU score -> edge softmax -> multi-head SpMM (gsp.h a5+a6+a7).
-    alpha_out: None, True (allocate) or a [nnz, heads] tensor.  Returns y or (y, alpha)."""
+    alpha_out: None, True (allocate) or a [nnz, heads] tensor.  Returns y or (y, alpha).
+    ws: statistics workspace (allocated when None); single_launch=True passes no
+    workspace, so the statistics are reduced inside the aggregate kernel."""
     _vec(el, torch.float32, "el")
     _vec(er, torch.float32, "er")
     z, ldz = _mat(z, "z")
@@ -339,13 +348,11 @@ def gsp_gat_aggregate(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tenso
     want = alpha_out is not None
     if alpha_out is True:
         alpha_out = torch.empty((a.nnz, heads), dtype=torch.float32, device=z.device)
-    need = gsp_gat_workspace(a, heads)
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=z.device)
+    ws = None if single_launch else _gat_ws(a, heads, z.device, ws)
     v = a.view()
     _check(lib().gsp_gat_aggregate(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope), _ptr(z), d,
-                                   ldz, _ptr(y), ldy, _ptr(alpha_out if want else None), _ptr(ws), ws.numel(),
-                                   _stream(stream)), "gsp_gat_aggregate")
+                                   ldz, _ptr(y), ldy, _ptr(alpha_out if want else None), _ptr(ws),
+                                   0 if ws is None else ws.numel(), _stream(stream)), "gsp_gat_aggregate")
     return (y, alpha_out) if want else y
 
 
@@ -552,13 +559,17 @@ def gsp_gcn_layer(a: CSR, x: torch.Tensor, w: torch.Tensor, bias: Optional[torch
 
 def gsp_gat_aggregate_bias_act(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tensor, heads: int, d: int,
                                bias: Optional[torch.Tensor] = None, act: str = "none", negative_slope: float = 0.2,
-                               y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                               y: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+                               single_launch: bool = False, stream=None) -> torch.Tensor:
+    """gsp_gat_aggregate with act(Y + bias) fused; ws / single_launch as there."""
     z, ldz = _mat(z, "z")
     y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device) if y is None else y
     y, ldy = _mat(y, "y")
+    ws = None if single_launch else _gat_ws(a, heads, z.device, ws)
     v = a.view()
     _check(lib().gsp_gat_aggregate_bias_act(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope),
-                                            _ptr(z), d, ldz, _ptr(bias), ACT[act], _ptr(y), ldy, _stream(stream)),
+                                            _ptr(z), d, ldz, _ptr(bias), ACT[act], _ptr(y), ldy, _ptr(ws),
+                                            0 if ws is None else ws.numel(), _stream(stream)),
            "gsp_gat_aggregate_bias_act")
     return y
 

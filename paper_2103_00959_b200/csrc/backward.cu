@@ -259,7 +259,7 @@ struct WeightAlphaPerm {
   const int32_t *perm;
   int heads;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true, kInStats = false;
     const float *alpha;
     const int32_t *perm;
     int heads, h;

@@ -7,50 +7,227 @@
 namespace gsp {
 
 // ------------------------------------------------------------------------
-// Row statistics: m[u,h] = max_e s[e,h] (fp64) and 1 / sum_e exp(s - m).
-// One warp per row; lane l serves head l % H and every (32/H)-th edge, so
-// the max and the sum are warp-shuffle reductions over lanes of equal head
-// ("warp level intrinsic ... find the max ... reduce ... the sum").
-// Order per (row, head): sequential per lane, then an xor tree -> fixed.
+// Row statistics: m[u,h] = max_e s[e,h] (fp64) and 1 / sum_e exp(s - m),
+// all heads of a row at once ("warp level intrinsic ... find the max
+// ... reduce ... the sum").  H (heads, dividing 32) is a template parameter.
+// Grid: one CTA of 8 warps per 32 rows; warp w owns rows 4w .. 4w+3 of them.
+//  * SHORT rows (<= kTile = 1024 / H entries): the entries of the warp's 4
+//    rows (contiguous in CSR) are loaded into the warp's shared tile
+//    T[kTile][H] in one sweep when they fit (else row by row); each lane
+//    issues all of its loads before the first use (kU entries in flight).
+//    Then, per row, lane l reduces head h = l % H over the row's entries
+//    part, part + P, ... (part = l / H, P = 32 / H) and an xor tree over
+//    lanes of equal head finishes the max and the sum.  exp(s - m) stays in
+//    the tile for the apply pass.
+//  * LONG rows: the whole CTA, after the short rows.  Warp w takes the
+//    tile-sized chunks w, w+8, ... of the row (same tile and lane layout),
+//    then the xor tree per warp and the 8 warps' partials in warp order.
+// Every order depends on the row alone (deterministic, partition-invariant).
 // ------------------------------------------------------------------------
 // kScores: s from el/er (GAT) or s = logits (edge softmax).
-// kApply : write alpha = exp(s - m) / sum in a third pass (standalone edge
-//          softmax; logits may alias alpha) instead of storing the statistics.
-template <bool kScores, bool kApply>
-__global__ void __launch_bounds__(256) row_stats_warp(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                                      const float *__restrict__ el, const float *__restrict__ er,
-                                                      const float *logits, double slope, int H, int64_t n_rows,
-                                                      GatStat *__restrict__ st, float *alpha) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (r >= n_rows) return;
-  const int lane = threadIdx.x & 31;
-  const int h = lane % H, j0 = lane / H, step = 32 / H;
-  const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-  if (b == e1) return;
-  const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-  auto score = [&](int64_t e) -> double {
-    if (kScores) {
-      const double t = el_u + (double)__ldg(er + (int64_t)__ldg(col + e) * H + h);
-      return t >= 0.0 ? t : slope * t;
-    } else {
-      return (double)logits[e * H + h];
+// kApply : write alpha = exp(s - m) / sum (standalone edge softmax; logits
+//          may alias alpha) instead of storing the statistics.
+constexpr int kStatWarps = 8;
+constexpr int kStatRPW = 4;            // rows per warp
+constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
+
+template <bool kScores>
+__device__ __forceinline__ double stat_score(float t, double el_u, double slope) {
+  if (kScores) {
+    const double x = el_u + (double)t;
+    return x >= 0.0 ? x : slope * x;
+  }
+  return (double)t;
+}
+
+// entries [e0, e0 + cnt) of the CSR -> T[j][H] (er rows of their columns, or logits rows)
+template <int H, bool kScores>
+__device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
+                                          const float *__restrict__ er, const float *logits, int lane) {
+  if (kScores) {
+    constexpr int kU = (32 / H) < 4 ? ((32 / H) < 1 ? 1 : 32 / H) : 4;  // entries per lane per round
+    constexpr int kV = H >= 4 ? 4 : H;                                 // floats per load
+    using VT = typename VecT<kV>::T;
+    for (int base = 0; base < cnt; base += 32 * kU) {
+      int c[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = base + lane + 32 * u;
+        c[u] = j < cnt ? __ldg(col + e0 + j) : 0;
+      }
+      float v[kU][H];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = base + lane + 32 * u;
+#pragma unroll
+        for (int q = 0; q < H; q += kV) {
+          if (j < cnt) {
+            float t[kV];
+            vld<kV>(t, reinterpret_cast<const VT *>(er + (int64_t)c[u] * H + q));
+#pragma unroll
+            for (int i = 0; i < kV; ++i) v[u][q + i] = t[i];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = base + lane + 32 * u;
+        if (j < cnt) {
+#pragma unroll
+          for (int q = 0; q < H; q += kV) {
+            float t[kV];
+#pragma unroll
+            for (int i = 0; i < kV; ++i) t[i] = v[u][q + i];
+            Vec<kV>::st_shared(T + j * H + q, t);
+          }
+        }
+      }
     }
-  };
+  } else {
+    const float *src = logits + e0 * H;  // cnt rows of H logits are contiguous
+    const int nf = cnt * H;
+    constexpr int kU = 8;
+    for (int base = 0; base < nf; base += 32 * kU) {
+      float v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = base + lane + 32 * u;
+        v[u] = k < nf ? src[k] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = base + lane + 32 * u;
+        if (k < nf) T[k] = v[u];
+      }
+    }
+  }
+}
+
+// reduce one short row held in T[0 .. d) and write its statistics or alpha
+template <int H, bool kScores, bool kApply>
+__device__ __forceinline__ void stat_row(float *T, int64_t r, int64_t b, int d, const float *__restrict__ el,
+                                         double slope, GatStat *__restrict__ st, float *alpha, int lane) {
+  constexpr int P = 32 / H;
+  const int h = lane % H, part = lane / H;
+  const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
   double m = -INFINITY;
-  for (int64_t e = b + j0; e < e1; e += step) m = fmax(m, score(e));
+  for (int j = part; j < d; j += P) m = fmax(m, stat_score<kScores>(T[j * H + h], el_u, slope));
+#pragma unroll
   for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
   double s = 0.0;
-  for (int64_t e = b + j0; e < e1; e += step) s += (double)expf((float)(score(e) - m));
+  for (int j = part; j < d; j += P) {
+    const float ex = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - m));
+    s += (double)ex;
+    if (kApply) T[j * H + h] = ex;  // own slot: no other lane reads it
+  }
+#pragma unroll
   for (int off = H; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const float inv_s = (float)(1.0 / s);
   if (kApply) {
-    const float inv_s = (float)(1.0 / s);
-    for (int64_t e = b + j0; e < e1; e += step) alpha[e * H + h] = expf((float)(score(e) - m)) * inv_s;
-  } else if (lane < H) {
+    for (int j = part; j < d; j += P) alpha[(b + j) * H + h] = T[j * H + h] * inv_s;  // lane-contiguous
+  } else if (part == 0) {
     GatStat g;
     g.m = m;
-    g.inv_s = (float)(1.0 / s);
+    g.inv_s = inv_s;
     g.pad = 0.f;
     st[r * H + h] = g;
+  }
+}
+
+template <int H, bool kScores, bool kApply>
+__global__ void __launch_bounds__(kStatWarps * 32, 4) row_stats_warp(const int64_t *__restrict__ rp,
+                                                                  const int32_t *__restrict__ col,
+                                                                  const float *__restrict__ el,
+                                                                  const float *__restrict__ er, const float *logits,
+                                                                  double slope, int64_t n_rows,
+                                                                  GatStat *__restrict__ st, float *alpha) {
+  constexpr int kTile = kStatTileFloats / H;
+  __shared__ __align__(16) float s_tile[kStatWarps][kStatTileFloats];
+  __shared__ int s_long[kStatWarps * kStatRPW];
+  __shared__ int s_nlong;
+  __shared__ double s_red[kStatWarps][H];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (tid == 0) s_nlong = 0;
+  __syncthreads();
+  const int64_t rbase = (int64_t)blockIdx.x * kStatWarps * kStatRPW;
+  {
+    float *T = s_tile[warp];
+    const int64_t r0 = rbase + warp * kStatRPW;
+    const int64_t bl = (lane <= kStatRPW) ? __ldg(rp + min(r0 + lane, n_rows)) : 0;
+    int64_t B[kStatRPW + 1];
+#pragma unroll
+    for (int k = 0; k <= kStatRPW; ++k) B[k] = __shfl_sync(0xffffffffu, bl, k);
+    const bool together = B[kStatRPW] - B[0] <= kTile;
+    if (together) stat_load<H, kScores>(T, B[0], (int)(B[kStatRPW] - B[0]), col, er, logits, lane);
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kStatRPW; ++k) {
+      const int64_t d = B[k + 1] - B[k];
+      if (d == 0) continue;
+      if (d > kTile) {
+        if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp * kStatRPW + k;
+        continue;
+      }
+      float *Tk = T;
+      if (together) {
+        Tk = T + (B[k] - B[0]) * H;
+      } else {
+        __syncwarp();
+        stat_load<H, kScores>(T, B[k], (int)d, col, er, logits, lane);
+        __syncwarp();
+      }
+      stat_row<H, kScores, kApply>(Tk, r0 + k, B[k], (int)d, el, slope, st, alpha, lane);
+    }
+  }
+  __syncthreads();
+  // long rows: the whole CTA; warp w takes tile-sized chunks w, w+8, ... of
+  // the row (same tile loads and lane layout as short rows), partials of the
+  // 8 warps combined in warp order
+  const int nlong = s_nlong;
+  float *T = s_tile[warp];
+  constexpr int P = 32 / H;
+  const int h = lane % H, part = lane / H;
+  for (int k = 0; k < nlong; ++k) {
+    const int64_t r = rbase + s_long[k];
+    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+    const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
+    double m = -INFINITY, sum = 0.0;
+    for (int pass = 0; pass < (kApply ? 3 : 2); ++pass) {
+      const float inv_s = pass == 2 ? (float)(1.0 / sum) : 0.0f;
+      double acc = pass == 0 ? -INFINITY : 0.0;
+      for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
+        const int cnt = (int)min((int64_t)kTile, e1 - c0);
+        __syncwarp();
+        stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
+        __syncwarp();
+        for (int j = part; j < cnt; j += P) {
+          const double sc = stat_score<kScores>(T[j * H + h], el_u, slope);
+          if (pass == 0) acc = fmax(acc, sc);
+          else if (pass == 1) acc += (double)expf((float)(sc - m));
+          else alpha[(c0 + j) * H + h] = expf((float)(sc - m)) * inv_s;
+        }
+      }
+      if (pass == 2) break;
+#pragma unroll
+      for (int off = H; off < 32; off <<= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, acc, off);
+        acc = pass == 0 ? fmax(acc, o) : acc + o;
+      }
+      if (part == 0) s_red[warp][h] = acc;
+      __syncthreads();
+      double x = s_red[0][h];
+      for (int w = 1; w < kStatWarps; ++w) x = pass == 0 ? fmax(x, s_red[w][h]) : x + s_red[w][h];
+      __syncthreads();
+      if (pass == 0) m = x;
+      else sum = x;
+    }
+    if (!kApply && warp == 0 && part == 0) {
+      GatStat g;
+      g.m = m;
+      g.inv_s = (float)(1.0 / sum);
+      g.pad = 0.f;
+      st[r * H + h] = g;
+    }
   }
 }
 
@@ -94,10 +271,19 @@ template <bool kScores, bool kApply>
 static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *er, const float *logits, double slope,
                                int H, GatStat *st, float *alpha, cudaStream_t s) {
   if (a->n_rows == 0) return GSP_OK;
-  if (32 % H == 0) {
-    const int64_t blocks = ceil_div(a->n_rows, 8);
-    row_stats_warp<kScores, kApply><<<(unsigned)blocks, 256, 0, s>>>(a->row_ptr, a->col_idx, el, er, logits, slope,
-                                                                      H, a->n_rows, st, alpha);
+  const float *vsrc = kScores ? er : logits;
+  const bool vec_ok = H < 4 ? (H == 1 || aligned8(vsrc)) : aligned16(vsrc);
+  if (32 % H == 0 && (vec_ok || !kScores)) {
+    const unsigned blocks = (unsigned)ceil_div(a->n_rows, kStatWarps * kStatRPW);
+#define GSP_STATS_H(HH)                                                                                       \
+  case HH:                                                                                                   \
+    row_stats_warp<HH, kScores, kApply><<<blocks, kStatWarps * 32, 0, s>>>(a->row_ptr, a->col_idx, el, er,     \
+                                                                         logits, slope, a->n_rows, st, alpha); \
+    break;
+    switch (H) {
+      GSP_STATS_H(1) GSP_STATS_H(2) GSP_STATS_H(4) GSP_STATS_H(8) GSP_STATS_H(16) GSP_STATS_H(32)
+    }
+#undef GSP_STATS_H
   } else {
     const int64_t blocks = ceil_div(a->n_rows * H, 256);
     row_stats_thread<kScores, kApply><<<(unsigned)blocks, 256, 0, s>>>(a->row_ptr, a->col_idx, el, er, logits,
@@ -220,14 +406,14 @@ extern "C" gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, cons
 extern "C" gsp_status gsp_gat_workspace(const gsp_csr *a, int32_t heads, size_t *ws_bytes) {
   clear_detail();
   if (!a || heads <= 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_gat_workspace: bad argument");
-  *ws_bytes = 0;  // the softmax statistics live in registers / shared memory of the fused kernel
+  *ws_bytes = (size_t)std::max<int64_t>(a->n_rows, 0) * heads * sizeof(GatStat);  // (m, 1/S) per (row, head)
   return GSP_OK;
 }
 
 static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const float *el, const float *er,
                                      double negative_slope, const float *z, int64_t d, int64_t ldz, float *y,
-                                     int64_t ldy, float *alpha_out, const float *bias, int act, cudaStream_t s,
-                                     const char *fn) {
+                                     int64_t ldy, float *alpha_out, const float *bias, int act, void *ws,
+                                     size_t ws_bytes, cudaStream_t s, const char *fn) {
   clear_detail();
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
@@ -243,8 +429,14 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   int vmax = 1;
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
+  // two launches when the workspace can hold the statistics (row_stats_warp
+  // for all heads, then the aggregate, several whole heads per team);
+  // otherwise one launch with the statistics reduced inside the aggregate
+  // kernel, one head per team (fp64 row state in registers)
+  const size_t need = (size_t)a->n_rows * heads * sizeof(GatStat);
+  const bool pre = ws && ws_bytes >= need && aligned16(ws) && 32 % heads == 0;
   EngineLaunch L;
-  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, 1);  // one head per team (fp64 state in registers)
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, pre ? kMaxHpt : 1);
   if (st) return st;
   EngineParams p;
   p.row_ptr = a->row_ptr;
@@ -264,24 +456,28 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   p.bias = bias;
   p.act = act;
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
-  WeightGat w{el, er, alpha_out, negative_slope, heads};
+  if (pre) {
+    GatStat *stat = static_cast<GatStat *>(ws);
+    if ((st = launch_stats<true, false>(a, el, er, nullptr, negative_slope, heads, stat, nullptr, s))) return st;
+    WeightGatPre w{el, er, alpha_out, negative_slope, heads, stat};
+    return engine_launch(L, p, w, s);
+  }
+  WeightGat w{el, er, alpha_out, negative_slope, heads, nullptr};
   return engine_launch(L, p, w, s);
 }
 
 extern "C" gsp_status gsp_gat_aggregate(const gsp_csr *a, int32_t heads, const float *el, const float *er,
                                         double negative_slope, const float *z, int64_t d, int64_t ldz, float *y,
                                         int64_t ldy, float *alpha_out, void *ws, size_t ws_bytes, gsp_stream stream) {
-  (void)ws;
-  (void)ws_bytes;
-  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, alpha_out, nullptr, 0, cs(stream),
-                            "gsp_gat_aggregate");
+  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, alpha_out, nullptr, 0, ws, ws_bytes,
+                            cs(stream), "gsp_gat_aggregate");
 }
 
 extern "C" gsp_status gsp_gat_aggregate_bias_act(const gsp_csr *a, int32_t heads, const float *el, const float *er,
                                                  double negative_slope, const float *z, int64_t d, int64_t ldz,
-                                                 const float *bias, gsp_act act, float *y, int64_t ldy,
-                                                 gsp_stream stream) {
+                                                 const float *bias, gsp_act act, float *y, int64_t ldy, void *ws,
+                                                 size_t ws_bytes, gsp_stream stream) {
   if (act < GSP_ACT_NONE || act > GSP_ACT_ELU) return fail(GSP_ERR_INVALID_ARG, "gsp_gat_aggregate_bias_act: bad act");
-  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, nullptr, bias, (int)act, cs(stream),
-                            "gsp_gat_aggregate_bias_act");
+  return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, nullptr, bias, (int)act, ws, ws_bytes,
+                            cs(stream), "gsp_gat_aggregate_bias_act");
 }

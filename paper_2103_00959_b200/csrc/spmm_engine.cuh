@@ -88,6 +88,9 @@ struct Vec<4> {
   static __device__ __forceinline__ void st(float *p, const float (&r)[4]) {
     __stcs(reinterpret_cast<float4 *>(p), make_float4(r[0], r[1], r[2], r[3]));
   }
+  static __device__ __forceinline__ void st_shared(float *p, const float (&r)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(r[0], r[1], r[2], r[3]);
+  }
 };
 template <>
 struct Vec<8> {  // two float4 per lane (256-column slabs)
@@ -111,11 +114,15 @@ struct Vec<2> {
   static __device__ __forceinline__ void st(float *p, const float (&r)[2]) {
     __stcs(reinterpret_cast<float2 *>(p), make_float2(r[0], r[1]));
   }
+  static __device__ __forceinline__ void st_shared(float *p, const float (&r)[2]) {
+    *reinterpret_cast<float2 *>(p) = make_float2(r[0], r[1]);
+  }
 };
 template <>
 struct Vec<1> {
   static __device__ __forceinline__ void ld(float (&r)[1], const float *p) { r[0] = __ldg(p); }
   static __device__ __forceinline__ void st(float *p, const float (&r)[1]) { __stcs(p, r[0]); }
+  static __device__ __forceinline__ void st_shared(float *p, const float (&r)[1]) { *p = r[0]; }
 };
 
 template <int V>
@@ -194,7 +201,7 @@ struct RedMin {
 struct WeightVal {  // SpMM with A's values
   const float *val;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = false, kStagedVal = true, kMultiHead = false;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = true, kMultiHead = false, kInStats = false;
     const float *val;
     __device__ __forceinline__ float w(int64_t e, int /*c*/, int /*hh*/) const { return __ldcs(val + e); }
   };
@@ -203,7 +210,7 @@ struct WeightVal {  // SpMM with A's values
 
 struct WeightOne {  // SpMM with val == NULL: psi = copy
   struct Row {
-    static constexpr bool kUnit = true, kComputed = false, kStagedVal = false, kMultiHead = false;
+    static constexpr bool kUnit = true, kComputed = false, kStagedVal = false, kMultiHead = false, kInStats = false;
     __device__ __forceinline__ float w(int64_t, int, int) const { return 1.0f; }
   };
   __device__ __forceinline__ Row row(int64_t, int, bool, void *) const { return Row{}; }
@@ -213,7 +220,7 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   const float *alpha;
   int heads;
   struct Row {
-    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true;
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true, kInStats = false;
     const float *alpha;
     int heads, h;  // h: first head of the team's slab
     __device__ __forceinline__ float w(int64_t e, int, int hh) const { return __ldcs(alpha + e * heads + h + hh); }
@@ -228,37 +235,58 @@ struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax
 };
 
 // Fused GAT weight (A13): s = LeakyReLU(el[u] + er[v]) in fp64,
-// alpha = exp(s - m) / S with the row statistics (m, S) computed inside the
-// aggregate kernel by the team that owns the (row, head) -- no stats pass.
-// One head per team: the fp64 row state stays in registers (measured faster
-// than several heads per team with the state in shared memory).
-struct WeightGat {
+// alpha = exp(s - m) / S with the row statistics (m, S) of the (row, head).
+//  kPre = false: the statistics are reduced inside the aggregate kernel by
+//    the team that owns the (row, head) (single launch; one head per team, the
+//    fp64 row state in registers).
+//  kPre = true : the statistics come precomputed from row_stats_warp (gat.cu;
+//    one warp per row for all heads) through st[n_rows][H]; the aggregate
+//    kernel only forms alpha on the fly (never materialised).
+template <bool kPre>
+struct WeightGatT {
   const float *el, *er;
   float *alpha_out;
   double slope;
   int heads;
+  const GatStat *st;  // kPre only
   struct Row {
-    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = false;
+    // kPre: a team may own several whole heads (slab = hpt heads); el, m and
+    // 1/S of head h + hh are read on use (L1-resident)
+    static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = kPre, kInStats = !kPre;
     const float *er;
     float *alpha_out;
+    const float *el;
+    const GatStat *st;
+    int64_t r;
     double el_u, m, slope;
     float inv_s;
     int heads, h;
-    __device__ __forceinline__ double score(int c, int = 0) const {
-      const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
+    __device__ __forceinline__ double score(int c, int hh = 0) const {
+      const double eu = kPre ? (double)__ldg(el + r * heads + h + hh) : el_u;
+      const double t = eu + (double)__ldg(er + (int64_t)c * heads + h + hh);
       return t >= 0.0 ? t : slope * t;
     }
-    __device__ __forceinline__ float finish(int64_t e, double s, int = 0) const {
-      const float a = expf((float)(s - m)) * inv_s;
-      if (alpha_out) alpha_out[e * heads + h] = a;
+    __device__ __forceinline__ float finish(int64_t e, double s, int hh = 0) const {
+      double mm = m;
+      float is = inv_s;
+      if constexpr (kPre) {
+        const GatStat *g = st + r * heads + h + hh;
+        mm = __ldg(&g->m);
+        is = __ldg(&g->inv_s);
+      }
+      const float a = expf((float)(s - mm)) * is;
+      if (alpha_out) alpha_out[e * heads + h + hh] = a;
       return a;
     }
   };
   // first_slab: only the first slab of a head writes alpha_out (each entry once)
   __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab, void *) const {
-    return Row{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), 0.0, slope, 0.0f, heads, h};
+    return Row{er, first_slab ? alpha_out : nullptr, el, st, r, kPre ? 0.0 : (double)__ldg(el + r * heads + h),
+               0.0, slope, 0.0f, heads, h};
   }
 };
+using WeightGat = WeightGatT<false>;
+using WeightGatPre = WeightGatT<true>;
 
 // ------------------------------------------------------------------ params
 struct EngineParams {
@@ -374,12 +402,10 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       const int j = sg + SPR * (t0 + u);
       const bool ok = kFull || j < cnt;
       const uint32_t cj = ok ? (uint32_t)sc[j] : 0u;
-      if (ok && nact == V) {
+      // the last vector of a row-slab may cover ld padding (x is [n_cols][ldx],
+      // gsp.h): those columns are read whole and their sums never stored
+      if (ok && nact > 0) {
         vld<V>(xv[u], xb + cj * ldxv);
-      } else if (ok && nact > 0) {  // last vector of the row-slab: only columns < f are read
-        const float *src = reinterpret_cast<const float *>(xb + cj * ldxv);
-#pragma unroll
-        for (int i = 0; i < V; ++i) xv[u][i] = i < nact ? __ldg(src + i) : 0.0f;
       } else {
 #pragma unroll
         for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
@@ -475,7 +501,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
             for (int hh = 0; hh < kHH; ++hh) {
               if (hh == 0 || hh < p.hpt) {
                 if constexpr (Row::kComputed)
-                  tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
+                  tw[hh * kSeg + j] = wr.finish(e0 + j, (hh == 0 && cache && q < ncache) ? cache[q] : wr.score(c, hh), hh);
                 else
                   tw[hh * kSeg + j] = wr.w(e0 + j, c, hh);
               }
@@ -560,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   constexpr int kHptCap = (kMH && G >= 2) ? kMaxHpt : 1;  // G == 1 slabs never hold more than one head
   __shared__ float s_tw[NT][kHptCap * kSeg];              // per-team scratch: weights, per head
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
-  constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kComputed;
+  constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kInStats;  // in-kernel softmax statistics
   constexpr int kCache = kGat ? 1024 / NT : 1;  // per-team fp64 score cache (GAT)
   __shared__ double s_cache[NT][kCache];
   __shared__ double s_red[kThreads / 32];
@@ -862,5 +888,24 @@ gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &
   }
   return fail(GSP_ERR_UNSUPPORTED, "bad vector width %d", L.V);
 }
+
+// Explicit instantiations live in engine_inst_*.cu (one TU per weight /
+// reduce family, compiled in parallel); other TUs only declare them.
+#define GSP_ENGINE_INSTANCES(X) \
+  X(WeightVal, RedSum, sum)     \
+  X(WeightOne, RedSum, sum)     \
+  X(WeightVal, RedMax, maxmin)  \
+  X(WeightOne, RedMax, maxmin)  \
+  X(WeightVal, RedMin, maxmin)  \
+  X(WeightOne, RedMin, maxmin)  \
+  X(WeightAlpha, RedSum, alpha) \
+  X(WeightGat, RedSum, gat)     \
+  X(WeightGatPre, RedSum, gat)
+#ifndef GSP_ENGINE_INSTANTIATE
+#define GSP_ENGINE_EXTERN(W, R, tu) \
+  extern template gsp_status engine_launch<W, R>(const EngineLaunch &, const EngineParams &, const W &, cudaStream_t);
+GSP_ENGINE_INSTANCES(GSP_ENGINE_EXTERN)
+#undef GSP_ENGINE_EXTERN
+#endif
 
 }  // namespace gsp

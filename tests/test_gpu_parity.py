@@ -278,8 +278,11 @@ def _gat_ref(go, el, er, z, H, D, slope):
     return y, cond, a
 
 
+@pytest.mark.parametrize("single", [False, True], ids=["stats-launch", "single-launch"])
 @pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 64), (4, 32), (4, 1)])
-def test_gat_aggregate_parity(built, H, D):
+def test_gat_aggregate_parity(built, H, D, single):
+    """Both schedules of gsp_gat_aggregate (statistics launch + aggregate, or
+    one launch with in-kernel statistics) against the fp64 oracle."""
     for name in ("multi0", "cl4000", "rmat3000", "hubs"):
         go, gg, _, _ = built[name]
         n = go.n
@@ -288,8 +291,8 @@ def test_gat_aggregate_parity(built, H, D):
             el = uniform((n, H), seed=4, low=lo, high=hi)
             er = uniform((n, H), seed=5, low=lo, high=hi)
             yref, cond, aref = _gat_ref(go, el, er, z, H, D, 0.2)
-            y, a = G.gsp_gat_aggregate(gg, dev(el), dev(er), dev(z), H, D, 0.2, alpha_out=True)
-            assert_within(host(y), yref, cond, what=f"{name} H={H} D={D} range={hi}")
+            y, a = G.gsp_gat_aggregate(gg, dev(el), dev(er), dev(z), H, D, 0.2, alpha_out=True, single_launch=single)
+            assert_within(host(y), yref, cond, what=f"{name} H={H} D={D} range={hi} single={single}")
             err = np.abs(host(a) - aref)
             assert np.all(err <= 1e-5 * aref + 1e-9), (name, H, D, err.max())
 
@@ -515,15 +518,16 @@ def test_gcn_layer_parity(built, act):
         assert_within(y, yr, c, rel=_lin_rel(37), what=f"{name} {act}")
 
 
+@pytest.mark.parametrize("single", [False, True], ids=["stats-launch", "single-launch"])
 @pytest.mark.parametrize("H,D", [(4, 32), (1, 41), (8, 8)])
-def test_gat_aggregate_bias_act_parity(built, H, D):
+def test_gat_aggregate_bias_act_parity(built, H, D, single):
     go, gg, _, _ = built["cl4000"]
     n = go.n
     z = uniform((n, H * D), seed=3)
     el = uniform((n, H), seed=4, low=-3, high=3)
     er = uniform((n, H), seed=5, low=-3, high=3)
     b = uniform(H * D, seed=6)
-    y = host(G.gsp_gat_aggregate_bias_act(gg, dev(el), dev(er), dev(z), H, D, dev(b), "elu"))
+    y = host(G.gsp_gat_aggregate_bias_act(gg, dev(el), dev(er), dev(z), H, D, dev(b), "elu", single_launch=single))
     s = orc.gat_scores(go.row_ptr, go.col, el, er, H)
     al = orc.edge_softmax(go.row_ptr, s, H)
     yr, c = orc.multihead_spmm(go.row_ptr, go.col, al, z, H, D)
