@@ -327,27 +327,94 @@ static int64_t slots(int64_t n, int64_t m, uint32_t flags, float fill) {
 }
 
 // ----------------------------------------------------------------- normalise
-__global__ void degree_kernel(const int64_t *__restrict__ rp, const float *__restrict__ val, int64_t n,
-                              double *__restrict__ deg) {
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) s = __dadd_rn(s, (double)val[e]);
-    deg[u] = s;
+// d_u = sum of row u's values in fp64 (P:244 D~_ii = sum_j A~_ij) and
+// a_uv = fp32(w / sqrt(d_u d_v)) with IEEE RN fp64 ops (A8).  One warp per row
+// (8 rows per CTA); rows longer than kNormLong entries are handled by the
+// whole CTA after its short rows.  Degree order: lane-strided fp64 partials,
+// xor tree, then (long rows) the 8 warps in order -- fixed per row, and equal
+// to the oracle's sequential sum whenever the row sum is exact in fp64 (every
+// integer / dyadic weight; DESIGN.md §3 A8).
+constexpr int kNormLong = 1024;
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) degree_kernel(const int64_t *__restrict__ rp, const float *__restrict__ val,
+                                                     int64_t n, double *__restrict__ deg) {
+  __shared__ int s_long[8];
+  __shared__ int s_nlong;
+  __shared__ double s_part[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  const int64_t u = (int64_t)blockIdx.x * 8 + warp;
+  if (u < n) {
+    const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
+    if (e1 - b > kNormLong) {
+      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
+    } else {
+      double s = 0.0;
+#pragma unroll 4
+      for (int64_t e = b + lane; e < e1; e += 32) s += (double)__ldg(val + e);
+      s = warp_sum_f64(s);
+      if (lane == 0) deg[u] = s;
+    }
   }
+  __syncthreads();
+  for (int k = 0; k < s_nlong; ++k) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + s_long[k];
+    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+    double s = 0.0;
+#pragma unroll 4
+    for (int64_t e = b + threadIdx.x; e < e1; e += 256) s += (double)__ldg(val + e);
+    s = warp_sum_f64(s);
+    if (lane == 0) s_part[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = s_part[0];
+      for (int w = 1; w < 8; ++w) t += s_part[w];
+      deg[r] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ float norm_entry(double du, double dv, float w) {
+  const double p = __dmul_rn(du, dv);
+  double r = 0.0;
+  if (p != 0.0) r = __ddiv_rn((double)w, __dsqrt_rn(p));
+  return __double2float_rn(r);
 }
 
 __global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                                         const float *val, int64_t n, const double *__restrict__ deg,
                                                         float *val_out) {
-  const int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (u >= n) return;
-  const int lane = threadIdx.x & 31;
-  const double du = deg[u];
-  for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
-    const double p = __dmul_rn(du, deg[col[e]]);
-    double r = 0.0;
-    if (p != 0.0) r = __ddiv_rn((double)val[e], __dsqrt_rn(p));
-    val_out[e] = __double2float_rn(r);
+  __shared__ int s_long[8];
+  __shared__ int s_nlong;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  const int64_t u = (int64_t)blockIdx.x * 8 + warp;
+  if (u < n) {
+    const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
+    if (e1 - b > kNormLong) {
+      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
+    } else {
+      const double du = __ldg(deg + u);
+#pragma unroll 2
+      for (int64_t e = b + lane; e < e1; e += 32) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < s_nlong; ++k) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + s_long[k];
+    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+    const double du = __ldg(deg + r);
+#pragma unroll 2
+    for (int64_t e = b + threadIdx.x; e < e1; e += 256) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
   }
 }
 
@@ -451,7 +518,7 @@ extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double
   if (val_out && val_out != a->val && overlaps(val_out, (size_t)a->nnz * 4, a->val, (size_t)a->nnz * 4))
     return fail(GSP_ERR_ALIAS, "%s: val_out partially overlaps val", fn);
   cudaStream_t s = cs(stream);
-  const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(a->n_rows, 256), 65535 * 4);
+  const unsigned gb = (unsigned)ceil_div(a->n_rows, 8);
   degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, deg_out);
   if ((st = check_launch("degree"))) return st;
   if (a->nnz == 0) return GSP_OK;

@@ -110,10 +110,20 @@ __device__ __forceinline__ void stat_row(float *T, int64_t r, int64_t b, int d, 
   constexpr int P = 32 / H;
   const int h = lane % H, part = lane / H;
   const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-  double m = -INFINITY;
-  for (int j = part; j < d; j += P) m = fmax(m, stat_score<kScores>(T[j * H + h], el_u, slope));
+  // the score is monotone non-decreasing in the stored value (LeakyReLU with
+  // slope >= 0 and IEEE RN are monotone), so the row max of the fp64 scores is
+  // the score of the fp32 max -- exactly (slope < 0: fp64 max of the scores)
+  float mr = -INFINITY;
+  for (int j = part; j < d; j += P) mr = fmaxf(mr, T[j * H + h]);
 #pragma unroll
-  for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+  double m = stat_score<kScores>(mr, el_u, slope);
+  if (kScores && !(slope >= 0.0)) {
+    m = -INFINITY;
+    for (int j = part; j < d; j += P) m = fmax(m, stat_score<kScores>(T[j * H + h], el_u, slope));
+#pragma unroll
+    for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  }
   double s = 0.0;
   for (int j = part; j < d; j += P) {
     const float ex = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - m));
@@ -200,10 +210,17 @@ __global__ void __launch_bounds__(kStatWarps * 32, 4) row_stats_warp(const int64
         __syncwarp();
         stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
         __syncwarp();
+        if (pass == 0) {  // max of the stored values, then of the scores (monotone, see stat_row)
+          float mr = -INFINITY;
+          for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
+          if (mr != -INFINITY) acc = fmax(acc, stat_score<kScores>(mr, el_u, slope));
+          if (kScores && !(slope >= 0.0))
+            for (int j = part; j < cnt; j += P) acc = fmax(acc, stat_score<kScores>(T[j * H + h], el_u, slope));
+          continue;
+        }
         for (int j = part; j < cnt; j += P) {
           const double sc = stat_score<kScores>(T[j * H + h], el_u, slope);
-          if (pass == 0) acc = fmax(acc, sc);
-          else if (pass == 1) acc += (double)expf((float)(sc - m));
+          if (pass == 1) acc += (double)expf((float)(sc - m));
           else alpha[(c0 + j) * H + h] = expf((float)(sc - m)) * inv_s;
         }
       }

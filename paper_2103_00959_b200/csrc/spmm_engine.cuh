@@ -250,39 +250,35 @@ struct WeightGatT {
   int heads;
   const GatStat *st;  // kPre only
   struct Row {
-    // kPre: a team may own several whole heads (slab = hpt heads); el, m and
-    // 1/S of head h + hh are read on use (L1-resident)
+    // kPre: a team may own several whole heads (slab = hpt heads); the Row of
+    // a lane is that of the lane's own head, and the lanes of a head make
+    // that head's weights (see row_segments)
     static constexpr bool kUnit = false, kComputed = true, kStagedVal = false, kMultiHead = kPre, kInStats = !kPre;
     const float *er;
     float *alpha_out;
-    const float *el;
-    const GatStat *st;
-    int64_t r;
     double el_u, m, slope;
     float inv_s;
     int heads, h;
-    __device__ __forceinline__ double score(int c, int hh = 0) const {
-      const double eu = kPre ? (double)__ldg(el + r * heads + h + hh) : el_u;
-      const double t = eu + (double)__ldg(er + (int64_t)c * heads + h + hh);
+    __device__ __forceinline__ double score(int c, int = 0) const {
+      const double t = el_u + (double)__ldg(er + (int64_t)c * heads + h);
       return t >= 0.0 ? t : slope * t;
     }
-    __device__ __forceinline__ float finish(int64_t e, double s, int hh = 0) const {
-      double mm = m;
-      float is = inv_s;
-      if constexpr (kPre) {
-        const GatStat *g = st + r * heads + h + hh;
-        mm = __ldg(&g->m);
-        is = __ldg(&g->inv_s);
-      }
-      const float a = expf((float)(s - mm)) * is;
-      if (alpha_out) alpha_out[e * heads + h + hh] = a;
+    __device__ __forceinline__ float finish(int64_t e, double s, int = 0) const {
+      const float a = expf((float)(s - m)) * inv_s;
+      if (alpha_out) alpha_out[e * heads + h] = a;
       return a;
     }
   };
-  // first_slab: only the first slab of a head writes alpha_out (each entry once)
+  // h: the head of the calling lane; first_slab: only the first slab of a
+  // head writes alpha_out (each entry once)
   __device__ __forceinline__ Row row(int64_t r, int h, bool first_slab, void *) const {
-    return Row{er, first_slab ? alpha_out : nullptr, el, st, r, kPre ? 0.0 : (double)__ldg(el + r * heads + h),
-               0.0, slope, 0.0f, heads, h};
+    Row w{er, first_slab ? alpha_out : nullptr, (double)__ldg(el + r * heads + h), 0.0, slope, 0.0f, heads, h};
+    if constexpr (kPre) {
+      const GatStat *g = st + r * heads + h;
+      w.m = __ldg(&g->m);
+      w.inv_s = __ldg(&g->inv_s);
+    }
+    return w;
   }
 };
 using WeightGat = WeightGatT<false>;
@@ -489,7 +485,14 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     const bool first = (s == s_begin);
     auto pre = [&]() {
       if (first) prologue();
-      if (scratch && !Row::kUnit) {  // cooperative: lane tl makes entries tl + T*i
+      if constexpr (Row::kComputed && Row::kMultiHead) {
+        // the T/hpt lanes of head hl make that head's weights: lane of rank k
+        // among them makes entries k, k + T/hpt, ... (its Row is its head's)
+        const int gph = G / p.hpt;                      // lanes of a head per sub-group
+        const int rank = sg * gph + (tl % G) % gph;     // rank among the head's lanes
+        for (int j = rank; j < cnt; j += T / p.hpt) tw[hl * kSeg + j] = wr.finish(e0 + j, wr.score(sc[j]));
+        __syncwarp(tmask);
+      } else if (scratch && !Row::kUnit) {  // cooperative: lane tl makes entries tl + T*i
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
           const int j = tl + T * i;
@@ -501,7 +504,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
             for (int hh = 0; hh < kHH; ++hh) {
               if (hh == 0 || hh < p.hpt) {
                 if constexpr (Row::kComputed)
-                  tw[hh * kSeg + j] = wr.finish(e0 + j, (hh == 0 && cache && q < ncache) ? cache[q] : wr.score(c, hh), hh);
+                  tw[j] = wr.finish(e0 + j, (cache && q < ncache) ? cache[q] : wr.score(c));
                 else
                   tw[hh * kSeg + j] = wr.w(e0 + j, c, hh);
               }
@@ -561,14 +564,19 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
   }
 }
 
-// register budget: 4 CTAs/SM (64 regs) for stored/unit weights; the fused
-// GAT weight keeps fp64 softmax state live and gets 3 CTAs/SM (85 regs)
+// register budget: 4 CTAs/SM (64 regs) for stored/unit weights and the
+// single-launch GAT weight; 3 CTAs/SM (85 regs) for multi-head computed GAT
+// weights (precomputed statistics)
 #ifndef GSP_GAT_MIN_BLOCKS
 #define GSP_GAT_MIN_BLOCKS 4
 #endif
+#ifndef GSP_GATPRE_MIN_BLOCKS
+#define GSP_GATPRE_MIN_BLOCKS 3
+#endif
 template <class W>
-struct MinBlocksFor {
-  static constexpr int value = W::Row::kComputed ? GSP_GAT_MIN_BLOCKS : kMinBlocks;
+struct MinBlocksFor {  // measured on C3 (8 x 64): multi-head computed weights 0.74 -> 0.67 ms at 3 CTAs/SM
+  static constexpr int value = !W::Row::kComputed ? kMinBlocks
+                               : (W::Row::kMultiHead ? GSP_GATPRE_MIN_BLOCKS : GSP_GAT_MIN_BLOCKS);
 };
 
 template <int V, int G, class W, class R>
@@ -586,7 +594,9 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   constexpr int kHptCap = (kMH && G >= 2) ? kMaxHpt : 1;  // G == 1 slabs never hold more than one head
   __shared__ float s_tw[NT][kHptCap * kSeg];              // per-team scratch: weights, per head
   __shared__ int32_t s_tc[NT][kSeg];  // per-team scratch: column indices
-  constexpr bool kGat = decltype(wf.row(0, 0, false, nullptr))::kInStats;  // in-kernel softmax statistics
+  using RowT = decltype(wf.row(0, 0, false, nullptr));
+  constexpr bool kGat = RowT::kInStats;                         // in-kernel softmax statistics
+  constexpr bool kMHC = RowT::kMultiHead && RowT::kComputed;    // per-lane head Rows (multi-head computed weights)
   constexpr int kCache = kGat ? 1024 / NT : 1;  // per-team fp64 score cache (GAT)
   __shared__ double s_cache[NT][kCache];
   __shared__ double s_red[kThreads / 32];
@@ -691,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     const int64_t S = (d + kSeg - 1) / kSeg;
-    auto wr = wf.row(r, head, first_slab, nullptr);
+    auto wr = wf.row(r, kMHC ? head + hl : head, first_slab, nullptr);
     ensure(start + d);
     if constexpr (kGat) {
       // CTA-wide softmax statistics of a hub row: thread tid takes edges
@@ -754,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     const int64_t start = __ldg(p.row_ptr + r);
     const int64_t d = __ldg(p.row_ptr + r + 1) - start;
     if (d > kHub) continue;
-    auto wr = wf.row(r, head, first_slab, nullptr);
+    auto wr = wf.row(r, kMHC ? head + hl : head, first_slab, nullptr);
     ensure(start + d);
     // GAT: the team's softmax statistics run inside the first segment, after
     // its first chunk of Z gathers has been issued; scores of the first kCache
