@@ -392,6 +392,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
   constexpr int U = TM::U < UnrollFor<V>::U ? TM::U : UnrollFor<V>::U;
+  (void)nact;
   auto load = [&](int t0, float (&xv)[U][V]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -399,8 +400,10 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       const bool ok = kFull || j < cnt;
       const uint32_t cj = ok ? (uint32_t)sc[j] : 0u;
       // the last vector of a row-slab may cover ld padding (x is [n_cols][ldx],
-      // gsp.h): those columns are read whole and their sums never stored
-      if (ok && nact > 0) {
+      // gsp.h): those columns are read whole and their sums never stored.
+      // Lanes past f (nact == 0) read the last valid vector (xb is clamped
+      // there): same sectors as an active lane, no predicate, never stored.
+      if (ok) {
         vld<V>(xv[u], xb + cj * ldxv);
       } else {
 #pragma unroll
@@ -662,7 +665,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   const bool active = col0 < p.f;
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
   const int nact = active ? nvalid : 0;  // columns this lane gathers
-  const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + col0);
+  const int64_t last_vec = p.f > 0 ? ((p.f - 1) / V) * V : 0;  // first column of the last valid vector
+  const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + (active ? col0 : last_vec));
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
   const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
