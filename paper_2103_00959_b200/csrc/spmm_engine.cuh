@@ -392,6 +392,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
   constexpr int U = TM::U < UnrollFor<V>::U ? TM::U : UnrollFor<V>::U;
+  static_assert(EPS % U == 0, "GSP_UNROLL must divide the edges per sub-group and segment (power of two)");
   (void)nact;
   auto load = [&](int t0, float (&xv)[U][V]) {
 #pragma unroll
