@@ -316,21 +316,29 @@ gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const 
 /* ---------------------------------------------------------------------------
  * NEXT-1: layers for 2-layer GCN / GAT inference (P:239-246 Eq. gcn_layer
  * H^(l+1) = sigma(A^ H^(l) W^(l)); P:661-663 Table spmm_time).
- * gsp_linear: row-major y[n][f_out] = x[n][f_in] w[f_in][f_out] (ldw >= f_out),
- *   a plain dense GEMM delegated to cuBLAS with fp32 compute (no TF32); one
- *   cuBLAS handle per (thread, device) is created on first use.
+ * gsp_linear: row-major y[n][f_out] = x[n][f_in] w[f_in][f_out] (ldw >= f_out).
+ *   With ws >= gsp_linear_workspace(f_in, f_out) bytes (device, any
+ *   alignment), f_out <= 256, ldx % 4 == 0 and x 16-byte aligned: tcgen05
+ *   tensor cores, kind::tf32 with 3xTF32 splitting (x = hi + lo, w = hi + lo,
+ *   x w ~= lo.hi + hi.lo + hi.hi, fp32 accumulation in TMEM; per-product
+ *   error <= 2^-20 |x||w|), operands staged by TMA (SWIZZLE_128B), one CTA per
+ *   128 rows.  Otherwise (ws NULL / too small, wider or unaligned operands) a
+ *   cuBLAS SGEMM with fp32 compute (no TF32); one cuBLAS handle per (thread,
+ *   device) is created on first use.
  * gsp_spmm_bias_act: y = act(A x + bias) with bias [f] (nullable) and the
  *   activation fused into the SpMM epilogue.
  * gsp_gcn_layer: y = act(A (x w) + bias): gsp_linear into ws, then
- *   gsp_spmm_bias_act.  ws >= gsp_gcn_layer_workspace(a->n_cols, f_out).
+ *   gsp_spmm_bias_act.  ws >= gsp_gcn_layer_workspace(a->n_cols, f_in, f_out)
+ *   (holds x w and the tensor-core GEMM's split-W workspace).
  * gsp_gat_aggregate_bias_act: gsp_gat_aggregate with y = act(Y + bias[H*D])
  *   fused (ELU for hidden GAT layers); ws as for gsp_gat_aggregate. */
 typedef enum { GSP_ACT_NONE = 0, GSP_ACT_RELU = 1, GSP_ACT_ELU = 2 } gsp_act;
+gsp_status gsp_linear_workspace(int64_t f_in, int64_t f_out, size_t *ws_bytes);
 gsp_status gsp_linear(int64_t n, int64_t f_in, const float *x, int64_t ldx, const float *w, int64_t ldw,
-                      int64_t f_out, float *y, int64_t ldy, gsp_stream stream);
+                      int64_t f_out, float *y, int64_t ldy, void *ws, size_t ws_bytes, gsp_stream stream);
 gsp_status gsp_spmm_bias_act(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, const float *bias,
                              gsp_act act, float *y, int64_t ldy, gsp_stream stream);
-gsp_status gsp_gcn_layer_workspace(int64_t n, int64_t f_out, size_t *ws_bytes);
+gsp_status gsp_gcn_layer_workspace(int64_t n, int64_t f_in, int64_t f_out, size_t *ws_bytes);
 gsp_status gsp_gcn_layer(const gsp_csr *a, const float *x, int64_t f_in, int64_t ldx, const float *w,
                          int64_t f_out, const float *bias, gsp_act act, float *y, int64_t ldy, void *ws,
                          size_t ws_bytes, gsp_stream stream);

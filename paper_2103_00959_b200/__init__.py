@@ -35,7 +35,8 @@ EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "g
            "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
            "gsp_propagate_workspace", "gsp_propagate", "gsp_csr_transpose_workspace", "gsp_csr_transpose",
            "gsp_sddmm", "gsp_edge_softmax_backward", "gsp_gat_backward_workspace", "gsp_gat_aggregate_backward",
-           "gsp_attn_project_backward_workspace", "gsp_attn_project_backward", "gsp_linear", "gsp_spmm_bias_act",
+           "gsp_attn_project_backward_workspace", "gsp_attn_project_backward", "gsp_linear_workspace", "gsp_linear",
+           "gsp_spmm_bias_act",
            "gsp_gcn_layer_workspace", "gsp_gcn_layer", "gsp_gat_aggregate_bias_act")
 
 
@@ -88,9 +89,10 @@ def lib() -> ctypes.CDLL:
             "gsp_gat_aggregate_backward": [CP, CP, P, I32, P, P, D, P, I, I, P, I, P, I, P, P, P, ctypes.c_size_t, P],
             "gsp_attn_project_backward_workspace": [I, I32, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_attn_project_backward": [I, I32, I, P, I, P, P, P, P, P, I, P, P, P, ctypes.c_size_t, P],
-            "gsp_linear": [I, I, P, I, P, I, I, P, I, P],
+            "gsp_linear_workspace": [I, I, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_linear": [I, I, P, I, P, I, I, P, I, P, ctypes.c_size_t, P],
             "gsp_spmm_bias_act": [CP, P, I, I, P, ctypes.c_int, P, I, P],
-            "gsp_gcn_layer_workspace": [I, I, ctypes.POINTER(ctypes.c_size_t)],
+            "gsp_gcn_layer_workspace": [I, I, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_gcn_layer": [CP, P, I, I, P, I, P, ctypes.c_int, P, I, P, ctypes.c_size_t, P],
             "gsp_gat_aggregate_bias_act": [CP, I32, P, P, D, P, I, I, P, ctypes.c_int, P, I, P, ctypes.c_size_t, P],
             "gsp_spmm_plan_info": [CP, P, I, I, ctypes.POINTER(gsp_spmm_opts), ctypes.POINTER(ctypes.c_int32),
@@ -516,15 +518,25 @@ def gsp_attn_project_backward(z: torch.Tensor, a_l: torch.Tensor, a_r: torch.Ten
 ACT = {"none": 0, "relu": 1, "elu": 2}
 
 
-def gsp_linear(x: torch.Tensor, w: torch.Tensor, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    """y = x w (row-major, fp32 cuBLAS GEMM)."""
+def gsp_linear(x: torch.Tensor, w: torch.Tensor, y: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+               tensor_cores: bool = True, stream=None) -> torch.Tensor:
+    """y = x w (row-major): tcgen05 3xTF32 GEMM when a workspace is passed
+    (allocated here unless tensor_cores=False), else fp32 cuBLAS."""
     x, ldx = _mat(x, "x")
     w, ldw = _mat(w, "w")
     n, f_in = x.shape
     f_out = w.shape[1]
     y = torch.empty((n, f_out), dtype=torch.float32, device=x.device) if y is None else y
     y, ldy = _mat(y, "y")
-    _check(lib().gsp_linear(n, f_in, _ptr(x), ldx, _ptr(w), ldw, f_out, _ptr(y), ldy, _stream(stream)), "gsp_linear")
+    if tensor_cores:
+        nb = ctypes.c_size_t(0)
+        _check(lib().gsp_linear_workspace(f_in, f_out, ctypes.byref(nb)), "gsp_linear_workspace")
+        if ws is None or ws.numel() < nb.value:
+            ws = torch.empty(nb.value, dtype=torch.uint8, device=x.device)
+    else:
+        ws = None
+    _check(lib().gsp_linear(n, f_in, _ptr(x), ldx, _ptr(w), ldw, f_out, _ptr(y), ldy, _ptr(ws),
+                            0 if ws is None else ws.numel(), _stream(stream)), "gsp_linear")
     return y
 
 
@@ -548,7 +560,7 @@ def gsp_gcn_layer(a: CSR, x: torch.Tensor, w: torch.Tensor, bias: Optional[torch
     y = torch.empty((a.n_rows, f_out), dtype=torch.float32, device=x.device) if y is None else y
     y, ldy = _mat(y, "y")
     nb = ctypes.c_size_t(0)
-    _check(lib().gsp_gcn_layer_workspace(a.n_cols, f_out, ctypes.byref(nb)), "gsp_gcn_layer_workspace")
+    _check(lib().gsp_gcn_layer_workspace(a.n_cols, f_in, f_out, ctypes.byref(nb)), "gsp_gcn_layer_workspace")
     if ws is None or ws.numel() < nb.value:
         ws = torch.empty(nb.value, dtype=torch.uint8, device=x.device)
     v = a.view()

@@ -491,19 +491,47 @@ def test_attn_project_backward_parity():
 # ---------------------------------------------------------------- NEXT-1: inference layers
 
 def _lin_rel(f_in):
-    """Bound for y = act(A (x W) + b) with an fp32 GEMM of f_in terms (any
-    summation order: gamma_{f_in} <= f_in * 2^-24) followed by the SpMM bound
-    1e-5 (north_star); ReLU / ELU are 1-Lipschitz."""
-    return 1e-5 + f_in * 2.0 ** -24
+    """Bound for y = act(A (x W) + b): the GEMM bound (3xTF32 tensor cores,
+    _tc_rel; it also covers an fp32 SGEMM's gamma_{f_in} <= f_in * 2^-24)
+    followed by the SpMM bound 1e-5 (north_star); ReLU / ELU are 1-Lipschitz
+    (DESIGN.md §7)."""
+    return 1e-5 + _tc_rel(f_in)
 
 
-@pytest.mark.parametrize("f_in,f_out", [(3, 5), (33, 7), (128, 41), (602, 128)])
-def test_linear_parity(f_in, f_out):
-    x = uniform((5000, f_in), seed=1)
+def _tc_rel(f_in):
+    """3xTF32 tensor-core GEMM bound (DESIGN.md §NEXT rows): per product
+    <= 1.25 * 2^-20 |x||w| (TF32 lo parts + the dropped lo*lo term) <= 2^-19,
+    plus f_in fp32 accumulations at <= 2u each (tensor-core accumulation is
+    not assumed to round to nearest)."""
+    return 2.0 ** -19 + f_in * 2.0 ** -23
+
+
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cublas"])
+@pytest.mark.parametrize("n,f_in,f_out", [(5000, 3, 5), (5000, 33, 7), (5000, 128, 41), (5000, 602, 128),
+                                          (1, 1, 1), (128, 32, 16), (129, 31, 17), (3000, 1433, 256),
+                                          (2000, 300, 128), (777, 500, 41), (1000, 64, 512), (500, 100, 300)])
+def test_linear_parity(n, f_in, f_out, tc):
+    x = uniform((n, f_in), seed=1)
     w = uniform((f_in, f_out), seed=2)
-    y = host(G.gsp_linear(dev(x), dev(w)))
+    y = host(G.gsp_linear(dev(x), dev(w), tensor_cores=tc))
     yr, c = orc.linear(x, w)
-    assert_within(y, yr, c, rel=f_in * 2.0 ** -24 + 1e-7, what=f"linear {f_in}x{f_out}")
+    rel = _tc_rel(f_in) if tc else f_in * 2.0 ** -24 + 1e-7
+    assert_within(y, yr, c, rel=rel, what=f"linear {n}x{f_in}x{f_out} tc={tc}")
+
+
+def test_linear_tc_padded_views():
+    """Tensor-core GEMM on a padded X view (ld > f_in) into a padded Y view,
+    and a graph-sized ragged tail (n % 128 != 0)."""
+    n, f_in, f_out = 1001, 602, 128
+    xb = torch.zeros((n, 604), device=DEV)
+    x = uniform((n, f_in), seed=3)
+    xb[:, :f_in] = dev(x)
+    w = uniform((f_in, f_out), seed=4)
+    yb = torch.full((n, 132), 7.0, device=DEV)
+    G.gsp_linear(xb[:, :f_in], dev(w), y=yb[:, :f_out])
+    yr, c = orc.linear(x, w)
+    assert_within(host(yb[:, :f_out]), yr, c, rel=_tc_rel(f_in), what="padded")
+    assert torch.all(yb[:, f_out:] == 7.0)  # padding columns untouched
 
 
 @pytest.mark.parametrize("act", ["none", "relu", "elu"])
