@@ -27,8 +27,17 @@ namespace gsp {
 // kScores: s from el/er (GAT) or s = logits (edge softmax).
 // kApply : write alpha = exp(s - m) / sum (standalone edge softmax; logits
 //          may alias alpha) instead of storing the statistics.
-constexpr int kStatWarps = 8;
-constexpr int kStatRPW = 4;            // rows per warp
+#ifndef GSP_STAT_WARPS
+#define GSP_STAT_WARPS 8
+#endif
+#ifndef GSP_STAT_RPW
+#define GSP_STAT_RPW 4
+#endif
+#ifndef GSP_STAT_MINB
+#define GSP_STAT_MINB 4
+#endif
+constexpr int kStatWarps = GSP_STAT_WARPS;  // warps per CTA
+constexpr int kStatRPW = GSP_STAT_RPW;      // rows per warp
 constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
 
 template <bool kScores>
@@ -145,7 +154,7 @@ __device__ __forceinline__ void stat_row(float *T, int64_t r, int64_t b, int d, 
 }
 
 template <int H, bool kScores, bool kApply>
-__global__ void __launch_bounds__(kStatWarps * 32, 4) row_stats_warp(const int64_t *__restrict__ rp,
+__global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp(const int64_t *__restrict__ rp,
                                                                   const int32_t *__restrict__ col,
                                                                   const float *__restrict__ el,
                                                                   const float *__restrict__ er, const float *logits,
