@@ -392,6 +392,60 @@ __global__ void __launch_bounds__(256) attn_project_warp(int64_t n, int H, int64
   }
 }
 
+// Streaming form for the common layout (float4 vectors, a head = VH vectors
+// with VH | 32, H*D <= 32*4*NV): each warp owns kAPR consecutive rows, issues
+// every Z load of its rows before the first use (NV float4 per lane per row),
+// keeps a_l / a_r in registers, then reduces each head with a segmented xor
+// tree.  Same per-(row, head) order as attn_project_warp (lane-sequential fma
+// over V, then the xor tree).
+constexpr int kAPR = 2;  // rows per warp
+template <int NV>
+__global__ void __launch_bounds__(256) attn_project_stream(int64_t n, int H, int VH, const float *__restrict__ z,
+                                                           int64_t ldz, const float *__restrict__ al,
+                                                           const float *__restrict__ ar, float *__restrict__ el,
+                                                           float *__restrict__ er) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kAPR;
+  if (u0 >= n) return;
+  const int nvec = H * VH;
+  float4 a[NV], b[NV], zv[kAPR][NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int k = lane + 32 * i;
+    a[i] = k < nvec ? __ldg(reinterpret_cast<const float4 *>(al) + k) : make_float4(0, 0, 0, 0);
+    b[i] = k < nvec ? __ldg(reinterpret_cast<const float4 *>(ar) + k) : make_float4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int r = 0; r < kAPR; ++r) {
+    const int64_t u = u0 + r;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      zv[r][i] = (u < n && k < nvec) ? __ldg(reinterpret_cast<const float4 *>(z + u * ldz) + k) : make_float4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kAPR; ++r) {
+    const int64_t u = u0 + r;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float4 q = zv[r][i];
+      float sl = fmaf(a[i].w, q.w, fmaf(a[i].z, q.z, fmaf(a[i].y, q.y, a[i].x * q.x)));
+      float sr = fmaf(b[i].w, q.w, fmaf(b[i].z, q.z, fmaf(b[i].y, q.y, b[i].x * q.x)));
+      for (int off = 1; off < VH; off <<= 1) {
+        sl += __shfl_xor_sync(0xffffffffu, sl, off);
+        sr += __shfl_xor_sync(0xffffffffu, sr, off);
+      }
+      const int k = lane + 32 * i;
+      if (u < n && k < nvec && (lane % VH) == 0) {
+        const int64_t h = k / VH;
+        el[u * H + h] = sl;
+        er[u * H + h] = sr;
+      }
+    }
+  }
+}
+
 }  // namespace gsp
 
 using namespace gsp;
@@ -422,7 +476,14 @@ extern "C" gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, cons
   if (n >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "%s: n must be < 2^31", fn);
   const unsigned blocks = (unsigned)ceil_div(n, 8);
   cudaStream_t s = cs(stream);
-  if (d % 4 == 0 && ldz % 4 == 0 && aligned16(z) && aligned16(a_l) && aligned16(a_r))
+  const int64_t VH = d / 4, nvec = (int64_t)heads * VH;
+  const bool vec = d % 4 == 0 && ldz % 4 == 0 && aligned16(z) && aligned16(a_l) && aligned16(a_r);
+  if (vec && VH >= 1 && VH <= 32 && 32 % VH == 0 && nvec <= 32 * 4) {
+    const unsigned sb = (unsigned)ceil_div(n, 8 * kAPR);
+    if (nvec <= 32) attn_project_stream<1><<<sb, 256, 0, s>>>(n, heads, (int)VH, z, ldz, a_l, a_r, el, er);
+    else if (nvec <= 64) attn_project_stream<2><<<sb, 256, 0, s>>>(n, heads, (int)VH, z, ldz, a_l, a_r, el, er);
+    else attn_project_stream<4><<<sb, 256, 0, s>>>(n, heads, (int)VH, z, ldz, a_l, a_r, el, er);
+  } else if (vec)
     attn_project_warp<4><<<blocks, 256, 0, s>>>(n, heads, d, z, ldz, a_l, a_r, el, er);
   else
     attn_project_warp<1><<<blocks, 256, 0, s>>>(n, heads, d, z, ldz, a_l, a_r, el, er);
