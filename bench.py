@@ -376,6 +376,10 @@ def main():
 
     for v in out["rows"].values():
         v["frac_of_hbm_peak"] = v["alg_GB/s"] / peak
+    tr = out["roofline"].get("traffic")
+    if tr:  # what actually crossed HBM (ncu DRAM bytes of this kernel) at this run's launch time
+        out["roofline"]["dram_GB/s"] = tr / (t_ms * 1e-3) / 1e9
+        out["roofline"]["dram_frac"] = out["roofline"]["dram_GB/s"] / peak
     if not use_dist and args.sweep:
         sw = {}
         for sc in [int(v) for v in args.sweep.split(",")]:
