@@ -248,7 +248,7 @@ def test_edge_softmax_parity(built, H):
     assert np.all(np.abs(host(t) - aref) <= 1e-5 * aref + 1e-9)
 
 
-@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 128)])
+@pytest.mark.parametrize("H,D", [(1, 64), (2, 3), (4, 8), (8, 8), (8, 64), (3, 16), (2, 128), (4, 32), (16, 64), (1, 256), (5, 4)])
 def test_attn_project_parity(H, D):
     n = 5000
     z = uniform((n, H * D), seed=3)
