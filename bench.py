@@ -464,6 +464,19 @@ def main():
             red[r_] = {"ms": float(np.mean(ts)), "GE/s": ge / (np.mean(ts) * 1e-3)}
         out.setdefault("secondary", {})["C4_gspmm_reduce"] = red
 
+    # --- secondary: fp16 feature storage, fp32 arithmetic (P:1302-1320 mixed precision) on C4 ---
+    if not use_dist and not args.no_gat:
+        ld16 = (f + 3) // 4 * 4
+        xh16 = torch.zeros((n, ld16), dtype=torch.float16, device=dev)
+        xh16[:, :f] = x[:, :f].half()
+        t16 = timed(lambda: G.gsp_spmm_f16(gn, xh16, f=f, y=y), flush, args.warmup, 10)
+        b16 = 2 * nnz * f + 4 * n * f + 8 * nnz + 8 * (n + 1)
+        out.setdefault("secondary", {})["C4_spmm_f16_storage"] = {
+            "ms": t16, "GE/s": ge / (t16 * 1e-3), "alg_GB/s": b16 / (t16 * 1e-3) / 1e9,
+            "model": "2*nnz*F (fp16 gathers) + 4*n*F + 8*nnz + 8*(n+1)",
+            "note": "x stored in fp16, converted exactly, fp32 products and sums (gsp_spmm_f16); not the headline"}
+        del xh16
+
     # --- secondary: K-step propagation (APPNP, K=10, alpha=0.1) of 41-wide logits on C4 (NEXT-4) ---
     if not use_dist and not args.no_gat:
         fk, K = 41, 10

@@ -150,6 +150,16 @@ gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, 
 gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
                     int64_t ldy, gsp_stream stream);
 
+/* gsp_spmm_f16: gsp_spmm with fp16 feature storage (mixed
+ * precision "fp16=True"): x device IEEE binary16 [a->n_cols][ldx] (padding as
+ * for gsp_spmm), y device fp32 [a->n_rows][ldy].  Every x value is converted
+ * exactly to fp32; products and sums are fp32 in the same order as gsp_spmm,
+ * so the error bound is gsp_spmm's with x replaced by its fp16 values.  8-byte
+ * gathers of 4 halves when ldx % 4 == 0 and x is 8-byte aligned (scalar
+ * otherwise). */
+gsp_status gsp_spmm_f16(const gsp_csr *a, const void *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                        gsp_stream stream);
+
 /* ---------------------------------------------------------------------------
  * GSpMM with a selectable reduce operator phi (NEXT-2).
  * P:640-646 (§4.1 Eq. formula:1, "users could choose the reduce or compute

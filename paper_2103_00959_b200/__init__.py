@@ -29,7 +29,7 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
           8: "GSP_ERR_CUDA"}
 
 # every symbol include/gsp.h declares
-EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_ex",
+EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_f16", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
            "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
                                ctypes.POINTER(ctypes.c_int64), P, ctypes.c_size_t, P],
             "gsp_sym_normalize": [CP, P, P, P],
             "gsp_spmm": [CP, P, I, I, P, I, P],
+            "gsp_spmm_f16": [CP, P, I, I, P, I, P],
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
             "gsp_gspmm": [CP, ctypes.c_int, P, I, I, P, I, P],
             "gsp_probe_l2_read": [P, ctypes.c_size_t, I32, P, P],
@@ -247,6 +248,20 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
 gsp_spmm_ex = gsp_spmm
 
 REDUCE = {"sum": 0, "mean": 1, "max": 2, "min": 3}
+
+
+def gsp_spmm_f16(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    """y (fp32) = A x with x stored in fp16 (gsp.h gsp_spmm_f16; fp32 arithmetic)."""
+    if x.dtype != torch.float16 or x.dim() != 2 or x.stride(1) != 1:
+        raise TypeError("x must be a 2-D float16 tensor with unit column stride")
+    f = x.shape[1] if f is None else f
+    if y is None:
+        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+    y, ldy = _mat(y, "y")
+    v = a.view()
+    _check(lib().gsp_spmm_f16(ctypes.byref(v), _ptr(x), f, x.stride(0), _ptr(y), ldy, _stream(stream)), "gsp_spmm_f16")
+    return y
 
 
 def gsp_gspmm(a: CSR, x: torch.Tensor, reduce: str = "sum", f: Optional[int] = None,

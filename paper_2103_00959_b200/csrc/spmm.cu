@@ -227,6 +227,70 @@ extern "C" gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int6
   return spmm_impl(a, x, f, ldx, y, ldy, nullptr, GSP_REDUCE_SUM, cs(stream), "gsp_spmm");
 }
 
+// fp16 feature storage (P:1302-1320 mixed precision): y (fp32) = A x with x in
+// fp16, products and sums in fp32.  Same engine, order and epilogue as
+// gsp_spmm; V = 4 halves (8-byte gathers, 128-column slabs: half of fp32's
+// L2 footprint per slab) when ldx % 4 == 0 and x is 8-byte aligned, else
+// scalar halves (V = 8, 16-byte gathers, is available via GSP_F16_VMAX=8).
+static gsp_status spmm_f16_part(const gsp_csr *a, const EngineLaunch &L, const __half *x, int64_t f, int64_t ldx,
+                                float *y, int64_t ldy, cudaStream_t s) {
+  EngineParams p;
+  p.row_ptr = a->row_ptr;
+  p.col = a->col_idx;
+  p.x = x;
+  p.y = y;
+  p.n_rows = a->n_rows;
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.f = f;
+  p.block_nnz = L.block_nnz;
+  p.nblk = L.nblk;
+  p.head_dim = 0;
+  p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
+  engine_stage(p, L, a->nnz, a->col_idx, a->val);
+  const int64_t ldxv = ldx / L.V;  // in 16-byte (V = 8) or 2-byte (V = 1) units
+  if (a->n_cols > 0 && (a->n_cols - 1) * ldxv + ldxv >= (int64_t(1) << 32))
+    return fail(GSP_ERR_UNSUPPORTED, "feature matrix too large for 32-bit vector offsets");
+  p.ldxv = (uint32_t)ldxv;
+  return a->val ? engine_launch_f16(L, p, WeightVal{a->val}, s) : engine_launch_f16(L, p, WeightOne{}, s);
+}
+
+extern "C" gsp_status gsp_spmm_f16(const gsp_csr *a, const void *x, int64_t f, int64_t ldx, float *y, int64_t ldy,
+                                   gsp_stream stream) {
+  const char *fn = "gsp_spmm_f16";
+  clear_detail();
+  gsp_status st = check_csr(a, false, fn);
+  if (st) return st;
+  if (f < 0 || ldx < f || ldy < f) return fail(GSP_ERR_INVALID_ARG, "%s: need f >= 0, ldx >= f, ldy >= f", fn);
+  if (a->n_rows == 0 || f == 0) return GSP_OK;
+  if (!y) return fail(GSP_ERR_INVALID_ARG, "%s: y is NULL", fn);
+  if (a->n_cols > 0 && !x) return fail(GSP_ERR_INVALID_ARG, "%s: x is NULL", fn);
+  const size_t xbytes = a->n_cols ? (size_t)((a->n_cols - 1) * ldx + f) * 2 : 0;
+  const size_t ybytes = (size_t)((a->n_rows - 1) * ldy + f) * 4;
+  if (overlaps(x, xbytes, y, ybytes)) return fail(GSP_ERR_ALIAS, "%s: x and y overlap", fn);
+#ifndef GSP_F16_VMAX
+#define GSP_F16_VMAX 4  // measured (tools/f16_probe.py): 4 halves per lane (128-column slabs, 60 MB of X per
+                        // slab on C4) 3.9 ms vs 8 halves (256 columns, 2 CTAs/SM) 4.7 ms; fp32 5.4 ms
+#endif
+  int vmax = 1;
+  if (GSP_F16_VMAX >= 8 && ldx % 8 == 0 && aligned16(x)) vmax = 8;
+  else if (ldx % 4 == 0 && aligned8(x)) vmax = 4;
+  EngineLaunch L, T;
+  if ((st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, 0, 0, &L, 1))) return st;
+  const __half *xh = static_cast<const __half *>(x);
+  const int64_t SW = L.slab_cols, rem = f % SW;
+  cudaStream_t s = cs(stream);
+  if (L.V >= 4 && f > SW && rem && rem <= SW / 2) {  // narrower tail launch (as gsp_spmm)
+    int64_t tw = 16;
+    while (tw < rem) tw *= 2;
+    if ((st = engine_plan(a->n_rows, a->n_cols, a->nnz, rem, 0, vmax, (int32_t)tw, 0, &T, 1))) return st;
+    L.nslab = (f - rem) / SW;
+    if ((st = spmm_f16_part(a, L, xh, f - rem, ldx, y, ldy, s))) return st;
+    return spmm_f16_part(a, T, xh + (f - rem), rem, ldx, y + (f - rem), ldy, s);
+  }
+  return spmm_f16_part(a, L, xh, f, ldx, y, ldy, s);
+}
+
 extern "C" gsp_status gsp_spmm_accumulate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t,
                                           int64_t ldt, float *acc, int64_t ldacc, float coef, const float *src,
                                           int64_t ldsrc, float src_coef, gsp_stream stream) {

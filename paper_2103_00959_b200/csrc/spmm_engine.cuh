@@ -34,6 +34,8 @@
 //              acc1, folded into acc2 every 32 segments.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace gsp {
@@ -140,6 +142,98 @@ template <int V>
 __device__ __forceinline__ void vld(float (&r)[V], const typename VecT<V>::T *p) {
   Vec<V>::ld(r, reinterpret_cast<const float *>(p));
 }
+
+// ------------------------------------------------- feature element policies
+// XE: how a lane's V features of one gathered row are stored in X.
+//  XF32<V>: fp32 (float4 / float2 / float loads, the default);
+//  XF16<V>: fp16 storage ("fp16" mixed precision): V = 8 halves
+//           per 16-byte load (or 1), converted to fp32 at FMA time -- the
+//           arithmetic stays fp32.
+// Raw: what a gather lands in (registers); unpack() runs after all gathers of
+// a chunk are issued, so conversion never stalls the loads.
+template <int V>
+struct XF32 {
+  using Elem = float;
+  using Ptr = typename VecT<V>::T;  // addressed in these units (ldxv = ldx / width)
+  static constexpr int kWidth = V == 8 ? 4 : V;
+  static constexpr int kU = V >= 8 ? (kUnroll < 4 ? kUnroll : 4) : kUnroll;  // gathers in flight per lane
+  static constexpr int kMinBlocks = 0;                                        // engine default
+  struct Raw {
+    float v[V];
+  };
+  static __device__ __forceinline__ void ld(Raw &r, const Ptr *p) { vld<V>(r.v, p); }
+  static __device__ __forceinline__ void zero(Raw &r) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) r.v[i] = 0.0f;
+  }
+  static __device__ __forceinline__ void unpack(const Raw &r, float (&x)[V]) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) x[i] = r.v[i];
+  }
+};
+template <int V>
+struct XF16;
+#ifndef GSP_F16_MIN_BLOCKS
+#define GSP_F16_MIN_BLOCKS 2
+#endif
+template <>
+struct XF16<8> {
+  using Elem = __half;
+  using Ptr = uint4;
+  static constexpr int kWidth = 8;
+  static constexpr int kU = kUnroll;
+  static constexpr int kMinBlocks = GSP_F16_MIN_BLOCKS;  // 8 fp32 accumulators x 4 residues per lane
+  struct Raw {
+    uint4 q;
+  };
+  static __device__ __forceinline__ void ld(Raw &r, const Ptr *p) { r.q = __ldg(p); }
+  static __device__ __forceinline__ void zero(Raw &r) { r.q = make_uint4(0u, 0u, 0u, 0u); }
+  static __device__ __forceinline__ void unpack(const Raw &r, float (&x)[8]) {
+    const uint32_t w[4] = {r.q.x, r.q.y, r.q.z, r.q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+  }
+};
+template <>
+struct XF16<4> {
+  using Elem = __half;
+  using Ptr = uint2;
+  static constexpr int kWidth = 4;
+  static constexpr int kU = kUnroll;
+  static constexpr int kMinBlocks = 0;
+  struct Raw {
+    uint2 q;
+  };
+  static __device__ __forceinline__ void ld(Raw &r, const Ptr *p) { r.q = __ldg(p); }
+  static __device__ __forceinline__ void zero(Raw &r) { r.q = make_uint2(0u, 0u); }
+  static __device__ __forceinline__ void unpack(const Raw &r, float (&x)[4]) {
+    const uint32_t w[2] = {r.q.x, r.q.y};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+  }
+};
+template <>
+struct XF16<1> {
+  using Elem = __half;
+  using Ptr = __half;
+  static constexpr int kWidth = 1;
+  static constexpr int kU = kUnroll;
+  static constexpr int kMinBlocks = 0;
+  struct Raw {
+    __half h;
+  };
+  static __device__ __forceinline__ void ld(Raw &r, const Ptr *p) { r.h = __ldg(p); }
+  static __device__ __forceinline__ void zero(Raw &r) { r.h = __float2half(0.0f); }
+  static __device__ __forceinline__ void unpack(const Raw &r, float (&x)[1]) { x[0] = __half2float(r.h); }
+};
 
 // Store V values of which the first nvalid are real columns.
 template <int V>
@@ -288,7 +382,7 @@ using WeightGatPre = WeightGatT<true>;
 struct EngineParams {
   const int64_t *row_ptr;
   const int32_t *col;
-  const float *x;
+  const void *x;  // fp32 (XF32) or fp16 (XF16) features
   float *y;
   int64_t n_rows, ldx, ldy, f;
   uint32_t ldxv;  // ldx / V: row stride of x in V-wide vectors (32-bit gather offsets)
@@ -365,10 +459,6 @@ struct Team {
   static constexpr int EPS = kSeg / SPR;   // edges per sub-group per segment
   static constexpr int U = EPS < kUnroll ? EPS : kUnroll;
 };
-template <int V>
-struct UnrollFor {  // gathers in flight per lane, capped by register budget
-  static constexpr int U = V >= 8 ? (kUnroll < 4 ? kUnroll : 4) : kUnroll;
-};
 
 template <int T>
 __device__ __forceinline__ double team_max(double v, unsigned tmask) {
@@ -385,16 +475,17 @@ __device__ __forceinline__ double team_sum(double v, unsigned tmask) {  // xor b
 
 // Gather + FMA over one segment whose metadata is in shared memory (sc: 32
 // column indices, sw: 32 weights, unused when Row::kUnit).  kFull: cnt == 32.
-template <int V, int G, class Row, class R, bool kFull, class Pre>
+template <int V, int G, class Row, class R, bool kFull, class XE, class Pre>
 __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, int cnt,
-                                           const typename VecT<V>::T *__restrict__ xb, uint32_t ldxv, int nact,
+                                           const typename XE::Ptr *__restrict__ xb, uint32_t ldxv, int nact,
                                            int sg, float (&a)[Team<G>::NACC][V], Pre &&pre) {
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
-  constexpr int U = TM::U < UnrollFor<V>::U ? TM::U : UnrollFor<V>::U;
+  constexpr int U = TM::U < XE::kU ? TM::U : XE::kU;
+  using Raw = typename XE::Raw;
   static_assert(EPS % U == 0, "GSP_UNROLL must divide the edges per sub-group and segment (power of two)");
   (void)nact;
-  auto load = [&](int t0, float (&xv)[U][V]) {
+  auto load = [&](int t0, Raw (&xv)[U]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = sg + SPR * (t0 + u);
@@ -405,22 +496,23 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
       // Lanes past f (nact == 0) read the last valid vector (xb is clamped
       // there): same sectors as an active lane, no predicate, never stored.
       if (ok) {
-        vld<V>(xv[u], xb + cj * ldxv);
+        XE::ld(xv[u], xb + cj * ldxv);
       } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) xv[u][i] = 0.0f;
+        XE::zero(xv[u]);
       }
     }
   };
-  auto fma = [&](int t0, const float (&xv)[U][V]) {
+  auto fma = [&](int t0, const Raw (&xv)[U]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int t = t0 + u;
       const int j = sg + SPR * t;
       if (kFull || j < cnt) {
         const float ww = Row::kUnit ? 1.0f : sw[j];
+        float xf[V];
+        XE::unpack(xv[u], xf);
 #pragma unroll
-        for (int i = 0; i < V; ++i) a[t % NACC][i] = R::step(a[t % NACC][i], ww, xv[u][i]);
+        for (int i = 0; i < V; ++i) a[t % NACC][i] = R::step(a[t % NACC][i], ww, xf[i]);
       }
     }
   };
@@ -428,7 +520,7 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 #pragma unroll
     for (int t0 = 0; t0 < EPS; t0 += U) {
       if (!kFull && SPR * t0 >= cnt) break;
-      float xv[U][V];
+      Raw xv[U];
       load(t0, xv);
       // the first chunk's gathers are in flight: now make the weights (team-
       // uniform hook; fills sw when the weights need arithmetic or loads)
@@ -450,10 +542,10 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
 // Metadata: segments inside the TMA-staged window are read from it directly;
 // other segments (hub rows beyond the window, unstaged arrays) and computed
 // weights go through the team's 32-entry shared scratch (tc, tw).
-template <int V, int G, bool kLong, class R, class Row, class Pro>
+template <int V, int G, bool kLong, class R, class XE, class Row, class Pro>
 __device__ __forceinline__ void row_segments(const EngineParams &p, const Window &win, Row &wr, int64_t start,
                                              int64_t d, int64_t s_begin, int64_t s_end,
-                                             const typename VecT<V>::T *__restrict__ xb, int nact, int tl, int sg,
+                                             const typename XE::Ptr *__restrict__ xb, int nact, int tl, int sg,
                                              unsigned tmask, int32_t *tc, float *tw, int hl, const double *cache,
                                              int ncache, float (&out)[V], Pro &&prologue) {
   using TM = Team<G>;
@@ -523,8 +615,8 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int i = 0; i < V; ++i) a[q][i] = R::init();
-    if (cnt == kSeg) seg_gather<V, G, Row, R, true>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
-    else seg_gather<V, G, Row, R, false>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
+    if (cnt == kSeg) seg_gather<V, G, Row, R, true, XE>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
+    else seg_gather<V, G, Row, R, false, XE>(sc, sw, cnt, xb, p.ldxv, nact, sg, a, pre);
     if (scratch) __syncwarp(tmask);  // scratch is rewritten by the next segment
     // segment sum (r0 + r1) + (r2 + r3); residue k lives in sub-group k % SPR,
     // accumulator k / SPR
@@ -577,14 +669,15 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
 #ifndef GSP_GATPRE_MIN_BLOCKS
 #define GSP_GATPRE_MIN_BLOCKS 3
 #endif
-template <class W>
+template <class W, class XE>
 struct MinBlocksFor {  // measured on C3 (8 x 64): multi-head computed weights 0.74 -> 0.67 ms at 3 CTAs/SM
-  static constexpr int value = !W::Row::kComputed ? kMinBlocks
+  static constexpr int value = XE::kMinBlocks ? XE::kMinBlocks
+                               : !W::Row::kComputed ? kMinBlocks
                                : (W::Row::kMultiHead ? GSP_GATPRE_MIN_BLOCKS : GSP_GAT_MIN_BLOCKS);
 };
 
-template <int V, int G, class W, class R>
-__global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kernel(const EngineParams p, const W wf) {
+template <int V, int G, class W, class R, class XE = XF32<V>>
+__global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_kernel(const EngineParams p, const W wf) {
   using TM = Team<G>;
   constexpr int T = TM::T;
   constexpr int NT = kThreads / T;  // teams per CTA
@@ -667,7 +760,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
   const int nvalid = (int)(p.f - col0 < V ? p.f - col0 : V);
   const int nact = active ? nvalid : 0;  // columns this lane gathers
   const int64_t last_vec = p.f > 0 ? ((p.f - 1) / V) * V : 0;  // first column of the last valid vector
-  const auto *xb = reinterpret_cast<const typename VecT<V>::T *>(p.x + (active ? col0 : last_vec));
+  const auto *xb = reinterpret_cast<const typename XE::Ptr *>(reinterpret_cast<const typename XE::Elem *>(p.x) +
+                                                                (active ? col0 : last_vec));
   const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
   const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
@@ -733,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
     }
     for (int v = team; v < kVirt; v += NT) {
       float part[V];
-      row_segments<V, G, true, R>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, nact, tl, sg, tmask,
+      row_segments<V, G, true, R, XE>(p, win, wr, start, d, (S * v) / kVirt, (S * (v + 1)) / kVirt, xb, nact, tl, sg, tmask,
                                   s_tc[team], s_tw[team], hl, nullptr, 0, part, [] {});
       if (sg == 0) {
 #pragma unroll
@@ -797,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W>::value) engine_kerne
       }
     };
     float out[V];
-    row_segments<V, G, false, R>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, nact, tl, sg, tmask,
+    row_segments<V, G, false, R, XE>(p, win, wr, start, d, 0, (d + kSeg - 1) / kSeg, xb, nact, tl, sg, tmask,
                                  s_tc[team], s_tw[team], hl, kGat ? &s_cache[team][0] : nullptr, kGat ? kCache : 0,
                                  out, stats);
     finish_row<R, V>(out, d, p.mean);
@@ -859,7 +953,7 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.act = 0;
 }
 
-template <int V, int G, class W, class R>
+template <int V, int G, class W, class R, class XE = XF32<V>>
 gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
   const int64_t grid = L.nslab * L.nblk;
   if (grid <= 0) return GSP_OK;
@@ -870,13 +964,13 @@ gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const 
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || granted[dev] < (int)smem) {
-      if (cudaFuncSetAttribute(engine_kernel<V, G, W, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      if (cudaFuncSetAttribute(engine_kernel<V, G, W, R, XE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
         return check_launch("cudaFuncSetAttribute(engine_kernel)");
       if (dev >= 0 && dev < 64) granted[dev] = (int)smem;
     }
   }
-  engine_kernel<V, G, W, R><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
+  engine_kernel<V, G, W, R, XE><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
   return check_launch("engine_kernel");
 }
 
@@ -904,6 +998,40 @@ gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &
   return fail(GSP_ERR_UNSUPPORTED, "bad vector width %d", L.V);
 }
 
+// fp16 feature storage (XF16): V = 8 halves per lane (16-byte loads) or 1
+template <class W, class R = RedSum>
+gsp_status engine_launch_f16(const EngineLaunch &L, const EngineParams &p, const W &w, cudaStream_t s) {
+  if (L.V == 8) {
+    switch (L.G) {
+      case 1: return engine_launch_vg<8, 1, W, R, XF16<8>>(L, p, w, s);
+      case 2: return engine_launch_vg<8, 2, W, R, XF16<8>>(L, p, w, s);
+      case 4: return engine_launch_vg<8, 4, W, R, XF16<8>>(L, p, w, s);
+      case 8: return engine_launch_vg<8, 8, W, R, XF16<8>>(L, p, w, s);
+      case 16: return engine_launch_vg<8, 16, W, R, XF16<8>>(L, p, w, s);
+      case 32: return engine_launch_vg<8, 32, W, R, XF16<8>>(L, p, w, s);
+    }
+  } else if (L.V == 4) {
+    switch (L.G) {
+      case 1: return engine_launch_vg<4, 1, W, R, XF16<4>>(L, p, w, s);
+      case 2: return engine_launch_vg<4, 2, W, R, XF16<4>>(L, p, w, s);
+      case 4: return engine_launch_vg<4, 4, W, R, XF16<4>>(L, p, w, s);
+      case 8: return engine_launch_vg<4, 8, W, R, XF16<4>>(L, p, w, s);
+      case 16: return engine_launch_vg<4, 16, W, R, XF16<4>>(L, p, w, s);
+      case 32: return engine_launch_vg<4, 32, W, R, XF16<4>>(L, p, w, s);
+    }
+  } else if (L.V == 1) {
+    switch (L.G) {
+      case 1: return engine_launch_vg<1, 1, W, R, XF16<1>>(L, p, w, s);
+      case 2: return engine_launch_vg<1, 2, W, R, XF16<1>>(L, p, w, s);
+      case 4: return engine_launch_vg<1, 4, W, R, XF16<1>>(L, p, w, s);
+      case 8: return engine_launch_vg<1, 8, W, R, XF16<1>>(L, p, w, s);
+      case 16: return engine_launch_vg<1, 16, W, R, XF16<1>>(L, p, w, s);
+      case 32: return engine_launch_vg<1, 32, W, R, XF16<1>>(L, p, w, s);
+    }
+  }
+  return fail(GSP_ERR_UNSUPPORTED, "fp16 engine: bad V %d / G %d", L.V, L.G);
+}
+
 // Explicit instantiations live in engine_inst_*.cu (one TU per weight /
 // reduce family, compiled in parallel); other TUs only declare them.
 #define GSP_ENGINE_INSTANCES(X) \
@@ -917,6 +1045,10 @@ gsp_status engine_launch(const EngineLaunch &L, const EngineParams &p, const W &
   X(WeightGat, RedSum, gat)     \
   X(WeightGatPre, RedSum, gat)
 #ifndef GSP_ENGINE_INSTANTIATE
+extern template gsp_status engine_launch_f16<WeightVal, RedSum>(const EngineLaunch &, const EngineParams &,
+                                                               const WeightVal &, cudaStream_t);
+extern template gsp_status engine_launch_f16<WeightOne, RedSum>(const EngineLaunch &, const EngineParams &,
+                                                               const WeightOne &, cudaStream_t);
 #define GSP_ENGINE_EXTERN(W, R, tu) \
   extern template gsp_status engine_launch<W, R>(const EngineLaunch &, const EngineParams &, const W &, cudaStream_t);
 GSP_ENGINE_INSTANCES(GSP_ENGINE_EXTERN)

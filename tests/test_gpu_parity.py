@@ -166,6 +166,23 @@ def test_spmm_parity(built, f):
             assert_within(host(y1), yref1, cond1, what=f"{name} unweighted f={f}")
 
 
+@pytest.mark.parametrize("f", FS)
+def test_spmm_f16_parity(built, f):
+    """gsp_spmm_f16 (fp16 feature storage, fp32 arithmetic) vs the oracle run
+    on the same fp16 values: the fp32 bound holds exactly as for gsp_spmm."""
+    for name in ("k2", "isolated-nofill", "multi1", "er300-weighted", "cl4000", "rmat3000", "hubs"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        n = go.n
+        for ld in sorted({f, (f + 3) // 4 * 4, (f + 7) // 8 * 8}):
+            xh = features(n, f, ld, seed=f).astype(np.float16)
+            yref, cond = orc.spmm(go.row_ptr, go.col, a64, xh.astype(np.float64), f=f)
+            y = G.gsp_spmm_f16(gn, torch.from_numpy(xh).to(DEV), f=f)
+            assert_within(host(y), yref, cond, what=f"f16 {name} f={f} ld={ld}")
+            y1 = G.gsp_spmm_f16(gn.with_val(None), torch.from_numpy(xh).to(DEV), f=f)
+            yref1, cond1 = orc.spmm(go.row_ptr, go.col, None, xh.astype(np.float64), f=f)
+            assert_within(host(y1), yref1, cond1, what=f"f16 {name} unweighted f={f}")
+
+
 def test_spmm_unaligned_and_strided(built):
     go, gg, (deg, a64, a32), gn = built["cl4000"]
     n = go.n
