@@ -88,6 +88,10 @@ extern "C" gsp_status gsp_gcn_layer(const gsp_csr *a, const float *x, int64_t f_
   const size_t hb = (size_t)a->n_cols * ldh * 4;
   uint8_t *lws = reinterpret_cast<uint8_t *>(h) + hb;
   const size_t lws_bytes = ws_bytes - (size_t)(lws - reinterpret_cast<uint8_t *>(ws));
+  if (ldh > f_out && a->n_cols > 0 &&  // keep the padding columns defined (the SpMM may read them, gsp.h)
+      cudaMemset2DAsync(h + f_out, (size_t)ldh * 4, 0, (size_t)(ldh - f_out) * 4, (size_t)a->n_cols, cs(stream)) !=
+          cudaSuccess)
+    return check_launch("cudaMemset2DAsync(gcn_layer padding)");
   if ((st = gsp_linear(a->n_cols, f_in, x, ldx, w, f_out, f_out, h, ldh, lws, lws_bytes, stream))) return st;
   return gsp_spmm_bias_act(a, h, f_out, ldh, bias, act, y, ldy, stream);
 }

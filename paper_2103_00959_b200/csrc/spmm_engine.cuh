@@ -794,7 +794,14 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
     }
   };
 
-  // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree
+  // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree.
+  //    CTAs with hub rows first wait for the whole window (every thread) and
+  //    meet at a barrier: hub rows span most of it, and compute-sanitizer's
+  //    racecheck then sees the TMA writes ordered before every thread's reads.
+  if (nhub > 0) {
+    ensure(win.we);
+    __syncthreads();
+  }
   for (int k = 0; k < nhub; ++k) {
     const int64_t r = rbeg + s_hub[k];
     const int64_t start = __ldg(p.row_ptr + r);

@@ -25,8 +25,14 @@ from . import (CSR, gsp_attn_project, gsp_gat_aggregate_bias_act, gsp_gcn_layer,
 
 def _padded(n: int, cols: int, device) -> torch.Tensor:
     """[n, cols] view of an [n, round_up(cols, 4)] buffer: rows stay 16-byte
-    aligned so the engine's float4 path applies to any width."""
-    return torch.empty((n, (cols + 3) // 4 * 4), dtype=torch.float32, device=device)[:, :cols]
+    aligned so the engine's float4 path applies to any width.  The padding
+    columns are zeroed once: the next layer's gathers may read them (gsp.h: x
+    is [n][ld]; their sums are never stored) and they stay defined."""
+    ld = (cols + 3) // 4 * 4
+    buf = torch.empty((n, ld), dtype=torch.float32, device=device)
+    if ld > cols:
+        buf[:, cols:].zero_()
+    return buf[:, :cols]
 
 
 def _glorot(shape, rng):
