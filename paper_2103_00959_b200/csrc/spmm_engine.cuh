@@ -779,8 +779,10 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
   const Window win{s_col, p.stage_val ? s_val : nullptr, s_win[0], s_win[1]};
   const int64_t wchunk = s_win[2];
   int ready = 0;  // chunks this thread has seen complete
-#ifdef GSP_DEBUG_WINDOW_BARRIER
-  // debug builds: every thread waits for the whole window, then a CTA barrier
+#ifndef GSP_WINDOW_PER_ROW_WAIT
+  // every thread waits for the whole window, then a CTA barrier: measured as
+  // fast as per-row chunk waits (C3 / C4 / C5 within noise) and it orders the
+  // TMA writes before every read for compute-sanitizer's racecheck too
   if (p.stage)
     for (; ready < kStageChunks && win.wb + ready * wchunk < win.we; ++ready) mbar_wait(&s_bar[ready], 0);
   __syncthreads();
@@ -794,14 +796,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
     }
   };
 
-  // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree.
-  //    CTAs with hub rows first wait for the whole window (every thread) and
-  //    meet at a barrier: hub rows span most of it, and compute-sanitizer's
-  //    racecheck then sees the TMA writes ordered before every thread's reads.
-  if (nhub > 0) {
-    ensure(win.we);
-    __syncthreads();
-  }
+  // 2. hub rows: all teams cooperate; 16 virtual ranges, pairwise tree
   for (int k = 0; k < nhub; ++k) {
     const int64_t r = rbeg + s_hub[k];
     const int64_t start = __ldg(p.row_ptr + r);
