@@ -550,7 +550,28 @@ def main():
         rows["a6_edge_softmax_C3"] = row(t_sm, 8 * e3 * H + 8 * (nn3 + 1), "read logits + write alpha 8 nnz H + row_ptr")
         rows["a7_multihead_spmm_C3"] = row(t_mh, 4 * e3 * H * D + 4 * nn3 * H * D + 4 * e3 + 4 * e3 * H + 8 * (nn3 + 1),
                                            "gathers 4 nnz H D + Y 4nHD + col 4nnz + alpha 4nnz H + row_ptr")
-        del alpha3, logits3
+        # NEXT-3 (GAT backward) on the same C3 inputs: A^T (one-off), SDDMM, edge-softmax
+        # backward, and the full aggregate backward (dz, d_el, d_er)
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record()
+        at3, perm3 = G.gsp_csr_transpose(g3)
+        t1e.record()
+        torch.cuda.synchronize()
+        t_tr = t0e.elapsed_time(t1e)
+        t_sd = timed(lambda: G.gsp_sddmm(g3, y3, z, heads=H, out=logits3), flush, args.warmup, 10)
+        t_sb = timed(lambda: G.gsp_edge_softmax_backward(g3, alpha3, logits3, H, ds=logits3), flush, args.warmup, 10)
+        t_gb = timed(lambda: G.gsp_gat_aggregate_backward(g3, at3, perm3, el, er, z, y3, H, D), flush, args.warmup, 5)
+        b_sd = 4 * e3 * H * D + 4 * nn3 * H * D + 4 * e3 * H + 4 * e3 + 8 * (nn3 + 1)
+        b_sb = 12 * e3 * H + 8 * (nn3 + 1)
+        out.setdefault("secondary", {})["NEXT3_gat_backward_C3"] = {
+            "workload": c3.name, "csr_transpose_ms": t_tr,
+            "sddmm_ms": t_sd, "sddmm_alg_GB/s": b_sd / (t_sd * 1e-3) / 1e9,
+            "sddmm_model": "gathers 4 nnz H D + P rows 4 n H D + out 4 nnz H + col + row_ptr",
+            "softmax_backward_ms": t_sb, "softmax_backward_alg_GB/s": b_sb / (t_sb * 1e-3) / 1e9,
+            "aggregate_backward_ms": t_gb,
+            "aggregate_backward_launches": "softmax, SDDMM, fused softmax/LeakyReLU backward with row sums, "
+                                           "column sums, A^T SpMM"}
+        del alpha3, logits3, at3, perm3
 
     # --- NEXT-1: the paper's Table spmm_time workload (2-layer GCN / GAT inference,
     #     hidden 128, GAT 4 heads), with the paper's RTX 3090 times ---

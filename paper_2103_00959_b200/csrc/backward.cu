@@ -91,50 +91,69 @@ static TransposeLayout transpose_layout(int64_t nnz) {
 constexpr int kSddmmEdgesPerWarp = 64;
 constexpr int kSddmmMaxChunks = 8;  // H*D <= 1024 on the vector path
 
+// H heads of width D starting at column 0 of p / q; out[e * Hout + h0 + h]
+template <int NC>  // 128-float chunks of the H*D row per lane group (NC * 128 >= H*D)
 __global__ void __launch_bounds__(256) sddmm_vec_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                                         int64_t n, int64_t nnz, int H, int D,
                                                         const float *__restrict__ p, int64_t ldp,
                                                         const float *__restrict__ q, int64_t ldq,
-                                                        float *__restrict__ out) {
+                                                        float *__restrict__ out, int Hout, int h0) {
+  constexpr int U = NC >= 8 ? 1 : 8 / NC;  // edges whose q rows are in flight together
+  static_assert(kSddmmEdgesPerWarp == 64, "two column indices per lane");
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t e0 = warp * kSddmmEdgesPerWarp;
   if (e0 >= nnz) return;
   const int64_t e1 = min(nnz, e0 + kSddmmEdgesPerWarp);
+  // the warp's column indices, loaded once (coalesced) and broadcast by shuffle
+  const int cl0 = e0 + lane < e1 ? __ldg(col + e0 + lane) : 0;
+  const int cl1 = e0 + 32 + lane < e1 ? __ldg(col + e0 + 32 + lane) : 0;
   // u = the row holding entry e0: first r with rp[r] > e0, minus one
   int64_t u = warp_lower_bound(rp, n, e0 + 1) - 1;
   int64_t u_end = __ldg(rp + u + 1);
-  const int W = H * D, nchunk = (W + 127) / 128, lpg = D / 4;  // lanes per head group
-  float4 pv[kSddmmMaxChunks];
+  const int W = H * D, lpg = D / 4;  // lanes per head group
+  float4 pv[NC];
   auto load_p = [&]() {
 #pragma unroll
-    for (int k = 0; k < kSddmmMaxChunks; ++k) {
+    for (int k = 0; k < NC; ++k) {
       const int c = 4 * lane + 128 * k;
-      pv[k] = (k < nchunk && c < W) ? __ldg(reinterpret_cast<const float4 *>(p + u * ldp + c)) : make_float4(0, 0, 0, 0);
+      pv[k] = c < W ? __ldg(reinterpret_cast<const float4 *>(p + u * ldp + c)) : make_float4(0, 0, 0, 0);
     }
   };
   load_p();
-  for (int64_t e = e0; e < e1; ++e) {
-    while (e >= u_end) {  // next row (warp-uniform)
-      ++u;
-      u_end = __ldg(rp + u + 1);
-      load_p();
-    }
-    const int64_t v = __ldg(col + e);
+  for (int64_t eb = e0; eb < e1; eb += U) {
+    float4 qv[U][NC];
 #pragma unroll
-    for (int k = 0; k < kSddmmMaxChunks; ++k) {
-      if (k < nchunk) {
+    for (int t = 0; t < U; ++t) {  // every q gather of the batch before the first use
+      const int i = (int)(eb - e0) + t;
+      const int v0 = __shfl_sync(0xffffffffu, cl0, i & 31), v1 = __shfl_sync(0xffffffffu, cl1, i & 31);
+      const int64_t v = i < 32 ? v0 : v1;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const int c = 4 * lane + 128 * k;
+        qv[t][k] = (eb + t < e1 && c < W) ? __ldg(reinterpret_cast<const float4 *>(q + v * ldq + c))
+                                          : make_float4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < U; ++t) {
+      const int64_t e = eb + t;
+      if (e >= e1) break;
+      while (e >= u_end) {  // next row (warp-uniform)
+        ++u;
+        u_end = __ldg(rp + u + 1);
+        load_p();
+      }
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
         const int c = 4 * lane + 128 * k;
         float acc = 0.0f;
-        if (c < W) {
-          const float4 qv = __ldg(reinterpret_cast<const float4 *>(q + v * ldq + c));
-          acc = fmaf(pv[k].x, qv.x, acc);
-          acc = fmaf(pv[k].y, qv.y, acc);
-          acc = fmaf(pv[k].z, qv.z, acc);
-          acc = fmaf(pv[k].w, qv.w, acc);
-        }
+        acc = fmaf(pv[k].x, qv[t][k].x, acc);
+        acc = fmaf(pv[k].y, qv[t][k].y, acc);
+        acc = fmaf(pv[k].z, qv[t][k].z, acc);
+        acc = fmaf(pv[k].w, qv[t][k].w, acc);
         for (int o = 1; o < lpg; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (c < W && (lane % lpg) == 0) out[e * H + c / D] = acc;
+        if (c < W && (lane % lpg) == 0) out[e * Hout + h0 + c / D] = acc;
       }
     }
   }
@@ -168,28 +187,85 @@ __global__ void __launch_bounds__(256) softmax_bwd_warp(const int64_t *__restric
                                                         const float *dalpha, float *ds, const float *__restrict__ el,
                                                         const float *__restrict__ er, double slope,
                                                         float *__restrict__ d_el) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (r >= n) return;
-  const int lane = threadIdx.x & 31;
-  const int h = lane % H, j0 = lane / H, step = 32 / H;
-  const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-  double dot = 0.0;
-  for (int64_t e = b + j0; e < e1; e += step) dot += (double)alpha[e * H + h] * (double)dalpha[e * H + h];
-  for (int off = H; off < 32; off <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-  double rs = 0.0;
-  const double el_u = kGat ? (double)__ldg(el + r * H + h) : 0.0;
-  for (int64_t e = b + j0; e < e1; e += step) {
-    double g = (double)alpha[e * H + h] * ((double)dalpha[e * H + h] - dot);
-    if (kGat) {
-      const double t = el_u + (double)__ldg(er + (int64_t)__ldg(col + e) * H + h);
-      g = t >= 0.0 ? g : g * slope;
-      rs += g;
+  // one warp per row; rows longer than kSbLong entries: the whole CTA after
+  // its short rows (threads t take entries t/H + k*256/H, head t%H; partials
+  // xor-reduced per warp, then the 8 warps in order) -- a single warp would
+  // walk a hub row sequentially
+  constexpr int kSbLong = 256;
+  __shared__ int s_long[8];
+  __shared__ int s_nlong;
+  __shared__ double s_red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  auto row_pass = [&](int64_t r, int64_t b, int64_t e1, int t, int nthreads, bool cta) {
+    const int h = t % H, j0 = t / H, step = nthreads / H;
+    double dot = 0.0;
+#pragma unroll 4
+    for (int64_t e = b + j0; e < e1; e += step) dot += (double)alpha[e * H + h] * (double)dalpha[e * H + h];
+    for (int off = H; off < 32; off <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (cta) {
+      if (lane < H) s_red[warp][lane] = dot;
+      __syncthreads();
+      dot = s_red[0][h];
+      for (int w = 1; w < 8; ++w) dot += s_red[w][h];
+      __syncthreads();
     }
-    ds[e * H + h] = (float)g;
+    double rs = 0.0;
+    const double el_u = kGat ? (double)__ldg(el + r * H + h) : 0.0;
+    for (int64_t e0 = b + j0; e0 < e1; e0 += 4 * (int64_t)step) {
+      // 4 entries' loads before their stores (ds may alias dalpha entry-wise)
+      float a4[4], d4[4], t4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = e0 + k * (int64_t)step;
+        a4[k] = e < e1 ? alpha[e * H + h] : 0.0f;
+        d4[k] = e < e1 ? dalpha[e * H + h] : 0.0f;
+        t4[k] = (kGat && e < e1) ? __ldg(er + (int64_t)__ldg(col + e) * H + h) : 0.0f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = e0 + k * (int64_t)step;
+        if (e < e1) {
+          double g = (double)a4[k] * ((double)d4[k] - dot);
+          if (kGat) {
+            const double tt = el_u + (double)t4[k];
+            g = tt >= 0.0 ? g : g * slope;
+            rs += g;
+          }
+          ds[e * H + h] = (float)g;
+        }
+      }
+    }
+    if (kGat) {
+      for (int off = H; off < 32; off <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+      if (cta) {
+        if (lane < H) s_red[warp][lane] = rs;
+        __syncthreads();
+        rs = s_red[0][h];
+        for (int w = 1; w < 8; ++w) rs += s_red[w][h];
+        __syncthreads();
+        if (threadIdx.x < H) d_el[r * H + h] = (float)rs;
+      } else if (lane < H) {
+        d_el[r * H + h] = (float)rs;
+      }
+    }
+  };
+  const int64_t r = (int64_t)blockIdx.x * 8 + warp;
+  if (r < n) {
+    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+    if (e1 - b > kSbLong) {
+      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
+    } else if (e1 > b) {
+      row_pass(r, b, e1, lane, 32, false);
+    } else if (kGat && lane < H) {
+      d_el[r * H + lane] = 0.0f;
+    }
   }
-  if (kGat) {
-    for (int off = H; off < 32; off <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
-    if (lane < H) d_el[r * H + h] = (float)rs;
+  __syncthreads();
+  for (int k = 0; k < s_nlong; ++k) {
+    const int64_t rr = (int64_t)blockIdx.x * 8 + s_long[k];
+    row_pass(rr, __ldg(rp + rr), __ldg(rp + rr + 1), threadIdx.x, 256, true);
   }
 }
 
@@ -197,15 +273,45 @@ __global__ void __launch_bounds__(256) softmax_bwd_warp(const int64_t *__restric
 __global__ void __launch_bounds__(256) colsum_warp(const int64_t *__restrict__ rpt, const int32_t *__restrict__ perm,
                                                    int64_t n_cols, int H, const float *__restrict__ vals,
                                                    float *__restrict__ out) {
-  const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (v >= n_cols) return;
-  const int lane = threadIdx.x & 31;
-  const int h = lane % H, j0 = lane / H, step = 32 / H;
-  double s = 0.0;
-  for (int64_t k = __ldg(rpt + v) + j0; k < __ldg(rpt + v + 1); k += step)
-    s += (double)vals[(int64_t)__ldg(perm + k) * H + h];
-  for (int off = H; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane < H) out[v * H + h] = (float)s;
+  // one warp per column; columns with more than 256 entries: the whole CTA
+  // after its short columns (partials xor-reduced per warp, warps in order)
+  __shared__ int s_long[8];
+  __shared__ int s_nlong;
+  __shared__ double s_red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  auto col_sum = [&](int64_t v, int t, int nthreads) {
+    const int h = t % H, j0 = t / H, step = nthreads / H;
+    double s = 0.0;
+    const int64_t kend = __ldg(rpt + v + 1);
+#pragma unroll 4
+    for (int64_t k = __ldg(rpt + v) + j0; k < kend; k += step) s += (double)vals[(int64_t)__ldg(perm + k) * H + h];
+    for (int off = H; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+  };
+  const int64_t v = (int64_t)blockIdx.x * 8 + warp;
+  if (v < n_cols) {
+    if (__ldg(rpt + v + 1) - __ldg(rpt + v) > 256) {
+      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
+    } else {
+      const double s = col_sum(v, lane, 32);
+      if (lane < H) out[v * H + lane] = (float)s;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < s_nlong; ++k) {
+    const int64_t vv = (int64_t)blockIdx.x * 8 + s_long[k];
+    const double s = col_sum(vv, threadIdx.x, 256);
+    if (lane < H) s_red[warp][lane] = s;
+    __syncthreads();
+    if (threadIdx.x < H) {
+      double t = s_red[0][threadIdx.x];
+      for (int w = 1; w < 8; ++w) t += s_red[w][threadIdx.x];
+      out[vv * H + threadIdx.x] = (float)t;
+    }
+    __syncthreads();
+  }
 }
 
 // ----------------------------------------------------- attn projection backward
@@ -278,8 +384,18 @@ static gsp_status launch_sddmm(const gsp_csr *a, int H, int64_t D, const float *
                    ldp % 4 == 0 && ldq % 4 == 0 && aligned16(p) && aligned16(q);
   if (vec) {
     const int64_t warps = ceil_div(a->nnz, kSddmmEdgesPerWarp);
-    sddmm_vec_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(a->row_ptr, a->col_idx, a->n_rows, a->nnz, H,
-                                                                   (int)D, p, ldp, q, ldq, out);
+    const unsigned gb = (unsigned)ceil_div(warps, 8);
+    {  // (128-column slab launches measured slower on C3: 1.35 vs 1.23 ms)
+      const int nc = (int)((W + 127) / 128);
+#define GSP_SDDMM_NC(NCV)                                                                                       \
+  sddmm_vec_kernel<NCV><<<gb, 256, 0, s>>>(a->row_ptr, a->col_idx, a->n_rows, a->nnz, H, (int)D, p, ldp, q, ldq, out, \
+                                           H, 0)
+      if (nc <= 1) GSP_SDDMM_NC(1);
+      else if (nc <= 2) GSP_SDDMM_NC(2);
+      else if (nc <= 4) GSP_SDDMM_NC(4);
+      else GSP_SDDMM_NC(8);
+#undef GSP_SDDMM_NC
+    }
   } else {
     sddmm_scalar_kernel<<<(unsigned)std::min<int64_t>(ceil_div(a->nnz * H, 256), 65535 * 8), 256, 0, s>>>(
         a->row_ptr, a->col_idx, a->n_rows, a->nnz, H, (int)D, p, ldp, q, ldq, out);
