@@ -102,7 +102,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 // global -> shared bulk copy (TMA engine, no registers); 16-byte aligned, size % 16 == 0
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-#if defined(GSP_L2HINT) && GSP_L2HINT
+// The staged CSR window is read once per CTA: its L2 lines carry an
+// evict_first policy so the streamed CSR does not push the gathered X slab
+// out of L2 (C4 -0.7%, fp16 C4 -1.5%, profiles/r1_sweep_variants.txt);
+// -DGSP_CSR_EVICT_NORMAL turns it off.
+#if !defined(GSP_CSR_EVICT_NORMAL)
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   asm volatile(
