@@ -648,5 +648,24 @@ def main():
     return 0
 
 
+def _json_stdout():
+    """Keep stdout for the one JSON line: libraries that print banners to fd 1
+    (NCCL prints its version at communicator creation) are moved to stderr;
+    the JSON line goes to the saved original stdout."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    global print
+    out = os.fdopen(saved, "w", buffering=1)
+    _builtin_print = print
+
+    def _print(*a, **k):
+        if "file" not in k:
+            k["file"] = out
+        _builtin_print(*a, **k)
+    print = _print
+
+
 if __name__ == "__main__":
+    _json_stdout()
     sys.exit(main())
