@@ -56,6 +56,33 @@ def test_c4_spmm_sampled_rows(c4):
     assert np.array_equal(y, y2)
 
 
+def test_c4_spmm_f16_sampled_rows(c4):
+    """gsp_spmm_f16 at full size (bench's C4_spmm_f16_storage line) vs the oracle
+    on the fp16 values, sampled rows incl. the heaviest hubs."""
+    cfg, go, (deg, a64, a32), gg, gn = c4
+    x = features(cfg.n, cfg.f, cfg.ld, seed=2)
+    xh = x.astype(np.float16)
+    y = host(G.gsp_spmm_f16(gn, torch.from_numpy(xh).to(DEV), f=cfg.f))
+    x64 = xh.astype(np.float64)
+    for r in _sample_rows(go.row_ptr, k=200, seed=1):
+        yr, cr = orc.spmm(go.row_ptr, go.col, a64, x64, f=cfg.f, r0=r, r1=r + 1)
+        assert_within(y[r:r + 1], yr, cr, what=f"C4 f16 row {r}")
+
+
+def test_c4_linear_tensor_cores_sampled_rows():
+    """The NEXT-1 layer-1 GEMM shape (232,965 x 602 -> 128) on the tcgen05 path
+    vs the oracle's dense product on sampled rows (3xTF32 bound)."""
+    from test_gpu_parity import _tc_rel
+    cfg = CONFIGS["C4"]
+    x = features(cfg.n, cfg.f, cfg.ld, seed=2)
+    w = uniform((cfg.f, 128), seed=7)
+    y = host(G.gsp_linear(dev(x)[:, :cfg.f], dev(w)))
+    rows = np.random.default_rng(3).choice(cfg.n, 300, replace=False)
+    rows = np.concatenate([rows, [0, cfg.n - 1]])
+    yr, c = orc.linear(x[rows, :cfg.f].copy(), w)
+    assert_within(y[rows], yr, c, rel=_tc_rel(cfg.f), what="C4 layer-1 GEMM")
+
+
 def test_c4_identity_every_row(c4):
     """I1: A^ sqrt(d) = sqrt(d) on all 232,965 rows."""
     cfg, go, (deg, a64, a32), gg, gn = c4
