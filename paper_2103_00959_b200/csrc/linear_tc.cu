@@ -231,14 +231,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {  // thread-safe one-time lookup
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
+      return reinterpret_cast<EncodeTiledFn>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -305,13 +305,13 @@ gsp_status linear_tc(int64_t n, int64_t f_in, const float *x, int64_t ldx, const
   int stages = (int)std::min<size_t>(4, (100u * 1024u) / stage);  // <= ~100 KB: 2 CTAs per SM
   p.stages = std::max(stages, 2);
   const size_t smem = (size_t)p.stages * stage + 1024;
-  static int granted[64] = {0};
+  static std::atomic<int> granted[64];  // per device: largest dynamic smem already granted
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || granted[dev] < (int)smem) {
+  if (dev < 0 || dev >= 64 || granted[dev].load(std::memory_order_relaxed) < (int)smem) {
     if (cudaFuncSetAttribute(linear_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute(linear_tc_kernel)");
-    if (dev >= 0 && dev < 64) granted[dev] = (int)smem;
+    if (dev >= 0 && dev < 64) granted[dev].store((int)smem, std::memory_order_relaxed);
   }
   linear_tc_kernel<<<dim3((unsigned)ceil_div(n, kTcBM), (unsigned)ntiles), kTcThreads, smem, s>>>(tx, tb, p);
   return check_launch("linear_tc_kernel");

@@ -962,14 +962,14 @@ gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const 
   if (grid >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", (long long)grid);
   const size_t smem = p.stage ? (size_t)p.win_cap * (p.stage_val ? 8 : 4) : 0;
   if (smem > 0) {  // static + dynamic may exceed the 48 KB default: raise the cap once per device
-    static int granted[64] = {0};
+    static std::atomic<int> granted[64];  // per device: largest dynamic smem already granted
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || granted[dev] < (int)smem) {
+    if (dev < 0 || dev >= 64 || granted[dev].load(std::memory_order_relaxed) < (int)smem) {
       if (cudaFuncSetAttribute(engine_kernel<V, G, W, R, XE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
         return check_launch("cudaFuncSetAttribute(engine_kernel)");
-      if (dev >= 0 && dev < 64) granted[dev] = (int)smem;
+      if (dev >= 0 && dev < 64) granted[dev].store((int)smem, std::memory_order_relaxed);
     }
   }
   engine_kernel<V, G, W, R, XE><<<(unsigned)grid, kThreads, smem, s>>>(p, w);
