@@ -159,6 +159,89 @@ __global__ void __launch_bounds__(256) sddmm_vec_kernel(const int64_t *__restric
   }
 }
 
+// Transposed reduction (LPG = D/4 lanes per head, LPG <= 16): a batch of up to
+// LPG consecutive entries of ONE row is gathered together; each lane forms
+// its 4-column partial dot for every entry of the batch, then a butterfly
+// reduce-scatter over the head's LPG lanes (LPG-1 shuffles instead of
+// LPG*log2(LPG)) leaves the full dot of entry j in the head's lane j.
+// Order per (entry, head): lane fma chain over x,y,z,w, then the butterfly
+// from distance LPG/2 down to 1 -- fixed.
+template <int LPG, int NC>
+__global__ void __launch_bounds__(256, 2) sddmm_tr_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                          int64_t n, int64_t nnz, int H, int D,
+                                                          const float *__restrict__ p, int64_t ldp,
+                                                          const float *__restrict__ q, int64_t ldq,
+                                                          float *__restrict__ out) {
+  static_assert(kSddmmEdgesPerWarp == 64, "two column indices per lane");
+  const int lane = threadIdx.x & 31, gl = lane % LPG;
+  const int64_t warp = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t e0 = warp * kSddmmEdgesPerWarp;
+  if (e0 >= nnz) return;
+  const int64_t e1 = min(nnz, e0 + kSddmmEdgesPerWarp);
+  const int cl0 = e0 + lane < e1 ? __ldg(col + e0 + lane) : 0;
+  const int cl1 = e0 + 32 + lane < e1 ? __ldg(col + e0 + 32 + lane) : 0;
+  int64_t u = warp_lower_bound(rp, n, e0 + 1) - 1;
+  int64_t u_end = __ldg(rp + u + 1);
+  const int W = H * D;
+  float4 pv[NC];
+  auto load_p = [&]() {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = 4 * lane + 128 * k;
+      pv[k] = c < W ? __ldg(reinterpret_cast<const float4 *>(p + u * ldp + c)) : make_float4(0, 0, 0, 0);
+    }
+  };
+  load_p();
+  int64_t e = e0;
+  while (e < e1) {
+    while (e >= u_end) {  // next row (warp-uniform)
+      ++u;
+      u_end = __ldg(rp + u + 1);
+      load_p();
+    }
+    const int cnt = (int)min((int64_t)LPG, min(u_end, e1) - e);
+    int vcol[LPG];
+#pragma unroll
+    for (int i = 0; i < LPG; ++i) {
+      const int idx = (int)(e - e0) + i;
+      const int a0 = __shfl_sync(0xffffffffu, cl0, idx & 31), a1 = __shfl_sync(0xffffffffu, cl1, idx & 31);
+      vcol[i] = idx < 32 ? a0 : a1;
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int c = 4 * lane + 128 * k;
+      float4 qv[LPG];
+#pragma unroll
+      for (int i = 0; i < LPG; ++i)  // every gather of the batch before the first use
+        qv[i] = (i < cnt && c < W) ? __ldg(reinterpret_cast<const float4 *>(q + (int64_t)vcol[i] * ldq + c))
+                                   : make_float4(0, 0, 0, 0);
+      float v[LPG];
+#pragma unroll
+      for (int i = 0; i < LPG; ++i) {
+        float acc = 0.0f;
+        acc = fmaf(pv[k].x, qv[i].x, acc);
+        acc = fmaf(pv[k].y, qv[i].y, acc);
+        acc = fmaf(pv[k].z, qv[i].z, acc);
+        acc = fmaf(pv[k].w, qv[i].w, acc);
+        v[i] = acc;
+      }
+#pragma unroll
+      for (int m = LPG / 2; m >= 1; m >>= 1) {  // reduce-scatter: lane j of the group ends with entry j
+        const bool hi = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+          const float send = hi ? v[i] : v[i + m];
+          const float keep = hi ? v[i + m] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+      const int cg = 128 * k + 4 * (lane - gl);  // first column of this lane's head group
+      if (gl < cnt && cg < W) out[(e + gl) * H + cg / D] = v[0];
+    }
+    e += cnt;
+  }
+}
+
 // generic path: one thread per (entry, head), sequential dot product
 __global__ void sddmm_scalar_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col, int64_t n,
                                     int64_t nnz, int H, int D, const float *__restrict__ p, int64_t ldp,
@@ -385,8 +468,23 @@ static gsp_status launch_sddmm(const gsp_csr *a, int H, int64_t D, const float *
   if (vec) {
     const int64_t warps = ceil_div(a->nnz, kSddmmEdgesPerWarp);
     const unsigned gb = (unsigned)ceil_div(warps, 8);
-    {  // (128-column slab launches measured slower on C3: 1.35 vs 1.23 ms)
-      const int nc = (int)((W + 127) / 128);
+    const int lpg = (int)(D / 4), nc = (int)((W + 127) / 128);
+    if (lpg >= 2 && lpg <= 16 && nc <= 4) {
+#define GSP_SDDMM_TR(L, NCV)                                                                                 \
+  sddmm_tr_kernel<L, NCV><<<gb, 256, 0, s>>>(a->row_ptr, a->col_idx, a->n_rows, a->nnz, H, (int)D, p, ldp, q, ldq, out)
+#define GSP_SDDMM_TR_NC(L)        \
+  if (nc <= 1) GSP_SDDMM_TR(L, 1); \
+  else if (nc <= 2) GSP_SDDMM_TR(L, 2); \
+  else GSP_SDDMM_TR(L, 4);
+      switch (lpg) {
+        case 2: GSP_SDDMM_TR_NC(2) break;
+        case 4: GSP_SDDMM_TR_NC(4) break;
+        case 8: GSP_SDDMM_TR_NC(8) break;
+        case 16: GSP_SDDMM_TR_NC(16) break;
+      }
+#undef GSP_SDDMM_TR_NC
+#undef GSP_SDDMM_TR
+    } else {  // (128-column slab launches measured slower on C3: 1.35 vs 1.23 ms)
 #define GSP_SDDMM_NC(NCV)                                                                                       \
   sddmm_vec_kernel<NCV><<<gb, 256, 0, s>>>(a->row_ptr, a->col_idx, a->n_rows, a->nnz, H, (int)D, p, ldp, q, ldq, out, \
                                            H, 0)

@@ -425,7 +425,7 @@ def test_csr_transpose_bit_exact(built):
         np.testing.assert_array_equal(host(perm).astype(np.int64), pm, err_msg=name)
 
 
-@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 64), (3, 16), (1, 602)])
+@pytest.mark.parametrize("H,D", [(1, 1), (1, 64), (2, 3), (4, 8), (8, 64), (3, 16), (1, 602), (8, 32), (4, 64), (2, 128), (16, 8)])
 def test_sddmm_parity(built, H, D):
     """|t - t_ref| <= 1e-5 * sum_k |p q| + 1e-6 (D-term dot products)."""
     for name in ("multi1", "cl4000", "hubs"):
