@@ -563,12 +563,8 @@ def main():
                                            "gathers 4 nnz H D + Y 4nHD + col 4nnz + alpha 4nnz H + row_ptr")
         # NEXT-3 (GAT backward) on the same C3 inputs: A^T (one-off), SDDMM, edge-softmax
         # backward, and the full aggregate backward (dz, d_el, d_er)
-        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0e.record()
         at3, perm3 = G.gsp_csr_transpose(g3)
-        t1e.record()
-        torch.cuda.synchronize()
-        t_tr = t0e.elapsed_time(t1e)
+        t_tr = timed(lambda: G.gsp_csr_transpose(g3), flush, 1, 3)  # one-off per graph; steady state
         t_sd = timed(lambda: G.gsp_sddmm(g3, y3, z, heads=H, out=logits3), flush, args.warmup, 10)
         t_sb = timed(lambda: G.gsp_edge_softmax_backward(g3, alpha3, logits3, H, ds=logits3), flush, args.warmup, 10)
         t_gb = timed(lambda: G.gsp_gat_aggregate_backward(g3, at3, perm3, el, er, z, y3, H, D), flush, args.warmup, 5)
