@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
     dig[i] = d;
   }
   __syncthreads();
+  uint32_t total;  // this tile's count of digit tid
   {
     uint32_t run = 0;
 #pragma unroll
@@ -164,15 +165,44 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(
       wcnt[w][tid] = run;
       run += t;
     }
+    total = run;
   }
+  // tile-local bucket starts: exclusive scan of the 256 digit totals
+  __shared__ uint32_t tb[256];
+  __shared__ uint32_t wsum[8];
+  uint32_t incl = total;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
   __syncthreads();
+  uint32_t wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += wsum[w];
+  tb[tid] = wpre + incl - total;
+  __syncthreads();
+  // stage the tile in shared memory in output order (same positions as a
+  // direct scatter: stable), then write each digit's run contiguously
+  __shared__ uint64_t sk[kRadixTile];
+  __shared__ uint32_t sv[kRadixTile];
 #pragma unroll
   for (int i = 0; i < kRadixItems; ++i) {
     if (dig[i] < 256) {
-      const uint32_t pos = gbase[dig[i]] + wcnt[warp][dig[i]] + rank[i];
-      kout[pos] = k[i];
-      vout[pos] = v[i];
+      const uint32_t lpos = tb[dig[i]] + wcnt[warp][dig[i]] + rank[i];
+      sk[lpos] = k[i];
+      sv[lpos] = v[i];
     }
+  }
+  __syncthreads();
+  const int64_t tile0 = (int64_t)blockIdx.x * kRadixTile;
+  const int cnt = (int)min((int64_t)kRadixTile, N - tile0);
+  for (int j = tid; j < cnt; j += kRadixThreads) {
+    const uint64_t key = sk[j];
+    const int d = (int)((key >> shift) & 255u);
+    const uint32_t pos = gbase[d] + (uint32_t)j - tb[d];
+    kout[pos] = key;
+    vout[pos] = sv[j];
   }
 }
 
