@@ -249,6 +249,15 @@ __global__ void head_flags_kernel(const uint64_t *__restrict__ keys, int64_t S, 
 
 // For every head: fp64 sum of the run's weights in pos order -> fp32; the
 // column; and the row_ptr entries of rows that start here (gap filling).
+// key / n for key < n^2, n < 2^31 without the 64-bit division subroutine:
+// a double-precision estimate (off by at most one) corrected exactly
+__device__ __forceinline__ uint64_t div_by_n(uint64_t key, uint64_t n, double inv_n) {
+  uint64_t r = (uint64_t)((double)key * inv_n);
+  if (r * n > key) --r;
+  else if ((r + 1) * n <= key) ++r;
+  return r;
+}
+
 __global__ void coalesce_kernel(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ pos, int64_t S,
                                 int64_t n, int64_t m, int und, const float *__restrict__ w, float fill,
                                 const uint32_t *__restrict__ head, const uint32_t *__restrict__ idx,
@@ -256,11 +265,12 @@ __global__ void coalesce_kernel(const uint64_t *__restrict__ keys, const uint32_
                                 int64_t *__restrict__ nnz_out) {
   const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
   const int64_t mm = und ? 2 * m : m;
+  const double inv_n = 1.0 / (double)n;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S; k += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = keys[k];
     if (key >= EMPTY) continue;
     const bool last_valid = (k + 1 == S) || keys[k + 1] >= EMPTY;
-    const int64_t r = (int64_t)(key / (uint64_t)n);
+    const int64_t r = (int64_t)div_by_n(key, (uint64_t)n, inv_n);
     if (head[k]) {
       double s = 0.0;
       for (int64_t j = k; j < S && keys[j] == key; ++j) {
@@ -277,7 +287,7 @@ __global__ void coalesce_kernel(const uint64_t *__restrict__ keys, const uint32_
       const int64_t o = idx[k];
       col[o] = (int32_t)(key - (uint64_t)r * n);
       val[o] = __double2float_rn(s);
-      const int64_t prev_r = (k == 0) ? -1 : (int64_t)(keys[k - 1] / (uint64_t)n);
+      const int64_t prev_r = (k == 0) ? -1 : (int64_t)div_by_n(keys[k - 1], (uint64_t)n, inv_n);
       for (int64_t rr = prev_r + 1; rr <= r; ++rr) row_ptr[rr] = o;
     }
     if (last_valid) {
