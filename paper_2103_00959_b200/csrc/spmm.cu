@@ -276,7 +276,11 @@ extern "C" gsp_status gsp_spmm_f16(const gsp_csr *a, const void *x, int64_t f, i
   if (GSP_F16_VMAX >= 8 && ldx % 8 == 0 && aligned16(x)) vmax = 8;
   else if (ldx % 4 == 0 && aligned8(x)) vmax = 4;
   EngineLaunch L, T;
-  if ((st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, 0, 0, &L, 1))) return st;
+#ifndef GSP_F16_SLAB
+#define GSP_F16_SLAB 0  // 0: the engine's default (32 lanes x V)
+#endif
+  const int32_t slab_req = (GSP_F16_SLAB > 0 && vmax == 4 && f > GSP_F16_SLAB) ? GSP_F16_SLAB : 0;
+  if ((st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, slab_req, 0, &L, 1))) return st;
   const __half *xh = static_cast<const __half *>(x);
   const int64_t SW = L.slab_cols, rem = f % SW;
   cudaStream_t s = cs(stream);
