@@ -545,6 +545,10 @@ def main():
             "alg_GB/s": gb / (tgm * 1e-3) / 1e9, "frac_of_hbm_peak": gb / (tgm * 1e-3) / 1e9 / peak,
             "launches": "row_stats_warp<8,1,0> (softmax statistics, all heads) + engine_kernel<4,32,WeightGatT<1>> "
                         "(alpha formed on the fly, 2 heads per warp)"}
+        out["secondary"]["C3_gat"]["single_launch_ms"] = timed(
+            lambda: G.gsp_gat_aggregate(g3, el, er, z, H, D, 0.2, y=y3, single_launch=True), flush, args.warmup, 10)
+        out["secondary"]["C3_gat"]["single_launch_note"] = (
+            "ws = NULL schedule: statistics reduced inside the aggregate kernel per (row, head), one launch")
         # standalone a6 (edge softmax of given logits) and a7 (multi-head SpMM with given alpha) on C3
         _, alpha3 = G.gsp_gat_aggregate(g3, el, er, z, H, D, 0.2, y=y3, alpha_out=True, ws=ws)
         logits3 = alpha3.clone()
