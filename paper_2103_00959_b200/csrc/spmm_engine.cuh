@@ -481,7 +481,10 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
                                            int sg, float (&a)[Team<G>::NACC][V], Pre &&pre) {
   using TM = Team<G>;
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
-  constexpr int U = TM::U < XE::kU ? TM::U : XE::kU;
+  // gathers in flight per lane: the element policy's budget; the single-launch
+  // GAT (in-kernel statistics, fp64 row state live) measured best at 4
+  constexpr int kUx = Row::kInStats ? (XE::kU < 4 ? XE::kU : 4) : XE::kU;
+  constexpr int U = TM::U < kUx ? TM::U : kUx;
   using Raw = typename XE::Raw;
   static_assert(EPS % U == 0, "GSP_UNROLL must divide the edges per sub-group and segment (power of two)");
   (void)nact;
