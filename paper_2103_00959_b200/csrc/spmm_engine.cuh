@@ -198,12 +198,15 @@ struct XF16<8> {
     }
   }
 };
+#ifndef GSP_F16_UNROLL
+#define GSP_F16_UNROLL GSP_UNROLL
+#endif
 template <>
 struct XF16<4> {
   using Elem = __half;
   using Ptr = uint2;
   static constexpr int kWidth = 4;
-  static constexpr int kU = kUnroll;
+  static constexpr int kU = GSP_F16_UNROLL;
   static constexpr int kMinBlocks = 0;
   struct Raw {
     uint2 q;
