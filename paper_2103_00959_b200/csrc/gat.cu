@@ -210,15 +210,18 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
     const int64_t r = rbase + s_long[k];
     const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
     const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
+    const bool resident = (e1 - b) <= (int64_t)kStatWarps * kTile;  // one chunk per warp: no reloads
     double m = -INFINITY, sum = 0.0;
     for (int pass = 0; pass < (kApply ? 3 : 2); ++pass) {
       const float inv_s = pass == 2 ? (float)(1.0 / sum) : 0.0f;
       double acc = pass == 0 ? -INFINITY : 0.0;
       for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
         const int cnt = (int)min((int64_t)kTile, e1 - c0);
-        __syncwarp();
-        stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
-        __syncwarp();
+        if (pass == 0 || !resident) {  // a row of <= 8 tiles keeps each warp's chunk in its tile
+          __syncwarp();
+          stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
+          __syncwarp();
+        }
         if (pass == 0) {  // max of the stored values, then of the scores (monotone, see stat_row)
           float mr = -INFINITY;
           for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
