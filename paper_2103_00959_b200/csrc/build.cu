@@ -425,7 +425,12 @@ __global__ void __launch_bounds__(256) degree_kernel(const int64_t *__restrict__
 __device__ __forceinline__ float norm_entry(double du, double dv, float w) {
   const double p = __dmul_rn(du, dv);
   double r = 0.0;
-  if (p != 0.0) r = __ddiv_rn((double)w, __dsqrt_rn(p));
+  if (p != 0.0) {
+    const double q = __dsqrt_rn(p);
+    // unit weights (every benchmark graph): the correctly rounded reciprocal
+    // is exactly the correctly rounded 1 / q, and cheaper than the division
+    r = (w == 1.0f) ? __drcp_rn(q) : __ddiv_rn((double)w, q);
+  }
   return __double2float_rn(r);
 }
 
