@@ -437,29 +437,39 @@ __device__ __forceinline__ float norm_entry(double du, double dv, float w) {
 __global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                                         const float *val, int64_t n, const double *__restrict__ deg,
                                                         float *val_out) {
-  __shared__ int s_long[8];
-  __shared__ int s_nlong;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_nlong = 0;
-  __syncthreads();
-  const int64_t u = (int64_t)blockIdx.x * 8 + warp;
-  if (u < n) {
-    const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
-    if (e1 - b > kNormLong) {
-      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
-    } else {
-      const double du = __ldg(deg + u);
+  // rows of at most kNormLong entries: one warp each (no CTA barrier);
+  // longer rows are left to normalize_long_kernel
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= n) return;
+  const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
+  if (e1 - b > kNormLong) return;
+  const double du = __ldg(deg + u);
 #pragma unroll 2
-      for (int64_t e = b + lane; e < e1; e += 32) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
+  for (int64_t e = b + lane; e < e1; e += 32) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
+}
+
+// entries of rows longer than kNormLong, edge-balanced: warp w takes entries
+// [256 w, 256 w + 256); each lane walks the rows its entries fall in (from
+// the warp's first row) and normalises the entries of long rows only
+constexpr int kNormChunk = 256;
+__global__ void __launch_bounds__(256) normalize_long_kernel(const int64_t *__restrict__ rp,
+                                                             const int32_t *__restrict__ col, const float *val,
+                                                             int64_t n, int64_t nnz, const double *__restrict__ deg,
+                                                             float *val_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kNormChunk;
+  if (e0 >= nnz) return;
+  const int64_t e1 = min(nnz, e0 + kNormChunk);
+  int64_t u = warp_lower_bound(rp, n, e0 + 1) - 1;  // row holding entry e0
+  int64_t ub = __ldg(rp + u), ue = __ldg(rp + u + 1);
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    while (e >= ue) {
+      ++u;
+      ub = ue;
+      ue = __ldg(rp + u + 1);
     }
-  }
-  __syncthreads();
-  for (int k = 0; k < s_nlong; ++k) {
-    const int64_t r = (int64_t)blockIdx.x * 8 + s_long[k];
-    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-    const double du = __ldg(deg + r);
-#pragma unroll 2
-    for (int64_t e = b + threadIdx.x; e < e1; e += 256) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
+    if (ue - ub > kNormLong) val_out[e] = norm_entry(__ldg(deg + u), __ldg(deg + __ldg(col + e)), val[e]);
   }
 }
 
@@ -569,5 +579,7 @@ extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double
   if (a->nnz == 0) return GSP_OK;
   normalize_kernel<<<(unsigned)ceil_div(a->n_rows, 8), 256, 0, s>>>(a->row_ptr, a->col_idx, a->val, a->n_rows,
                                                                    deg_out, val_out);
+  normalize_long_kernel<<<(unsigned)ceil_div(a->nnz, 8 * kNormChunk), 256, 0, s>>>(
+      a->row_ptr, a->col_idx, a->val, a->n_rows, a->nnz, deg_out, val_out);
   return check_launch("normalize");
 }
