@@ -88,6 +88,31 @@ def test_host_validation(L):
     assert L.gsp_csr_slice(ctypes.byref(c), hb, 2, 0, 5, P(0x7000), P(0x8000), None, s) == 1
 
 
+def test_host_validation_new_entry_points(L):
+    """fp16-storage SpMM and the tensor-core GEMM reject bad arguments on the
+    host, before any launch (gsp.h Errors)."""
+    P = ctypes.c_void_p
+    s = P(0)
+    c = _csr()
+    # gsp_spmm_f16: ld < f, NULL y, x / y overlap (x counted in 2-byte elements)
+    assert L.gsp_spmm_f16(ctypes.byref(c), P(0x10000), 8, 4, P(0x90000), 8, s) == 1
+    assert L.gsp_spmm_f16(ctypes.byref(c), P(0x10000), 4, 4, None, 4, s) == 1
+    assert L.gsp_spmm_f16(ctypes.byref(c), P(0x10000), 4, 4, P(0x10010), 4, s) == 5
+    # gsp_linear: ldw < f_out; x / y overlap
+    assert L.gsp_linear(10, 8, P(0x10000), 8, P(0x20000), 2, 4, P(0x90000), 4, None, 0, s) == 1
+    assert L.gsp_linear(10, 8, P(0x10000), 8, P(0x20000), 4, 4, P(0x10020), 4, None, 0, s) == 5
+    # workspace queries
+    n = ctypes.c_size_t(0)
+    assert L.gsp_linear_workspace(-1, 4, ctypes.byref(n)) == 1
+    assert L.gsp_linear_workspace(602, 128, ctypes.byref(n)) == 0
+    assert n.value >= 2 * 128 * 608 * 4  # hi + lo copies of W^T, K padded to the tile
+    assert L.gsp_gcn_layer_workspace(1000, 602, 128, ctypes.byref(n)) == 0
+    assert n.value >= 1000 * 128 * 4 + 2 * 128 * 608 * 4
+    cg = _csr(n_rows=100, n_cols=100, nnz=500)
+    assert L.gsp_gat_workspace(ctypes.byref(cg), 8, ctypes.byref(n)) == 0
+    assert n.value == 100 * 8 * 16  # (m fp64, 1/S fp32, pad) per (row, head)
+
+
 def test_build_workspace_query(L):
     ws = ctypes.c_size_t(0)
     nmax = ctypes.c_int64(0)
