@@ -35,7 +35,8 @@
  *    which other rows are in the call: a row-partitioned multi-GPU run is
  *    bitwise equal to the single-GPU run.
  *  - Threads.  Re-entrant; no global mutable state except the thread-local
- *    error string and a per-device cached SM count.
+ *    error string, the thread-local flags of gsp_set_flags and a per-device
+ *    cached SM count.
  */
 #ifndef GSP_H_
 #define GSP_H_
@@ -47,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GSP_VERSION 1
+#define GSP_VERSION 2
 
 /* ABI-compatible with cudaStream_t / CUstream. */
 typedef struct CUstream_st *gsp_stream;
@@ -66,8 +67,23 @@ typedef enum {
 
 typedef enum { GSP_I32 = 0, GSP_I64 = 1 } gsp_index_type;
 
-/* flags for gsp_coo_to_csr */
-enum { GSP_UNDIRECTED = 1u };
+/* flags: GSP_UNDIRECTED for gsp_coo_to_csr; GSP_VALIDATE for gsp_set_flags */
+enum { GSP_UNDIRECTED = 1u, GSP_VALIDATE = 2u };
+
+/* ---------------------------------------------------------------------------
+ * Validate mode ("pre: all finite ... errors: non-finite
+ * logit"; reading A12).  gsp_set_flags(GSP_VALIDATE) turns it on for calls
+ * made BY THE CALLING THREAD (thread-local; 0 turns it off; other bits are
+ * GSP_ERR_INVALID_ARG).  In validate mode gsp_edge_softmax checks `logits`,
+ * and gsp_gat_aggregate, gsp_gat_aggregate_bias_act and
+ * gsp_gat_aggregate_backward check `el` and `er`, for NaN / Inf before any
+ * compute launch: one streaming kernel per array, then the call synchronises
+ * its stream once and returns GSP_ERR_NONFINITE (outputs untouched) if any
+ * value is non-finite.  Outside validate mode nothing is checked and a NaN
+ * propagates within its row only.  Validating calls on one device are
+ * serialised internally. */
+gsp_status gsp_set_flags(uint32_t flags);
+uint32_t gsp_get_flags(void);
 
 /*
  * Borrowed view of a CSR matrix in device memory ("CogDL utilizes
@@ -124,15 +140,21 @@ gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, const void *dst
 /* ---------------------------------------------------------------------------
  * a2. Degree and GCN symmetric normalisation A^ = D~^-1/2 A~ D~^-1/2.
  * P:244 (Eq. gcn_layer: D~_ii = sum_j A~_ij).  Readings A3, A7, A8.
- *   d_u = sum of row u's weights, fp64, sequential in column order;
- *   val_out[e] = fp32( w_e / sqrt(d_u * d_v) ) with IEEE round-to-nearest
- *   double operations (bit-identical to the oracle), 0 when d_u * d_v == 0.
- *   a->val must be non-NULL (the A~ weights).  val_out may equal a->val
- *   (in place).  deg_out: device fp64 [n_rows].
- *   Requires a square matrix (n_rows == n_cols).
+ *   d_u = sum of row u's weights, fp64 (exact whenever the row sum is exact
+ *   in fp64, A8); val_out[e] = fp32( w_e / sqrt(d_u * d_v) ) with IEEE
+ *   round-to-nearest double operations (bit-identical to the oracle), 0 when
+ *   d_u * d_v == 0.  a->val must be non-NULL (the A~ weights).  val_out may
+ *   equal a->val (in place).  Requires a square matrix (n_rows == n_cols).
+ *   deg_out  device fp64 [n_rows] receiving d, or NULL;
+ *   ws       when deg_out is NULL: device, 8-byte aligned, >=
+ *            gsp_sym_normalize_workspace() bytes (holds d between the two
+ *            passes; the library never allocates) -- else ignored (may be NULL).
+ * Errors: GSP_ERR_WORKSPACE if deg_out and ws are both missing / too small;
+ * GSP_ERR_ALIAS if val_out overlaps the degree array.
  */
-gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, gsp_stream stream);
-/* deg_out is REQUIRED (it is also the scratch holding d for the second pass). */
+gsp_status gsp_sym_normalize_workspace(const gsp_csr *a, size_t *ws_bytes);
+gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, void *ws, size_t ws_bytes,
+                             gsp_stream stream);
 
 /* ---------------------------------------------------------------------------
  * a3. SpMM  Y = A X  (GSpMM, phi = sum, psi = multiply).
@@ -149,6 +171,9 @@ gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, 
  */
 gsp_status gsp_spmm(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *y,
                     int64_t ldy, gsp_stream stream);
+
+/* gsp_spmm_ex with slab_cols == 256 reads two float4 per lane: it needs
+ * ldx % 8 == 0 and a 32-byte aligned x (else GSP_ERR_INVALID_ARG). */
 
 /* gsp_spmm_f16: gsp_spmm with fp16 feature storage (mixed
  * precision "fp16=True"): x device IEEE binary16 [a->n_cols][ldx] (padding as
@@ -328,17 +353,19 @@ gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const 
  * H^(l+1) = sigma(A^ H^(l) W^(l)); P:661-663 Table spmm_time).
  * gsp_linear: row-major y[n][f_out] = x[n][f_in] w[f_in][f_out] (ldw >= f_out).
  *   With ws >= gsp_linear_workspace(f_in, f_out) bytes (device, any
- *   alignment), f_out <= 256, ldx % 4 == 0 and x 16-byte aligned: tcgen05
+ *   alignment), f_out <= 4096, ldx % 4 == 0 and x 16-byte aligned: tcgen05
  *   tensor cores, kind::tf32 with 3xTF32 splitting (x = hi + lo, w = hi + lo,
  *   x w ~= lo.hi + hi.lo + hi.hi, fp32 accumulation in TMEM; per-product
- *   error <= 2^-20 |x||w|), operands staged by TMA (SWIZZLE_128B), one CTA per
- *   128 rows.  Otherwise (ws NULL / too small, wider or unaligned operands) a
+ *   error <= 2^-20 |x||w|), operands staged by TMA (SWIZZLE_64B: 16-float K
+ *   tiles), one CTA per (128 rows, <= 256 output columns).  Otherwise (ws
+ *   NULL / too small, wider or unaligned operands) a
  *   cuBLAS SGEMM with fp32 compute (no TF32); one cuBLAS handle per (thread,
  *   device) is created on first use.
  * gsp_spmm_bias_act: y = act(A x + bias) with bias [f] (nullable) and the
  *   activation fused into the SpMM epilogue.
  * gsp_gcn_layer: y = act(A (x w) + bias): gsp_linear into ws, then
- *   gsp_spmm_bias_act.  ws >= gsp_gcn_layer_workspace(a->n_cols, f_in, f_out)
+ *   gsp_spmm_bias_act.  Every argument (act, pointers, leading dimensions, y
+ *   and x against ws: GSP_ERR_ALIAS) is checked before the first enqueue.  ws >= gsp_gcn_layer_workspace(a->n_cols, f_in, f_out)
  *   (holds x w and the tensor-core GEMM's split-W workspace).
  * gsp_gat_aggregate_bias_act: gsp_gat_aggregate with y = act(Y + bias[H*D])
  *   fused (ELU for hidden GAT layers); ws as for gsp_gat_aggregate. */
@@ -379,13 +406,6 @@ gsp_status gsp_partition_rows(const gsp_csr *a, int32_t parts, int64_t *row_boun
 gsp_status gsp_csr_slice(const gsp_csr *a, const int64_t *row_bounds, int32_t parts, int32_t rank,
                          int64_t rows_padded, int64_t *row_ptr_out, int32_t *col_out,
                          float *val_out, gsp_stream stream);
-
-/* ---------------------------------------------------------------------------
- * Measurement helper (not part of the method): one launch that streams
- * `bytes` of device memory `iters` times through L2 (ld.global.cg), used by
- * bench.py to measure the L2 read ceiling live.  sink: device fp32
- * [8 * SM count], never read. */
-gsp_status gsp_probe_l2_read(const void *buf, size_t bytes, int32_t iters, float *sink, gsp_stream stream);
 
 /* ---------------------------------------------------------------------------
  * Misc. */

@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("GSP_LIB") or os.path.join(_HERE, "libgsp.so")
 
 GSP_OK = 0
 GSP_UNDIRECTED = 1
+GSP_VALIDATE = 2
 GSP_I32, GSP_I64 = 0, 1
 STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "GSP_ERR_NEGATIVE_WEIGHT",
           4: "GSP_ERR_NONFINITE", 5: "GSP_ERR_ALIAS", 6: "GSP_ERR_WORKSPACE", 7: "GSP_ERR_UNSUPPORTED",
@@ -32,7 +33,8 @@ STATUS = {0: "GSP_OK", 1: "GSP_ERR_INVALID_ARG", 2: "GSP_ERR_INDEX_RANGE", 3: "G
 EXPORTS = ("gsp_coo_to_csr_workspace", "gsp_coo_to_csr", "gsp_sym_normalize", "gsp_spmm", "gsp_spmm_f16", "gsp_spmm_ex",
            "gsp_edge_softmax", "gsp_multihead_spmm", "gsp_attn_project", "gsp_gat_workspace", "gsp_gat_aggregate",
            "gsp_partition_rows", "gsp_csr_slice", "gsp_status_string", "gsp_last_error_detail", "gsp_version",
-           "gsp_spmm_plan_info", "gsp_gspmm", "gsp_probe_l2_read", "gsp_spmm_accumulate",
+           "gsp_spmm_plan_info", "gsp_gspmm", "gsp_spmm_accumulate", "gsp_set_flags", "gsp_get_flags",
+           "gsp_sym_normalize_workspace",
            "gsp_propagate_workspace", "gsp_propagate", "gsp_csr_transpose_workspace", "gsp_csr_transpose",
            "gsp_sddmm", "gsp_edge_softmax_backward", "gsp_gat_backward_workspace", "gsp_gat_aggregate_backward",
            "gsp_attn_project_backward_workspace", "gsp_attn_project_backward", "gsp_linear_workspace", "gsp_linear",
@@ -73,12 +75,12 @@ def lib() -> ctypes.CDLL:
                                          ctypes.POINTER(ctypes.c_int64)],
             "gsp_coo_to_csr": [I, I, P, P, ctypes.c_int, P, ctypes.c_uint32, F, P, P, P,
                                ctypes.POINTER(ctypes.c_int64), P, ctypes.c_size_t, P],
-            "gsp_sym_normalize": [CP, P, P, P],
+            "gsp_sym_normalize": [CP, P, P, P, ctypes.c_size_t, P],
+            "gsp_sym_normalize_workspace": [CP, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_spmm": [CP, P, I, I, P, I, P],
             "gsp_spmm_f16": [CP, P, I, I, P, I, P],
             "gsp_spmm_ex": [CP, P, I, I, P, I, ctypes.POINTER(gsp_spmm_opts), P],
             "gsp_gspmm": [CP, ctypes.c_int, P, I, I, P, I, P],
-            "gsp_probe_l2_read": [P, ctypes.c_size_t, I32, P, P],
             "gsp_spmm_accumulate": [CP, P, I, I, P, I, P, I, F, P, I, F, P],
             "gsp_propagate_workspace": [CP, I, I, ctypes.POINTER(ctypes.c_size_t)],
             "gsp_propagate": [CP, P, I, I, I, P, P, I, P, ctypes.c_size_t, P],
@@ -114,6 +116,10 @@ def lib() -> ctypes.CDLL:
         L.gsp_status_string.restype = ctypes.c_char_p
         L.gsp_last_error_detail.argtypes = []
         L.gsp_last_error_detail.restype = ctypes.c_char_p
+        L.gsp_set_flags.argtypes = [ctypes.c_uint32]
+        L.gsp_set_flags.restype = ctypes.c_int
+        L.gsp_get_flags.argtypes = []
+        L.gsp_get_flags.restype = ctypes.c_uint32
         L.gsp_version.argtypes = []
         L.gsp_version.restype = ctypes.c_int
         _lib = L
@@ -155,6 +161,22 @@ def _mat(t: torch.Tensor, name: str):
     return t, ld
 
 
+def _rows(t: torch.Tensor, n: int, name: str):
+    """The C ABI cannot see tensor extents: catch caller shape mistakes here."""
+    if t.shape[0] < n:
+        raise ValueError(f"{name} has {t.shape[0]} rows, needs >= {n}")
+
+
+def _numel(t: torch.Tensor, n: int, name: str):
+    if t.numel() < n:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {n}")
+
+
+def _width(t: torch.Tensor, f: int, name: str):
+    if t.dim() != 2 or t.shape[1] < f:
+        raise ValueError(f"{name} must be 2-D with >= {f} columns, got {tuple(t.shape)}")
+
+
 class CSR:
     """Device CSR held in torch tensors; .view() is the borrowed gsp_csr."""
 
@@ -191,6 +213,8 @@ def gsp_coo_to_csr(n: int, src: torch.Tensor, dst: torch.Tensor, w: Optional[tor
     if w is not None:
         _vec(w, torch.float32, "w")
     m = src.numel()
+    if dst.numel() != m or (w is not None and w.numel() != m):
+        raise ValueError("src, dst (and w) must have the same length")
     flags = GSP_UNDIRECTED if undirected else 0
     wsb = ctypes.c_size_t(0)
     nmax = ctypes.c_int64(0)
@@ -211,16 +235,35 @@ def gsp_coo_to_csr(n: int, src: torch.Tensor, dst: torch.Tensor, w: Optional[tor
     return CSR(row_ptr, col[:k], val[:k], n)
 
 
-def gsp_sym_normalize(a: CSR, in_place: bool = False, stream=None) -> CSR:
+def gsp_sym_normalize(a: CSR, in_place: bool = False, keep_deg: bool = True, stream=None) -> CSR:
     """A^ = D~^-1/2 A~ D~^-1/2 (gsp.h a2).  Returns a CSR sharing the structure,
-    with the normalised values and the fp64 degrees in .deg."""
+    with the normalised values and (keep_deg) the fp64 degrees in .deg; with
+    keep_deg=False the degrees live in a workspace only (deg_out = NULL)."""
     if a.val is None:
         raise ValueError("gsp_sym_normalize needs A~ values")
     out = a.val if in_place else torch.empty_like(a.val)
-    deg = torch.empty(max(a.n_rows, 1), dtype=torch.float64, device=a.row_ptr.device)
     v = a.view()
-    _check(lib().gsp_sym_normalize(ctypes.byref(v), _ptr(out), _ptr(deg), _stream(stream)), "gsp_sym_normalize")
-    return CSR(a.row_ptr, a.col, out, a.n_cols, deg[:a.n_rows])
+    if keep_deg:
+        deg = torch.empty(max(a.n_rows, 1), dtype=torch.float64, device=a.row_ptr.device)
+        _check(lib().gsp_sym_normalize(ctypes.byref(v), _ptr(out), _ptr(deg), None, 0, _stream(stream)),
+               "gsp_sym_normalize")
+        return CSR(a.row_ptr, a.col, out, a.n_cols, deg[:a.n_rows])
+    nb = ctypes.c_size_t(0)
+    _check(lib().gsp_sym_normalize_workspace(ctypes.byref(v), ctypes.byref(nb)), "gsp_sym_normalize_workspace")
+    ws = torch.empty(max(nb.value // 8, 1), dtype=torch.float64, device=a.row_ptr.device)
+    _check(lib().gsp_sym_normalize(ctypes.byref(v), _ptr(out), None, _ptr(ws), nb.value, _stream(stream)),
+           "gsp_sym_normalize")
+    return CSR(a.row_ptr, a.col, out, a.n_cols, None)
+
+
+def gsp_set_flags(flags: int) -> None:
+    """Thread-local library flags (gsp.h): GSP_VALIDATE checks logits / el / er
+    for NaN / Inf before compute (GSP_ERR_NONFINITE)."""
+    _check(lib().gsp_set_flags(int(flags)), "gsp_set_flags")
+
+
+def gsp_get_flags() -> int:
+    return int(lib().gsp_get_flags())
 
 
 # ---------------------------------------------------------------------------
@@ -235,6 +278,7 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
     if y is None:
         y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
     y, ldy = _mat(y, "y")
+    _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
     if slab_cols or block_nnz:
         o = gsp_spmm_opts(slab_cols, block_nnz)
@@ -259,6 +303,7 @@ def gsp_spmm_f16(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[t
     if y is None:
         y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
     y, ldy = _mat(y, "y")
+    _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
     _check(lib().gsp_spmm_f16(ctypes.byref(v), _ptr(x), f, x.stride(0), _ptr(y), ldy, _stream(stream)), "gsp_spmm_f16")
     return y
@@ -272,6 +317,7 @@ def gsp_gspmm(a: CSR, x: torch.Tensor, reduce: str = "sum", f: Optional[int] = N
     if y is None:
         y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
     y, ldy = _mat(y, "y")
+    _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
     _check(lib().gsp_gspmm(ctypes.byref(v), REDUCE[reduce], _ptr(x), f, ldx, _ptr(y), ldy, _stream(stream)),
            "gsp_gspmm")
@@ -301,6 +347,7 @@ def gsp_edge_softmax(a: CSR, logits: torch.Tensor, heads: int, alpha: Optional[t
     if alpha is None:
         alpha = torch.empty_like(logits)
     _vec(alpha, torch.float32, "alpha")
+    _numel(logits, a.nnz * heads, "logits"), _numel(alpha, a.nnz * heads, "alpha")
     v = a.view()
     _check(lib().gsp_edge_softmax(ctypes.byref(v), heads, _ptr(logits), _ptr(alpha), _stream(stream)),
            "gsp_edge_softmax")
@@ -315,6 +362,8 @@ def gsp_multihead_spmm(a: CSR, alpha: torch.Tensor, z: torch.Tensor, heads: int,
     if y is None:
         y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device)
     y, ldy = _mat(y, "y")
+    _numel(alpha, a.nnz * heads, "alpha"), _rows(z, a.n_cols, "z"), _rows(y, a.n_rows, "y")
+    _width(z, heads * d, "z"), _width(y, heads * d, "y")
     v = a.view()
     _check(lib().gsp_multihead_spmm(ctypes.byref(v), heads, _ptr(alpha), _ptr(z), d, ldz, _ptr(y), ldy,
                                     _stream(stream)), "gsp_multihead_spmm")
@@ -330,6 +379,8 @@ def gsp_attn_project(z: torch.Tensor, a_l: torch.Tensor, a_r: torch.Tensor, head
     _vec(a_r, torch.float32, "a_r")
     el = torch.empty((n, heads), dtype=torch.float32, device=z.device) if el is None else el
     er = torch.empty((n, heads), dtype=torch.float32, device=z.device) if er is None else er
+    _width(z, heads * d, "z"), _numel(a_l, heads * d, "a_l"), _numel(a_r, heads * d, "a_r")
+    _numel(el, n * heads, "el"), _numel(er, n * heads, "er")
     _check(lib().gsp_attn_project(n, heads, d, _ptr(z), ldz, _ptr(a_l), _ptr(a_r), _ptr(el), _ptr(er),
                                   _stream(stream)), "gsp_attn_project")
     return el, er
@@ -365,6 +416,10 @@ def gsp_gat_aggregate(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tenso
     want = alpha_out is not None
     if alpha_out is True:
         alpha_out = torch.empty((a.nnz, heads), dtype=torch.float32, device=z.device)
+    _numel(el, a.n_rows * heads, "el"), _numel(er, a.n_cols * heads, "er"), _rows(z, a.n_cols, "z")
+    _rows(y, a.n_rows, "y"), _width(z, heads * d, "z"), _width(y, heads * d, "y")
+    if want:
+        _numel(alpha_out, a.nnz * heads, "alpha_out")
     ws = None if single_launch else _gat_ws(a, heads, z.device, ws)
     v = a.view()
     _check(lib().gsp_gat_aggregate(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope), _ptr(z), d,
@@ -592,6 +647,10 @@ def gsp_gat_aggregate_bias_act(a: CSR, el: torch.Tensor, er: torch.Tensor, z: to
     z, ldz = _mat(z, "z")
     y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device) if y is None else y
     y, ldy = _mat(y, "y")
+    _numel(el, a.n_rows * heads, "el"), _numel(er, a.n_cols * heads, "er"), _rows(z, a.n_cols, "z")
+    _rows(y, a.n_rows, "y"), _width(z, heads * d, "z"), _width(y, heads * d, "y")
+    if bias is not None:
+        _numel(bias, heads * d, "bias")
     ws = None if single_launch else _gat_ws(a, heads, z.device, ws)
     v = a.view()
     _check(lib().gsp_gat_aggregate_bias_act(ctypes.byref(v), heads, _ptr(el), _ptr(er), float(negative_slope),
@@ -599,12 +658,6 @@ def gsp_gat_aggregate_bias_act(a: CSR, el: torch.Tensor, er: torch.Tensor, z: to
                                             0 if ws is None else ws.numel(), _stream(stream)),
            "gsp_gat_aggregate_bias_act")
     return y
-
-
-def gsp_probe_l2_read(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None):
-    """Measurement helper: stream buf (L2-resident size) iters times."""
-    _check(lib().gsp_probe_l2_read(_ptr(buf), buf.numel() * buf.element_size(), iters, _ptr(sink), _stream(stream)),
-           "gsp_probe_l2_read")
 
 
 def version() -> int:

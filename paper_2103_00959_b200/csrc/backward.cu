@@ -603,6 +603,12 @@ extern "C" gsp_status gsp_gat_aggregate_backward(const gsp_csr *a, const gsp_csr
   gsp_gat_backward_workspace(a, heads, &need);
   if (!ws || ws_bytes < need) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, need);
   cudaStream_t s = cs(stream);
+  if (validate_mode()) {  // the score inputs el / er must be finite
+    const float *arr[2] = {el, er};
+    const int64_t cnt[2] = {a->n_rows * heads, a->n_cols * heads};
+    const char *nm[2] = {"el", "er"};
+    if ((st = check_finite(s, fn, 2, arr, cnt, nm))) return st;
+  }
   float *alpha = reinterpret_cast<float *>(ws);
   float *g = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + a256((size_t)std::max<int64_t>(a->nnz, 1) *
                                                                                  heads * 4));
@@ -638,7 +644,7 @@ extern "C" gsp_status gsp_gat_aggregate_backward(const gsp_csr *a, const gsp_csr
   p.head_dim = d;
   p.y_vec_ok = engine_y_vec_ok(L, dz, lddz);
   engine_stage(p, L, at->nnz, at->col_idx, nullptr);
-  p.hpt = engine_hpt(L, d);
+  p.hpt = engine_hpt(L, d, heads);
   if ((st = engine_ldxv(p, L, at->n_cols, lddy))) return st;
   return engine_launch(L, p, WeightAlphaPerm{alpha, perm, heads}, s);
 }

@@ -561,25 +561,41 @@ extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, cons
   return GSP_OK;
 }
 
-extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, gsp_stream stream) {
+extern "C" gsp_status gsp_sym_normalize_workspace(const gsp_csr *a, size_t *ws_bytes) {
+  clear_detail();
+  if (!a || !ws_bytes || a->n_rows < 0) return fail(GSP_ERR_INVALID_ARG, "gsp_sym_normalize_workspace: bad argument");
+  *ws_bytes = (size_t)a->n_rows * sizeof(double);
+  return GSP_OK;
+}
+
+extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double *deg_out, void *ws, size_t ws_bytes,
+                                        gsp_stream stream) {
   const char *fn = "gsp_sym_normalize";
   clear_detail();
   gsp_status st = check_csr(a, true, fn);
   if (st) return st;
   if (a->n_rows != a->n_cols) return fail(GSP_ERR_INVALID_ARG, "%s: matrix must be square", fn);
   if (a->n_rows == 0) return GSP_OK;
-  if (!deg_out) return fail(GSP_ERR_INVALID_ARG, "%s: deg_out is required (fp64 [n_rows])", fn);
   if (a->nnz > 0 && !val_out) return fail(GSP_ERR_INVALID_ARG, "%s: val_out is NULL", fn);
   if (val_out && val_out != a->val && overlaps(val_out, (size_t)a->nnz * 4, a->val, (size_t)a->nnz * 4))
     return fail(GSP_ERR_ALIAS, "%s: val_out partially overlaps val", fn);
+  double *d = deg_out;
+  if (!d) {  // the degrees go to the caller's workspace (the library never allocates)
+    if (!ws || ws_bytes < (size_t)a->n_rows * sizeof(double) || !aligned8(ws))
+      return fail(GSP_ERR_WORKSPACE, "%s: deg_out is NULL: an 8-byte aligned workspace of %zu bytes is required", fn,
+                  (size_t)a->n_rows * sizeof(double));
+    d = static_cast<double *>(ws);
+  }
+  if (val_out && overlaps(val_out, (size_t)a->nnz * 4, d, (size_t)a->n_rows * 8))
+    return fail(GSP_ERR_ALIAS, "%s: val_out overlaps the degree array", fn);
   cudaStream_t s = cs(stream);
   const unsigned gb = (unsigned)ceil_div(a->n_rows, 8);
-  degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, deg_out);
+  degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, d);
   if ((st = check_launch("degree"))) return st;
   if (a->nnz == 0) return GSP_OK;
   normalize_kernel<<<(unsigned)ceil_div(a->n_rows, 8), 256, 0, s>>>(a->row_ptr, a->col_idx, a->val, a->n_rows,
-                                                                   deg_out, val_out);
+                                                                   d, val_out);
   normalize_long_kernel<<<(unsigned)ceil_div(a->nnz, 8 * kNormChunk), 256, 0, s>>>(
-      a->row_ptr, a->col_idx, a->val, a->n_rows, a->nnz, deg_out, val_out);
+      a->row_ptr, a->col_idx, a->val, a->n_rows, a->nnz, d, val_out);
   return check_launch("normalize");
 }

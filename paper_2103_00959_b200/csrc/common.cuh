@@ -40,6 +40,12 @@ inline bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes)
 
 gsp_status check_csr(const gsp_csr *a, bool need_val, const char *fn);
 
+// GSP_VALIDATE mode of the calling thread (validate.cu) and the finite check
+// of logit-like inputs it enables
+bool validate_mode();
+gsp_status check_finite(cudaStream_t s, const char *fn, int narr, const float *const *arr, const int64_t *count,
+                        const char *const *name);
+
 // Device-side helpers --------------------------------------------------------
 
 // Warp-cooperative lower_bound: first r in [0, n) with rp[r] >= t, or n.

@@ -465,6 +465,12 @@ extern "C" gsp_status gsp_edge_softmax(const gsp_csr *a, int32_t heads, const fl
   const size_t bytes = (size_t)a->nnz * heads * 4;
   if (logits != alpha && overlaps(logits, bytes, alpha, bytes))
     return fail(GSP_ERR_ALIAS, "%s: logits and alpha partially overlap", fn);
+  if (validate_mode()) {
+    const float *arr[1] = {logits};
+    const int64_t cnt[1] = {a->nnz * heads};
+    const char *nm[1] = {"logits"};
+    if ((st = check_finite(cs(stream), fn, 1, arr, cnt, nm))) return st;
+  }
   return launch_stats<false, true>(a, nullptr, nullptr, logits, 0.0, heads, nullptr, alpha, cs(stream));
 }
 
@@ -516,6 +522,12 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   const size_t zb = a->n_cols ? (size_t)((a->n_cols - 1) * ldz + f) * 4 : 0;
   const size_t yb = (size_t)((a->n_rows - 1) * ldy + f) * 4;
   if (overlaps(z, zb, y, yb)) return fail(GSP_ERR_ALIAS, "%s: z and y overlap", fn);
+  if (validate_mode()) {  // the score inputs el / er must be finite
+    const float *arr[2] = {el, er};
+    const int64_t cnt[2] = {a->n_rows * heads, a->n_cols * heads};
+    const char *nm[2] = {"el", "er"};
+    if ((st = check_finite(s, fn, 2, arr, cnt, nm))) return st;
+  }
   int vmax = 1;
   if (ldz % 4 == 0 && aligned16(z)) vmax = 4;
   else if (ldz % 2 == 0 && aligned8(z)) vmax = 2;
@@ -542,7 +554,7 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   p.head_dim = d;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
-  p.hpt = engine_hpt(L, d);
+  p.hpt = engine_hpt(L, d, heads);
   p.bias = bias;
   p.act = act;
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;

@@ -80,9 +80,20 @@ extern "C" gsp_status gsp_gcn_layer(const gsp_csr *a, const float *x, int64_t f_
   clear_detail();
   gsp_status st = check_csr(a, false, fn);
   if (st) return st;
+  // every argument is checked before the first enqueue (gsp.h: nothing is
+  // touched on a host-detected error)
+  if (act < GSP_ACT_NONE || act > GSP_ACT_ELU) return fail(GSP_ERR_INVALID_ARG, "%s: bad activation", fn);
+  if (f_in < 0 || f_out < 0 || ldx < f_in || ldy < f_out) return fail(GSP_ERR_INVALID_ARG, "%s: bad sizes", fn);
+  if (a->n_rows == 0 || f_out == 0) return GSP_OK;
+  if (!y || !w || (a->n_cols > 0 && !x)) return fail(GSP_ERR_INVALID_ARG, "%s: null pointer", fn);
+  if (a->n_cols >= (int64_t(1) << 31) || f_in >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "%s: too large", fn);
   size_t need = 0;
   gsp_gcn_layer_workspace(a->n_cols, f_in, f_out, &need);
   if (!ws || ws_bytes < need) return fail(GSP_ERR_WORKSPACE, "%s: workspace needs %zu bytes", fn, need);
+  const size_t yb = (size_t)((a->n_rows - 1) * ldy + f_out) * 4;
+  if (overlaps(y, yb, ws, ws_bytes)) return fail(GSP_ERR_ALIAS, "%s: y overlaps the workspace", fn);
+  if (a->n_cols > 0 && (overlaps(x, (size_t)((a->n_cols - 1) * ldx + f_in) * 4, ws, ws_bytes)))
+    return fail(GSP_ERR_ALIAS, "%s: x overlaps the workspace", fn);
   float *h = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
   const int64_t ldh = (f_out + 3) / 4 * 4;
   const size_t hb = (size_t)a->n_cols * ldh * 4;

@@ -94,6 +94,10 @@ static gsp_status spmm_plan(const gsp_csr *a, const float *x, int64_t f, int64_t
   if (ldx % 4 == 0 && aligned16(x)) vmax = 4;
   else if (ldx % 2 == 0 && aligned8(x)) vmax = 2;
   const int32_t slab_req = opts ? opts->slab_cols : 0, block_req = opts ? opts->block_nnz : 0;
+  // 256-column slabs read two float4 per lane (32 bytes): the last vector of a
+  // row must stay inside [0, ldx), so ldx % 8 == 0 and a 32-byte aligned base
+  if (slab_req == 256 && vmax == 4 && !(ldx % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 32 == 0))
+    return fail(GSP_ERR_INVALID_ARG, "slab_cols 256 needs ldx %% 8 == 0 and a 32-byte aligned x");
   gsp_status st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, 0, vmax, slab_req, block_req, &P->main, 1);
   if (st) return st;
   P->f_main = f;
@@ -437,7 +441,7 @@ extern "C" gsp_status gsp_multihead_spmm(const gsp_csr *a, int32_t heads, const 
   p.head_dim = d;
   p.y_vec_ok = engine_y_vec_ok(L, y, ldy);
   engine_stage(p, L, a->nnz, a->col_idx, nullptr);
-  p.hpt = engine_hpt(L, d);
+  p.hpt = engine_hpt(L, d, heads);
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
   return engine_launch(L, p, WeightAlpha{alpha, heads}, cs(stream));
 }

@@ -923,9 +923,16 @@ gsp_status engine_plan(int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t f, i
 gsp_status launch_row_softmax_scores(const gsp_csr *a, const float *el, const float *er, double slope, int H,
                                      float *alpha, cudaStream_t s);
 
-// heads per team for a multi-head launch planned with slab L.slab_cols
-inline int engine_hpt(const EngineLaunch &L, int64_t head_dim) {
-  return (head_dim > 0 && L.slab_cols > head_dim) ? (int)(L.slab_cols / head_dim) : 1;
+// heads per team for a multi-head launch planned with slab L.slab_cols.  A
+// team holds hpt > 1 heads only when the slab is exactly hpt whole heads of
+// whole lanes (engine_plan's multi-head plan); a single head (whose plan is
+// the plain one, possibly wider than d) or a slab inside a head gives 1.
+inline int engine_hpt(const EngineLaunch &L, int64_t head_dim, int64_t heads) {
+  if (heads <= 1 || head_dim <= 0 || L.slab_cols <= head_dim) return 1;
+  if (L.slab_cols % head_dim || head_dim % L.V) return 1;
+  const int64_t hpt = L.slab_cols / head_dim;
+  if (hpt > heads || hpt > kMaxHpt || L.G % hpt) return 1;
+  return (int)hpt;
 }
 
 // y may take the V-wide (at most float4) stores

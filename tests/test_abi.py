@@ -46,7 +46,7 @@ def test_sm100a_cubin(L):
 
 
 def test_version_and_strings(L):
-    assert L.gsp_version() == 1
+    assert L.gsp_version() == 2
     assert L.gsp_status_string(0) == b"GSP_OK"
     assert L.gsp_status_string(5) == b"GSP_ERR_ALIAS"
 
@@ -80,7 +80,15 @@ def test_host_validation(L):
                                None, None, 0, s) == 1
     # normalize needs values
     c0 = _csr(val=None)
-    assert L.gsp_sym_normalize(ctypes.byref(c0), P(0x7000), P(0x8000), s) == 1
+    assert L.gsp_sym_normalize(ctypes.byref(c0), P(0x7000), P(0x8000), None, 0, s) == 1
+    # deg_out NULL: a workspace of n_rows doubles is required (nothing launched)
+    assert L.gsp_sym_normalize(ctypes.byref(c), P(0x7000), None, None, 0, s) == 6
+    assert L.gsp_sym_normalize(ctypes.byref(c), P(0x7000), None, P(0x8000), 79, s) == 6
+    assert L.gsp_sym_normalize(ctypes.byref(c), P(0x7000), None, P(0x8004), 80, s) == 6  # misaligned
+    # val_out overlapping the degree array
+    assert L.gsp_sym_normalize(ctypes.byref(c), P(0x7000), P(0x7010), None, 0, s) == 5
+    nb = ctypes.c_size_t(0)
+    assert L.gsp_sym_normalize_workspace(ctypes.byref(c), ctypes.byref(nb)) == 0 and nb.value == 80
     # partition parts out of range
     assert L.gsp_partition_rows(ctypes.byref(c), 0, P(0x7000), None, s) == 1
     # slice: bounds must span [0, n)
@@ -143,3 +151,69 @@ def test_product_does_not_import_oracle():
                 assert not pat.search(txt), f
     nm = subprocess.run(["nm", "-D", G.LIB_PATH], capture_output=True, text=True).stdout
     assert "orc_" not in nm
+
+
+def test_flags(L):
+    """gsp_set_flags: only GSP_VALIDATE is a known bit; the mode is per thread."""
+    import threading
+    assert L.gsp_get_flags() == 0
+    assert L.gsp_set_flags(4) == 1
+    assert L.gsp_set_flags(G.GSP_VALIDATE) == 0
+    assert L.gsp_get_flags() == G.GSP_VALIDATE
+    seen = []
+    t = threading.Thread(target=lambda: seen.append(L.gsp_get_flags()))
+    t.start()
+    t.join()
+    assert seen == [0]  # thread-local
+    assert L.gsp_set_flags(0) == 0 and L.gsp_get_flags() == 0
+
+
+def test_gcn_layer_validates_before_enqueue(L):
+    """gsp_gcn_layer checks act, sizes, pointers and y / x against the workspace
+    before its first enqueue (it used to memset the workspace first)."""
+    P = ctypes.c_void_p
+    s = P(0)
+    c = _csr(n_rows=10, n_cols=10, nnz=20)
+    n = ctypes.c_size_t(0)
+    assert L.gsp_gcn_layer_workspace(10, 8, 4, ctypes.byref(n)) == 0
+    ws = P(0x100000)
+    assert L.gsp_gcn_layer(ctypes.byref(c), P(0x10000), 8, 8, P(0x20000), 4, None, 7, P(0x90000), 4, ws, n.value,
+                           s) == 1  # bad activation
+    assert L.gsp_gcn_layer(ctypes.byref(c), P(0x10000), 8, 4, P(0x20000), 4, None, 1, P(0x90000), 4, ws, n.value,
+                           s) == 1  # ldx < f_in
+    assert L.gsp_gcn_layer(ctypes.byref(c), P(0x10000), 8, 8, None, 4, None, 1, P(0x90000), 4, ws, n.value,
+                           s) == 1  # NULL w
+    assert L.gsp_gcn_layer(ctypes.byref(c), P(0x10000), 8, 8, P(0x20000), 4, None, 1, P(0x100010), 4, ws, n.value,
+                           s) == 5  # y inside the workspace
+    assert L.gsp_gcn_layer(ctypes.byref(c), P(0x10000), 8, 8, P(0x20000), 4, None, 1, P(0x90000), 4, ws, 16,
+                           s) == 6  # workspace too small
+
+
+def test_spmm_ex_slab256_alignment(L):
+    """slab_cols 256 (two float4 per lane) is refused unless ldx % 8 == 0 and x
+    is 32-byte aligned (the last vector could read past the row)."""
+    P = ctypes.c_void_p
+    c = _csr()
+    o = G.gsp_spmm_opts(256, 0)
+    assert L.gsp_spmm_ex(ctypes.byref(c), P(0x10000), 260, 260, P(0x900000), 260, ctypes.byref(o), P(0)) == 1
+    assert L.gsp_spmm_ex(ctypes.byref(c), P(0x10010), 256, 264, P(0x900000), 256, ctypes.byref(o), P(0)) == 1
+    o2 = G.gsp_spmm_opts(256, 0)
+    launches, sc = ctypes.c_int32(0), ctypes.c_int32(0)
+    assert L.gsp_spmm_plan_info(ctypes.byref(c), P(0x10000), 300, 304, ctypes.byref(o2), ctypes.byref(launches),
+                                ctypes.byref(sc), None) == 0 and sc.value == 256
+
+
+def test_binding_shape_checks():
+    """The binding rejects shape mistakes the C ABI cannot see."""
+    import torch
+    rp = torch.zeros(4, dtype=torch.int64)
+    col = torch.zeros(0, dtype=torch.int32)
+    a = G.CSR.__new__(G.CSR)
+    a.row_ptr, a.col, a.val, a.n_rows, a.n_cols, a.nnz, a.deg = rp, col, None, 3, 5, 6, None
+    x = torch.zeros((4, 8))
+    with pytest.raises(ValueError):
+        G._rows(x, a.n_cols, "x")
+    with pytest.raises(ValueError):
+        G._numel(torch.zeros(5), a.nnz, "alpha")
+    with pytest.raises(ValueError):
+        G._width(x, 9, "x")

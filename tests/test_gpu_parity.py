@@ -623,3 +623,116 @@ def test_gat_inference_end_to_end_small(built):
     al = orc.edge_softmax(go.row_ptr, s, 1)
     yr, c = orc.multihead_spmm(go.row_ptr, go.col, al, host(z2), 1, 41)
     assert_within(out, orc.bias_act(yr, host(p.b2), "none"), c, what="gat output layer")
+
+
+# ---------------------------------------------------------------- single head, padded rows
+
+def _padded_view(a, ld):
+    t = torch.zeros((a.shape[0], ld), dtype=torch.float32, device=DEV)
+    t[:, :a.shape[1]] = dev(a)
+    return t[:, :a.shape[1]]
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_single_head_padded_z(built, D):
+    """H = 1 with d < 4 and ldz = 4: the plain plan's slab is wider than d, so a
+    team must still hold ONE head (engine_hpt caps at the head count).  Covers
+    multi-head SpMM, both GAT schedules and the aggregate backward."""
+    H = 1
+    for name in ("multi0", "cl4000", "hubs"):
+        go, gg, _, _ = built[name]
+        n = go.n
+        z = uniform((n, H * D), seed=3)
+        zt = _padded_view(z, 4)
+        alpha = uniform((go.nnz, H), seed=4, low=0, high=1)
+        yref, cond = orc.multihead_spmm(go.row_ptr, go.col, alpha.astype(np.float64), z, H, D)
+        assert_within(host(G.gsp_multihead_spmm(gg, dev(alpha), zt, H, D)), yref, cond, what=f"mh {name} D={D}")
+        el = uniform((n, H), seed=4, low=-3, high=3)
+        er = uniform((n, H), seed=5, low=-3, high=3)
+        yref, cond, aref = _gat_ref(go, el, er, z, H, D, 0.2)
+        for single in (False, True):
+            y, a = G.gsp_gat_aggregate(gg, dev(el), dev(er), zt, H, D, 0.2, alpha_out=True, single_launch=single)
+            assert_within(host(y), yref, cond, what=f"gat {name} D={D} single={single}")
+            assert np.all(np.abs(host(a) - aref) <= 1e-5 * aref + 1e-9), (name, D, single)
+        dy = uniform((n, H * D), seed=7)
+        at, perm = G.gsp_csr_transpose(gg)
+        dz, d_el, d_er = [host(t) for t in G.gsp_gat_aggregate_backward(gg, at, perm, dev(el), dev(er), zt,
+                                                                         _padded_view(dy, 4), H, D)]
+        dz_r, del_r, der_r, _ = orc.gat_backward(go.row_ptr, go.col, el, er, z, dy, H, D)
+        rp_t, ct, pm = orc.csr_transpose(go.row_ptr, go.col, n)
+        dz_c, _ = orc.multihead_spmm(rp_t, ct, aref[pm], np.abs(dy), H, D)
+        assert_within(dz, dz_r, dz_c, what=f"dz {name} D={D}")
+
+
+@pytest.mark.parametrize("classes", [1, 2])
+def test_gat_inference_few_classes(built, classes):
+    """gat_inference's output layer is one head of `classes` columns in a padded
+    buffer (ld 4): the case that used to form hpt > 1 for a single head."""
+    from paper_2103_00959_b200.inference import GATParams, gat_inference, _padded
+    go, gg, _, _ = built["cl4000"]
+    n = go.n
+    x = uniform((n, 50), seed=1)
+    p = GATParams.init(50, 64, 4, classes, DEV, seed=2)
+    out = host(gat_inference(gg, dev(x), p))
+    z1 = G.gsp_linear(dev(x), p.w1, y=_padded(n, 64, DEV))
+    el1, er1 = G.gsp_attn_project(z1, p.al1, p.ar1, 4, 16)
+    h1 = G.gsp_gat_aggregate_bias_act(gg, el1, er1, z1, 4, 16, p.b1, "elu", y=_padded(n, 64, DEV))
+    z2 = G.gsp_linear(h1, p.w2, y=_padded(n, classes, DEV))
+    el2, er2 = G.gsp_attn_project(z2, p.al2, p.ar2, 1, classes)
+    s = orc.gat_scores(go.row_ptr, go.col, host(el2), host(er2), 1)
+    al = orc.edge_softmax(go.row_ptr, s, 1)
+    yr, c = orc.multihead_spmm(go.row_ptr, go.col, al, host(z2), 1, classes)
+    assert_within(out, orc.bias_act(yr, host(p.b2), "none"), c, what=f"gat output layer classes={classes}")
+
+
+# ---------------------------------------------------------------- GSP_VALIDATE, nullable deg_out
+
+def test_validate_mode_rejects_nonfinite(built):
+    go, gg, _, _ = built["cl4000"]
+    H, D = 2, 8
+    n = go.n
+    z = dev(uniform((n, H * D), seed=3))
+    el = dev(uniform((n, H), seed=4, low=-3, high=3))
+    er = dev(uniform((n, H), seed=5, low=-3, high=3))
+    lg = dev(uniform((go.nnz, H), seed=6))
+    y0 = G.gsp_gat_aggregate(gg, el, er, z, H, D)
+    G.gsp_set_flags(G.GSP_VALIDATE)
+    try:
+        assert torch.equal(G.gsp_gat_aggregate(gg, el, er, z, H, D), y0)  # finite input: same result
+        a0 = G.gsp_edge_softmax(gg, lg, H)
+        for bad in (float("nan"), float("inf"), -float("inf")):
+            er2 = er.clone()
+            er2[n // 2, 1] = bad
+            y = torch.full((n, H * D), 7.0, device=DEV)
+            with pytest.raises(G.GspError) as e:
+                G.gsp_gat_aggregate(gg, el, er2, z, H, D, y=y)
+            assert e.value.status == 4 and "er" in str(e.value)
+            assert torch.all(y == 7.0)  # outputs untouched
+            lg2 = lg.clone()
+            lg2[go.nnz - 1, 0] = bad
+            with pytest.raises(G.GspError) as e:
+                G.gsp_edge_softmax(gg, lg2, H)
+            assert e.value.status == 4
+        el2 = el.clone()
+        el2[0, 0] = float("nan")
+        at, perm = G.gsp_csr_transpose(gg)
+        with pytest.raises(G.GspError):
+            G.gsp_gat_aggregate_backward(gg, at, perm, el2, er, z, z, H, D)
+        assert torch.equal(G.gsp_edge_softmax(gg, lg, H), a0)
+    finally:
+        G.gsp_set_flags(0)
+    # outside validate mode a NaN stays inside its row (A12)
+    lg2 = lg.clone()
+    r = 17
+    lg2[int(go.row_ptr[r]), 0] = float("nan")
+    a = host(G.gsp_edge_softmax(gg, lg2, H))
+    rows = np.repeat(np.arange(n), np.diff(go.row_ptr))
+    assert np.all(np.isnan(a[rows == r, 0])) and np.all(np.isfinite(a[rows != r]))
+
+
+def test_normalize_without_deg_out(built):
+    for name in ("isolated-nofill", "multi1", "cl4000", "star100k"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        g2 = G.gsp_sym_normalize(gg, keep_deg=False)
+        assert g2.deg is None
+        np.testing.assert_array_equal(host(g2.val).view(np.uint32), a32.view(np.uint32), err_msg=name)

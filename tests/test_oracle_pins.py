@@ -686,3 +686,92 @@ def test_gcn_layer_vs_dense_eq_gcn_layer():
     y2, _ = orc.gcn_layer(g2.row_ptr, g2.col, a2, np.array([[1.0], [0.0]], np.float32), np.array([[1.0]], np.float32),
                           None, "none")
     np.testing.assert_array_equal(y2, [[0.5], [0.5]])
+
+
+# ---------------------------------------------------------------------------
+# 12. tolerance scales (cond) -- every parity bound's scale is pinned against
+#     an independent dense |.| evaluation, so an indexing slip that inflates
+#     (or deflates) cond cannot silently change a parity bar
+# ---------------------------------------------------------------------------
+
+def _graph(n, m, seed, undirected=True):
+    s, d = chung_lu(n, m, seed=seed)
+    return orc.build_csr(n, s, d, None, undirected, 1.0)
+
+
+def test_cond_multihead_equals_dense_abs():
+    """orc_multihead_spmm's cond[u,h,:] == |A_h| @ |Z_h| per head (dense), with
+    signed alpha (so |.| placement matters) and a zero head."""
+    n = 400
+    g = _graph(n, 2500, seed=21)
+    for H, D in ((1, 3), (4, 6), (8, 2)):
+        z = uniform((n, H * D), seed=3)
+        alpha = uniform((g.nnz, H), seed=4, low=-1, high=1).astype(np.float64)
+        alpha[:, H // 2] = 0.0
+        _, cond = orc.multihead_spmm(g.row_ptr, g.col, alpha, z, H, D)
+        for h in range(H):
+            Ad = np.abs(g.dense(alpha[:, h]))
+            np.testing.assert_allclose(cond[:, h * D:(h + 1) * D], Ad @ np.abs(z[:, h * D:(h + 1) * D].astype(np.float64)),
+                                       rtol=1e-12, atol=0)
+        assert np.all(cond[:, (H // 2) * D:(H // 2 + 1) * D] == 0)
+        # row ranges give the same rows
+        _, c2 = orc.multihead_spmm(g.row_ptr, g.col, alpha, z, H, D, r0=100, r1=180)
+        np.testing.assert_array_equal(c2, cond[100:180])
+
+
+def test_cond_spmm_row_range_and_dense():
+    n = 300
+    g = _graph(n, 2000, seed=22)
+    _, a64, _ = orc.sym_norm(g)
+    x = uniform((n, 7), seed=5)
+    _, cond = orc.spmm(g.row_ptr, g.col, a64, x)
+    np.testing.assert_allclose(cond, np.abs(g.dense(a64)) @ np.abs(x.astype(np.float64)), rtol=1e-12, atol=0)
+    _, c2 = orc.spmm(g.row_ptr, g.col, a64, x, r0=37, r1=200)
+    np.testing.assert_array_equal(c2, cond[37:200])
+
+
+def test_cond_gcn_layer_equals_dense_abs():
+    """orc_gcn_layer's cond == |A^| (|X| |W|) + |b| (dense), before the activation."""
+    n = 250
+    g = _graph(n, 1200, seed=23)
+    _, a64, _ = orc.sym_norm(g)
+    x = uniform((n, 11), seed=7)
+    w = uniform((11, 6), seed=8)
+    b = uniform(6, seed=9)
+    ref = np.abs(g.dense(a64)) @ (np.abs(x.astype(np.float64)) @ np.abs(w.astype(np.float64))) + np.abs(b)
+    for act in ("none", "relu", "elu"):
+        _, cond = orc.gcn_layer(g.row_ptr, g.col, a64, x, w, b, act)
+        np.testing.assert_allclose(cond, ref, rtol=1e-12, atol=0)
+    _, c0 = orc.gcn_layer(g.row_ptr, g.col, a64, x, w, None, "relu")
+    np.testing.assert_allclose(c0, ref - np.abs(b), rtol=1e-12, atol=1e-15)
+
+
+def test_cond_attn_project_both_sides():
+    """el_cond and er_cond == einsum over |z| |a_l| and |z| |a_r| respectively."""
+    n, H, D = 200, 4, 5
+    z = uniform((n, H * D), seed=3)
+    al = uniform((H, D), seed=4)
+    ar = uniform((H, D), seed=5) * 3.0  # different scale: a swapped cond would fail
+    _, _, elc, erc = orc.attn_project(z, al, ar, H, D)
+    z3 = np.abs(z.reshape(n, H, D).astype(np.float64))
+    np.testing.assert_allclose(elc, np.einsum("nhd,hd->nh", z3, np.abs(al.astype(np.float64))), rtol=1e-12)
+    np.testing.assert_allclose(erc, np.einsum("nhd,hd->nh", z3, np.abs(ar.astype(np.float64))), rtol=1e-12)
+
+
+def test_cond_propagate_equals_matrix_power_of_abs():
+    """orc_propagate's cond == sum_k |theta_k| |A|^k |X| (dense matrix powers),
+    with signed thetas and signed weights."""
+    rng = np.random.default_rng(77)
+    for t in range(12):
+        n = int(rng.integers(2, 40))
+        m = int(rng.integers(1, 3 * n + 1))
+        g = orc.build_csr(n, rng.integers(0, n, m), rng.integers(0, n, m), None, bool(t % 2), 1.0)
+        _, a64, _ = orc.sym_norm(g)
+        a = a64 * np.where(rng.random(g.nnz) < 0.3, -1.0, 1.0)  # signed weights
+        A = np.abs(g.dense(a))
+        x = uniform((n, 3), seed=t)
+        K = int(rng.integers(1, 6))
+        th = uniform(K + 1, seed=80 + t).astype(np.float64)
+        _, cond = orc.propagate(g.row_ptr, g.col, a, x, th)
+        ref = sum(abs(th[k]) * np.linalg.matrix_power(A, k) @ np.abs(x.astype(np.float64)) for k in range(K + 1))
+        np.testing.assert_allclose(cond, ref, rtol=1e-12, atol=1e-300)
