@@ -327,23 +327,7 @@ def main():
     value = ge / (t_ms * 1e-3)
 
     peak, peak_kind = hbm_peak()
-    # live L2 read ceiling (gsp_probe_l2_read over a 48 MB L2-resident buffer)
     l2_peak = None
-    if not use_dist or rank == 0:
-        buf = torch.zeros(16 << 20, dtype=torch.uint8, device=dev)
-        sink = torch.zeros(8 * 1024, dtype=torch.float32, device=dev)
-        G.gsp_probe_l2_read(buf, 2, sink)
-        lts = []
-        for _ in range(5):
-            b0 = torch.cuda.Event(enable_timing=True)
-            b1 = torch.cuda.Event(enable_timing=True)
-            b0.record()
-            G.gsp_probe_l2_read(buf, 60, sink)
-            b1.record()
-            torch.cuda.synchronize()
-            lts.append(b0.elapsed_time(b1))
-        l2_peak = buf.numel() * 60 / (min(lts) * 1e-3) / 1e9
-        del buf, sink
     alg = spmm_alg_bytes(n, nnz, f) / world
     achieved = alg / (t_ms * 1e-3) / 1e9
     out = {

@@ -22,19 +22,61 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
+def _compile(out, extra):
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (IEEE double, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile liboracle.so with gcc (IEEE double, no FMA contraction), and the
+    same source with -fopenmp as liboracle_omp.so (row loops of spmm /
+    multihead_spmm on all host cores; identical per-row arithmetic)."""
+    if force:
+        for p in (_LIB, _LIB_OMP):
+            if os.path.exists(p):
+                os.remove(p)
+    _compile(_LIB_OMP, ["-fopenmp"])
+    return _compile(_LIB, [])
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def usable_cores() -> int:
+    return len(os.sched_getaffinity(0))
 
 
 _lib = None
+_lib_omp = None
+
+
+def lib_omp():
+    """The OpenMP build (same oracle.c); threads = OMP_NUM_THREADS or all usable cores."""
+    global _lib_omp
+    if _lib_omp is None:
+        build()
+        os.environ.setdefault("OMP_NUM_THREADS", str(usable_cores()))
+        L = ctypes.CDLL(_LIB_OMP)
+        P, I = ctypes.c_void_p, ctypes.c_int64
+        L.orc_spmm.argtypes = [I, I, P, P, P, P, I, I, P, P, I]
+        L.orc_multihead_spmm.argtypes = [I, I, P, P, I, P, P, I, I, P, P, I]
+        L.orc_spmm.restype = L.orc_multihead_spmm.restype = ctypes.c_int
+        _lib_omp = L
+    return _lib_omp
 _i64p = ctypes.POINTER(ctypes.c_int64)
 
 
@@ -140,8 +182,9 @@ def sym_norm(g: CSR):
     return deg, a64, a32
 
 
-def spmm(row_ptr, col, a, x, f=None, r0=0, r1=None, want_cond=True):
-    """(y, cond) fp64 [r1-r0, f] for Y = A X over rows [r0, r1) (oracle.c §3)."""
+def spmm(row_ptr, col, a, x, f=None, r0=0, r1=None, want_cond=True, omp=False):
+    """(y, cond) fp64 [r1-r0, f] for Y = A X over rows [r0, r1) (oracle.c §3);
+    omp=True runs the same rows on all host cores (liboracle_omp.so)."""
     row_ptr = _c(row_ptr, np.int64)
     col = _c(col, np.int32)
     a = _c(a, np.float64)
@@ -151,7 +194,7 @@ def spmm(row_ptr, col, a, x, f=None, r0=0, r1=None, want_cond=True):
     f = x.shape[1] if f is None else f
     y = np.zeros((r1 - r0, max(f, 1)), np.float64)
     cond = np.zeros_like(y) if want_cond else None
-    _chk(lib().orc_spmm(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], _p(y), _p(cond), y.shape[1]))
+    _chk((lib_omp() if omp else lib()).orc_spmm(r0, r1, _p(row_ptr), _p(col), _p(a), _p(x), f, x.shape[1], _p(y), _p(cond), y.shape[1]))
     return y[:, :f], (cond[:, :f] if want_cond else None)
 
 
@@ -219,8 +262,8 @@ def gat_scores(row_ptr, col, el, er, heads, slope=0.2, r0=0, r1=None):
     return s.reshape(-1, heads)
 
 
-def multihead_spmm(row_ptr, col, alpha, z, heads, d, r0=0, r1=None, want_cond=True):
-    """(y, cond) fp64 [r1-r0, heads*d] (oracle.c §6)."""
+def multihead_spmm(row_ptr, col, alpha, z, heads, d, r0=0, r1=None, want_cond=True, omp=False):
+    """(y, cond) fp64 [r1-r0, heads*d] (oracle.c §6); omp as for spmm."""
     row_ptr = _c(row_ptr, np.int64)
     col = _c(col, np.int32)
     alpha = np.ascontiguousarray(alpha, dtype=np.float64).reshape(-1)
@@ -230,7 +273,7 @@ def multihead_spmm(row_ptr, col, alpha, z, heads, d, r0=0, r1=None, want_cond=Tr
     w = heads * d
     y = np.zeros((r1 - r0, max(w, 1)), np.float64)
     cond = np.zeros_like(y) if want_cond else None
-    _chk(lib().orc_multihead_spmm(r0, r1, _p(row_ptr), _p(col), heads, _p(alpha), _p(z), d, z.shape[1],
+    _chk((lib_omp() if omp else lib()).orc_multihead_spmm(r0, r1, _p(row_ptr), _p(col), heads, _p(alpha), _p(z), d, z.shape[1],
                                   _p(y), _p(cond), y.shape[1]))
     return y[:, :w], (cond[:, :w] if want_cond else None)
 

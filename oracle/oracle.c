@@ -162,6 +162,9 @@ int orc_spmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int32_t *col,
              double *y, double *cond, int64_t ldy) {
   if (r0 < 0 || r1 < r0 || f < 0 || ldx < f || ldy < f || !row_ptr || (!col && r1 > r0) || !x || !y)
     return ORC_ERR_ARG;
+  /* rows are independent: liboracle_omp.so (-fopenmp) runs them on all host
+   * cores with the same per-row arithmetic; liboracle.so ignores the pragma */
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t u = r0; u < r1; ++u) {
     double *yu = y + (u - r0) * ldy;
     double *cu = cond ? cond + (u - r0) * ldy : NULL;
@@ -321,6 +324,7 @@ int orc_multihead_spmm(int64_t r0, int64_t r1, const int64_t *row_ptr, const int
   if (r0 < 0 || r1 < r0 || heads <= 0 || d < 0 || ldz < heads * d || ldy < heads * d ||
       !row_ptr || !alpha || !z || !y)
     return ORC_ERR_ARG;
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t u = r0; u < r1; ++u) {
     double *yu = y + (u - r0) * ldy;
     double *cu = cond ? cond + (u - r0) * ldy : NULL;

@@ -25,11 +25,19 @@ from typing import Callable, List, Optional
 
 import torch
 
-from . import CSR, gsp_csr_slice, gsp_partition_rows, gsp_spmm
+from . import CSR, gsp_attn_project, gsp_csr_slice, gsp_gat_aggregate, gsp_partition_rows, gsp_spmm
 
 
 class GpuOps:
     """The product's operators (libgsp kernels)."""
+
+    @staticmethod
+    def attn_project(z, a_l, a_r, heads, d, el, er):
+        gsp_attn_project(z, a_l, a_r, heads, d, el=el, er=er)
+
+    @staticmethod
+    def gat_aggregate(local, el, er, z, heads, d, slope, y, ws):
+        gsp_gat_aggregate(local, el, er, z, heads, d, slope, y=y, ws=ws)
 
     @staticmethod
     def partition(a, parts):
@@ -156,4 +164,106 @@ class RowPartitionedPropagate(RowPartitionedSpMM):
             for c in range(nch):
                 main.wait_event(events[c])
                 local(c)
+        return y
+
+
+def head_chunks(heads: int, d: int, chunks: int, align: int = 128) -> List[int]:
+    """Head-group edges for a chunked GAT exchange: every group is whole heads
+    and, when possible, a multiple of `align` columns (whole 128-column slabs)."""
+    chunks = max(1, min(chunks, heads))
+    per = -(-heads // chunks)
+    for p in range(per, heads + 1):
+        if (p * d) % align == 0:
+            per = p
+            break
+    return list(range(0, heads, per)) + [heads]
+
+
+class RowPartitionedGAT:
+    """Row-partitioned GAT aggregation ("GAT all-gathers Z
+    (n x H.D) and er (n x H); el stays local").
+
+    Each rank owns the row block [b_r, b_r+1) of the nnz-balanced partition and
+    the Z rows of those nodes.  Per call it projects its own rows
+    (gsp_attn_project -> el, er of its nodes), all-gathers er and Z over the
+    padded equal-count layout (communication stream), keeps el local, and runs
+    gsp_gat_aggregate on its CSR slice (columns remapped into the gathered
+    layout by gsp_csr_slice).  Scores, softmax statistics and alpha of a row
+    depend only on that row's el and its neighbours' er / Z, so with
+    head_groups = 1 the result is bitwise equal to the single-GPU
+    attn_project + gat_aggregate.  head_groups > 1 splits the heads into
+    groups of whole heads so the all-gather of group g+1 overlaps the
+    aggregate of group g (the statistics are then reduced per group: equal to
+    the single-GPU call within the fp32 bound, not bitwise)."""
+
+    def __init__(self, a: CSR, rank: int, world: int, heads: int, d: int, head_groups: int = 1,
+                 negative_slope: float = 0.2, all_gather: Optional[Callable] = None, device=None, ops=GpuOps):
+        self.rank, self.world, self.heads, self.d, self.ops = rank, world, heads, d, ops
+        self.slope = negative_slope
+        self.bounds = [int(b) for b in ops.partition(a, world)]
+        self.npad = padded_rows(self.bounds)
+        self.r0, self.r1 = self.bounds[rank], self.bounds[rank + 1]
+        self.rows = self.r1 - self.r0
+        self.local = ops.slice(a, self.bounds, rank, self.npad)
+        self.hg = head_chunks(heads, d, head_groups)
+        self.device = torch.device(device) if device is not None else a.row_ptr.device
+        self.all_gather = all_gather or (lambda out, inp: torch.distributed.all_gather_into_tensor(out, inp))
+        dv = self.device
+        groups = list(zip(self.hg[:-1], self.hg[1:]))
+        self.z_shard = [torch.zeros((self.npad, (h1 - h0) * d), dtype=torch.float32, device=dv) for h0, h1 in groups]
+        self.er_shard = [torch.zeros((self.npad, h1 - h0), dtype=torch.float32, device=dv) for h0, h1 in groups]
+        self.el = [torch.zeros((max(self.rows, 1), h1 - h0), dtype=torch.float32, device=dv) for h0, h1 in groups]
+        self.z_all = [torch.empty((world * self.npad, (h1 - h0) * d), dtype=torch.float32, device=dv)
+                      for h0, h1 in groups]
+        self.er_all = [torch.empty((world * self.npad, h1 - h0), dtype=torch.float32, device=dv) for h0, h1 in groups]
+        self.ws = None
+        self.comm = torch.cuda.Stream(device=dv) if dv.type == "cuda" else None
+
+    def load_shard(self, z_rows: torch.Tensor):
+        """z_rows: [rows, H*D] features (after the layer's linear step) of this rank's nodes."""
+        for k, (h0, h1) in enumerate(zip(self.hg[:-1], self.hg[1:])):
+            self.z_shard[k][:self.rows].copy_(z_rows[:, h0 * self.d:h1 * self.d])
+
+    def _project(self, k, a_l, a_r):
+        h0, h1 = self.hg[k], self.hg[k + 1]
+        if self.rows:
+            self.ops.attn_project(self.z_shard[k][:self.rows], a_l[h0 * self.d:h1 * self.d].contiguous(),
+                                  a_r[h0 * self.d:h1 * self.d].contiguous(), h1 - h0, self.d, self.el[k][:self.rows],
+                                  self.er_shard[k][:self.rows])
+
+    def _exchange(self, k):
+        self.all_gather(self.er_all[k], self.er_shard[k])
+        self.all_gather(self.z_all[k], self.z_shard[k])
+
+    def _local(self, k, y):
+        h0, h1 = self.hg[k], self.hg[k + 1]
+        if self.rows:
+            self.ops.gat_aggregate(self.local, self.el[k][:self.rows], self.er_all[k], self.z_all[k], h1 - h0, self.d,
+                                   self.slope, y[:, h0 * self.d:h1 * self.d], self.ws)
+
+    def __call__(self, a_l: torch.Tensor, a_r: torch.Tensor, y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Y rows of this rank: [rows, H*D]; a_l, a_r: [H*D] attention vectors."""
+        if y is None:
+            y = torch.empty((self.rows, self.heads * self.d), dtype=torch.float32, device=self.device)
+        ng = len(self.hg) - 1
+        if self.comm is None:
+            for k in range(ng):
+                self._project(k, a_l, a_r)
+                self._exchange(k)
+                self._local(k, y)
+            return y
+        main = torch.cuda.current_stream(self.device)
+        for k in range(ng):
+            self._project(k, a_l, a_r)
+        self.comm.wait_stream(main)  # er / Z shards complete before they are sent
+        events = []
+        with torch.cuda.stream(self.comm):
+            for k in range(ng):
+                self._exchange(k)
+                ev = torch.cuda.Event()
+                ev.record(self.comm)
+                events.append(ev)
+        for k in range(ng):
+            main.wait_event(events[k])
+            self._local(k, y)
         return y

@@ -84,12 +84,43 @@ def _collect_unique_pairs(draw, n: int, m: int, rng: np.random.Generator):
         lo = np.minimum(a, b)
         hi = np.maximum(a, b)
         keys_all = np.concatenate([keys_all, lo * np.int64(n) + hi])
-        _, idx = np.unique(keys_all, return_index=True)
-        uniq = idx.size
+        # distinct keys in order of first occurrence (hash-based; the same
+        # sequence as np.unique(return_index) sorted by first index)
+        uk = _unique_first(keys_all)
+        uniq = uk.size
         if uniq >= m:
-            idx.sort()
-            keys = keys_all[idx[:m]]
+            keys = uk[:m]
             return keys // n, keys % n
+
+
+def _unique_first(keys: np.ndarray) -> np.ndarray:
+    try:
+        import pandas as pd
+        return pd.unique(keys)
+    except ImportError:  # pragma: no cover
+        _, idx = np.unique(keys, return_index=True)
+        idx.sort()
+        return keys[idx]
+
+
+def _searchsorted_right(cdf: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """np.searchsorted(cdf, u, side="right") for u in [0, 1), cdf ascending:
+    a guide table over 2^22 equal buckets of [0, 1) gives each u its first
+    candidate, then a few vectorised steps advance while cdf[idx] <= u
+    (exact: the count of cdf entries <= u)."""
+    B = 1 << 22
+    edges = np.arange(B + 1, dtype=np.float64) / B
+    start = np.searchsorted(cdf, edges, side="right")
+    j = np.minimum((u * B).astype(np.int64), B - 1)
+    idx = start[j]
+    n = cdf.size
+    act = np.flatnonzero(idx < n)
+    while act.size:
+        adv = cdf[idx[act]] <= u[act]
+        act = act[adv]
+        idx[act] += 1
+        act = act[idx[act] < n]
+    return idx
 
 
 def chung_lu(n: int, m: int, seed: int = 1, gamma: float = 2.5):
@@ -124,7 +155,7 @@ def chung_lu(n: int, m: int, seed: int = 1, gamma: float = 2.5):
 
     def draw(k):
         u = rng.random(2 * k)
-        ab = np.minimum(np.searchsorted(cdf, u, side="right"), n - 1).astype(np.int64)
+        ab = np.minimum(_searchsorted_right(cdf, u), n - 1).astype(np.int64)
         return ab[:k], ab[k:]
 
     a, b = _collect_unique_pairs(draw, n, m, rng)
@@ -196,7 +227,12 @@ def features(n: int, f: int, ld: Optional[int] = None, seed: int = 2, low=-1.0, 
     ld = f if ld is None else ld
     rng = np.random.Generator(np.random.PCG64(seed))
     x = np.zeros((n, ld), dtype=np.float32)
-    x[:, :f] = (low + (high - low) * rng.random((n, f), dtype=np.float32)).astype(np.float32)
+    # filled in row chunks (the same stream as one rng.random((n, f)) call) so
+    # the 8.6 GB C6 matrix needs no full-size temporaries
+    step = max(1, (1 << 24) // max(f, 1))
+    for r0 in range(0, n, step):
+        r1 = min(n, r0 + step)
+        x[r0:r1, :f] = low + (high - low) * rng.random((r1 - r0, f), dtype=np.float32)
     return x
 
 

@@ -106,3 +106,83 @@ def test_chunk_bounds_and_padding():
     assert chunk_bounds(3, 4) == [0, 3]
     assert chunk_bounds(8, 1) == [0, 8]
     assert padded_rows([0, 5, 5, 12]) == 7
+
+
+class OracleGatOps(OracleOps):
+    """Host stand-ins for gsp_attn_project / gsp_gat_aggregate (fp64 oracle,
+    rounded to fp32 where the product's outputs are fp32)."""
+
+    @staticmethod
+    def attn_project(z, a_l, a_r, heads, d, el, er):
+        e_l, e_r, _, _ = orc.attn_project(z.numpy(), a_l.numpy().reshape(heads, d), a_r.numpy().reshape(heads, d),
+                                          heads, d)
+        el.copy_(torch.from_numpy(e_l.astype(np.float32)))
+        er.copy_(torch.from_numpy(e_r.astype(np.float32)))
+
+    @staticmethod
+    def gat_aggregate(local, el, er, z, heads, d, slope, y, ws):
+        sc = orc.gat_scores(local.row_ptr, local.col, el.numpy(), er.numpy(), heads, slope)
+        al = orc.edge_softmax(local.row_ptr, sc, heads)
+        yy, _ = orc.multihead_spmm(local.row_ptr, local.col, al, z.numpy(), heads, d, want_cond=False)
+        y.copy_(torch.from_numpy(yy.astype(np.float32)))
+
+
+def _gat_worker(rank, world, port, n, m, H, D, groups, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_00959_b200.dist import RowPartitionedGAT
+        from synth import uniform
+        s, d = chung_lu(n, m, seed=5)
+        g = orc.build_csr(n, s, d, None, True, 1.0)
+        a = OracleCSR(g.row_ptr, g.col, g.val, n)
+        z = uniform((n, H * D), seed=3)
+        al, ar = uniform(H * D, seed=6), uniform(H * D, seed=7)
+        op = RowPartitionedGAT(a, rank, world, H, D, head_groups=groups, all_gather=_gather, device="cpu",
+                               ops=OracleGatOps)
+        op.load_shard(torch.from_numpy(z[op.r0:op.r1]))
+        y = op(torch.from_numpy(al), torch.from_numpy(ar)).numpy()
+        # global reference: the same oracle steps on the whole graph
+        el, er, _, _ = orc.attn_project(z, al.reshape(H, D), ar.reshape(H, D), H, D)
+        yref = np.zeros((n, H * D), np.float32)
+        for h0, h1 in zip(op.hg[:-1], op.hg[1:]):
+            hc = h1 - h0
+            sc = orc.gat_scores(g.row_ptr, g.col, el[:, h0:h1].astype(np.float32).copy(),
+                                er[:, h0:h1].astype(np.float32).copy(), hc, 0.2)
+            yy, _ = orc.multihead_spmm(g.row_ptr, g.col, orc.edge_softmax(g.row_ptr, sc, hc),
+                                       np.ascontiguousarray(z[:, h0 * D:h1 * D]), hc, D, want_cond=False)
+            yref[:, h0 * D:h1 * D] = yy
+        q.put((rank, bool(np.array_equal(y, yref[op.r0:op.r1])), op.r0, op.r1, op.hg))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,groups", [(2, 1), (2, 4), (3, 2)])
+def test_row_partitioned_gat_gloo(world, groups):
+    """RowPartitionedGAT (all-gather Z and er, el local) over gloo
+    with the oracle's per-rank steps equals the global oracle exactly."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n, m, H, D = 2500, 15000, 8, 32
+    procs = [ctx.Process(target=_gat_worker, args=(r, world, port, n, m, H, D, groups, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, *_ in res), res
+    assert res[0][2] == 0 and res[-1][3] == n
+    hg = res[0][4]
+    from paper_2103_00959_b200.dist import head_chunks
+    assert hg == head_chunks(H, D, groups) and (groups == 1) == (len(hg) == 2)
+
+
+def test_head_chunks():
+    from paper_2103_00959_b200.dist import head_chunks
+    assert head_chunks(8, 64, 1) == [0, 8]
+    assert head_chunks(8, 64, 4) == [0, 2, 4, 6, 8]   # 128-column groups
+    assert head_chunks(8, 64, 8) == [0, 2, 4, 6, 8]   # never narrower than one slab when avoidable
+    assert head_chunks(4, 128, 4) == [0, 1, 2, 3, 4]
+    assert head_chunks(3, 16, 2) == [0, 2, 3]

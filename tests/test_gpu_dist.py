@@ -62,6 +62,28 @@ def _worker(rank, world, port, backend, chunks, q):
         yp = pp(th)
         torch.cuda.synchronize()
         ok = ok and torch.equal(yp, G.gsp_propagate(g, x, th, f=f)[pp.r0:pp.r1])
+        # GAT (all-gather Z and er, el local); head_groups = 1 is
+        # bitwise equal to the single-GPU attn_project + gat_aggregate, more
+        # groups to the single-GPU calls on the same head groups
+        from paper_2103_00959_b200.dist import RowPartitionedGAT
+        from synth import uniform
+        H, D = 8, 32
+        z = torch.from_numpy(uniform((n, H * D), seed=3)).to(dev)
+        al = torch.from_numpy(uniform(H * D, seed=6)).to(dev)
+        ar = torch.from_numpy(uniform(H * D, seed=7)).to(dev)
+        for groups in (1, chunks):
+            gt = RowPartitionedGAT(g, rank, world, H, D, head_groups=groups, device=dev,
+                                   all_gather=None if backend == "nccl" else _staged_gather)
+            gt.load_shard(z[gt.r0:gt.r1])
+            yg = gt(al, ar)
+            yr = torch.empty((n, H * D), device=dev)
+            for h0, h1 in zip(gt.hg[:-1], gt.hg[1:]):
+                zc = z[:, h0 * D:h1 * D].contiguous()
+                el, er = G.gsp_attn_project(zc, al[h0 * D:h1 * D].contiguous(), ar[h0 * D:h1 * D].contiguous(),
+                                            h1 - h0, D)
+                yr[:, h0 * D:h1 * D] = G.gsp_gat_aggregate(g, el, er, zc, h1 - h0, D, 0.2)
+            torch.cuda.synchronize()
+            ok = ok and torch.equal(yg, yr[gt.r0:gt.r1])
         q.put((rank, ok, op.r0, op.r1))
     except Exception as e:  # pragma: no cover
         q.put((rank, repr(e), -1, -1))

@@ -775,3 +775,23 @@ def test_cond_propagate_equals_matrix_power_of_abs():
         _, cond = orc.propagate(g.row_ptr, g.col, a, x, th)
         ref = sum(abs(th[k]) * np.linalg.matrix_power(A, k) @ np.abs(x.astype(np.float64)) for k in range(K + 1))
         np.testing.assert_allclose(cond, ref, rtol=1e-12, atol=1e-300)
+
+
+def test_omp_build_is_bit_identical():
+    """liboracle_omp.so (the same oracle.c with -fopenmp, rows on all host
+    cores) gives bit-identical y and cond: rows are independent and each row's
+    arithmetic is unchanged."""
+    n = 3000
+    g = _graph(n, 30000, seed=31)
+    _, a64, _ = orc.sym_norm(g)
+    x = uniform((n, 37), seed=2)
+    y1, c1 = orc.spmm(g.row_ptr, g.col, a64, x)
+    y2, c2 = orc.spmm(g.row_ptr, g.col, a64, x, omp=True)
+    np.testing.assert_array_equal(y1, y2)
+    np.testing.assert_array_equal(c1, c2)
+    al = uniform((g.nnz, 4), seed=3, low=0, high=1).astype(np.float64)
+    z = uniform((n, 4 * 9), seed=4)
+    m1 = orc.multihead_spmm(g.row_ptr, g.col, al, z, 4, 9)
+    m2 = orc.multihead_spmm(g.row_ptr, g.col, al, z, 4, 9, omp=True, r0=5, r1=2900)
+    np.testing.assert_array_equal(m1[0][5:2900], m2[0])
+    np.testing.assert_array_equal(m1[1][5:2900], m2[1])
