@@ -273,8 +273,9 @@ def run_reference(args):
             times.append(r["s"])
             ges.append(r["GE"])
     value = float(sum(ges) / sum(times))
-    sample = (f"each step: a contiguous row range of {cfg.name} with ~{args.ref_budget_ge / 1e9:.1f} G edge x "
-              f"feature units, fp64 oracle on {threads} threads ({orc.cpu_model()})")
+    sample = (f"each step: a contiguous row range of {cfg.name} with {np.mean(ges) / 1e9:.2f} G edge x feature "
+              f"units (of {cfg.nnz * cfg.f / 1e9:.2f} G per full SpMM), fp64 oracle on {threads} threads "
+              f"({orc.cpu_model()})")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GE/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
