@@ -470,6 +470,26 @@ def gat_rows(ctx, key, H, D, full_parity, budget_1t, budget_nt):
     par = {"max_err_over_bound": max(p_y, p_alpha), "y": p_y, "alpha": p_alpha, "checked": how,
            "csr_bit_exact": host["csr_bit_exact"]}
     par["pass"] = bool(par["max_err_over_bound"] <= 1.0 and par["csr_bit_exact"])
+    # standalone a6 (softmax of the given logits, every entry) and a7 (given alpha)
+    lg_h = logits.cpu().numpy()
+    G.gsp_edge_softmax(g, logits, H, alpha=alpha)
+    a6ref = orc.edge_softmax(go.row_ptr, lg_h.astype(np.float64), H)
+    p6 = float(np.max(np.abs(alpha.cpu().numpy() - a6ref) / (1e-5 * a6ref + 1e-9)))
+    par6 = {"max_err_over_bound": p6, "checked": "alpha on every entry", "pass": p6 <= 1.0}
+    a_h = alpha.cpu().numpy()
+    G.gsp_multihead_spmm(g, alpha, z, H, D, y=y)
+    y7 = y.cpu().numpy()
+    if full_parity:
+        y7r, c7 = orc.multihead_spmm(go.row_ptr, go.col, a_h.astype(np.float64), z_h, H, D, omp=True)
+        p7, how7 = err_ratio(y7, y7r, c7), "full output"
+        del y7r, c7
+    else:
+        p7 = 0.0
+        for r in rs:
+            yr, cr = orc.multihead_spmm(go.row_ptr, go.col, a_h.astype(np.float64), z_h, H, D, r0=int(r), r1=int(r) + 1)
+            p7 = max(p7, err_ratio(y7[r:r + 1], yr, cr))
+        how7 = f"{rs.size} sampled rows"
+    par7 = {"max_err_over_bound": p7, "checked": how7, "pass": p7 <= 1.0}
     legs = oracle_legs(lambda b, omp: oracle_mh_rate(go.row_ptr, go.col, aref, z_h, H, D, b, omp=omp),
                        budget_1t, budget_nt)
     ge = nnz * H * D
@@ -483,9 +503,10 @@ def gat_rows(ctx, key, H, D, full_parity, budget_1t, budget_nt):
                     "single_launch_schedule": tstats(t_g1),
                     "kernels": "row_stats_warp (softmax statistics, all heads) + engine_kernel<WeightGatT<1>>"}),
         report_row(ctx, cfg, "a6_edge_softmax", 1, t_sm, w_sm, None, softmax_bytes(n, nnz, H),
-                   {**common, "edge-heads/s": nnz * H / (float(np.median(t_sm)) * 1e-3), "launches": 1}),
+                   {**common, "edge-heads/s": nnz * H / (float(np.median(t_sm)) * 1e-3), "launches": 1,
+                    "parity": par6}),
         report_row(ctx, cfg, "a7_multihead_spmm", 1, t_mh, w_mh, ge, mh_bytes(n, nnz, H, D),
-                   {**common, "launches": 1}),
+                   {**common, "launches": 1, "parity": par7}),
     ]
     return rows, (cfg, g, el, er, z, y, ws, alpha, logits)
 

@@ -49,14 +49,25 @@ __device__ __forceinline__ double stat_score(float t, double el_u, double slope)
   return (double)t;
 }
 
-// entries [e0, e0 + cnt) of the CSR -> T[j][H] (er rows of their columns, or logits rows)
+// global -> shared asynchronous copies (LDGSTS): the data never passes through
+// registers, so a lane keeps many entries in flight at no register cost
+template <int B>
+__device__ __forceinline__ void cp_async(void *dst, const void *src) {
+  if constexpr (B == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// entries [e0, e0 + cnt) of the CSR -> T[j][H] (er rows of their columns, or
+// logits rows) by cp.async; the caller's __syncwarp after it publishes T
 template <int H, bool kScores>
 __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
                                           const float *__restrict__ er, const float *logits, int lane) {
   if (kScores) {
-    constexpr int kU = (32 / H) < 4 ? ((32 / H) < 1 ? 1 : 32 / H) : 4;  // entries per lane per round
-    constexpr int kV = H >= 4 ? 4 : H;                                 // floats per load
-    using VT = typename VecT<kV>::T;
+    constexpr int kV = H >= 4 ? 4 : H;  // floats per copy (er rows are 4 / 8 / 16-byte aligned, launch_stats)
+    constexpr int kU = 8;               // column indices in flight per lane
     for (int base = 0; base < cnt; base += 32 * kU) {
       int c[kU];
 #pragma unroll
@@ -64,52 +75,21 @@ __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const i
         const int j = base + lane + 32 * u;
         c[u] = j < cnt ? __ldg(col + e0 + j) : 0;
       }
-      float v[kU][H];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int j = base + lane + 32 * u;
-#pragma unroll
-        for (int q = 0; q < H; q += kV) {
-          if (j < cnt) {
-            float t[kV];
-            vld<kV>(t, reinterpret_cast<const VT *>(er + (int64_t)c[u] * H + q));
-#pragma unroll
-            for (int i = 0; i < kV; ++i) v[u][q + i] = t[i];
-          }
-        }
-      }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int j = base + lane + 32 * u;
         if (j < cnt) {
 #pragma unroll
-          for (int q = 0; q < H; q += kV) {
-            float t[kV];
-#pragma unroll
-            for (int i = 0; i < kV; ++i) t[i] = v[u][q + i];
-            Vec<kV>::st_shared(T + j * H + q, t);
-          }
+          for (int q = 0; q < H; q += kV) cp_async<kV * 4>(T + j * H + q, er + (int64_t)c[u] * H + q);
         }
       }
     }
   } else {
     const float *src = logits + e0 * H;  // cnt rows of H logits are contiguous
     const int nf = cnt * H;
-    constexpr int kU = 8;
-    for (int base = 0; base < nf; base += 32 * kU) {
-      float v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int k = base + lane + 32 * u;
-        v[u] = k < nf ? src[k] : 0.0f;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int k = base + lane + 32 * u;
-        if (k < nf) T[k] = v[u];
-      }
-    }
+    for (int k = lane; k < nf; k += 32) cp_async<4>(T + k, src + k);
   }
+  cp_async_wait_all();
 }
 
 // reduce one short row held in T[0 .. d) and write its statistics or alpha
@@ -153,6 +133,49 @@ __device__ __forceinline__ void stat_row(float *T, int64_t r, int64_t b, int d, 
   }
 }
 
+// rows of <= kTile entries: warp w owns rows 4w .. 4w+3 of the CTA (contiguous
+// in CSR, loaded into its tile in one sweep when they fit together)
+template <int H, bool kScores, bool kApply>
+__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
+                                                const int32_t *__restrict__ col, const float *__restrict__ el,
+                                                const float *__restrict__ er, const float *logits, double slope,
+                                                GatStat *__restrict__ st, float *alpha, int warp, int lane) {
+  constexpr int kTile = kStatTileFloats / H;
+  const int64_t r0 = rbase + warp * kStatRPW;
+  const int64_t B0 = s_rp[warp * kStatRPW], BN = s_rp[warp * kStatRPW + kStatRPW];
+  const bool together = BN - B0 <= kTile;
+  __syncwarp();
+  if (together) stat_load<H, kScores>(T, B0, (int)(BN - B0), col, er, logits, lane);
+  __syncwarp();
+  for (int k = 0; k < kStatRPW; ++k) {
+    const int64_t bk = s_rp[warp * kStatRPW + k], d = s_rp[warp * kStatRPW + k + 1] - bk;
+    if (d == 0 || d > kTile || r0 + k >= n_rows) continue;
+    float *Tk = T;
+    if (together) {
+      Tk = T + (bk - B0) * H;
+    } else {
+      __syncwarp();
+      stat_load<H, kScores>(T, bk, (int)d, col, er, logits, lane);
+      __syncwarp();
+    }
+    stat_row<H, kScores, kApply>(Tk, r0 + k, bk, (int)d, el, slope, st, alpha, lane);
+  }
+}
+
+// Long rows (> kTile entries) are cut into tile-sized chunks; warp w takes
+// chunks w, w + 8, ... and reduces them to a partial (m_w, s_w) with its OWN
+// maximum m_w (s_w = sum of exp(s - m_w), fp64).  The last warp to arrive
+// merges the 8 partials in warp order -- M = max m_w, S = sum_w s_w exp(m_w - M)
+// (fp64) -- so no warp ever waits at a CTA barrier for a long row: long rows
+// are processed first, the warps then continue with their short rows, and
+// only the alpha writes of a long row (kApply) wait for its merged (M, S).
+// Partials of up to kSlots long rows live in shared memory; a CTA with more
+// long rows processes them in batches separated by a CTA barrier.
+template <int H>
+struct StatSlots {
+  static constexpr int kSlots = (64 / H) < 16 ? (64 / H) : 16;  // <= 8 KB of partials (48 KB static smem)
+};
+
 template <int H, bool kScores, bool kApply>
 __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp(const int64_t *__restrict__ rp,
                                                                   const int32_t *__restrict__ col,
@@ -161,103 +184,148 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
                                                                   double slope, int64_t n_rows,
                                                                   GatStat *__restrict__ st, float *alpha) {
   constexpr int kTile = kStatTileFloats / H;
+  constexpr int kRows = kStatWarps * kStatRPW;  // rows per CTA
+  constexpr int kSlots = StatSlots<H>::kSlots;
+  constexpr int P = 32 / H;
   __shared__ __align__(16) float s_tile[kStatWarps][kStatTileFloats];
-  __shared__ int s_long[kStatWarps * kStatRPW];
+  __shared__ double s_pm[kSlots][kStatWarps][H];  // partial max (score) per slot, warp, head
+  __shared__ double s_ps[kSlots][kStatWarps][H];  // partial sum of exp(s - m_w)
+  __shared__ double s_M[kSlots][H];               // merged max (kApply)
+  __shared__ float s_inv[kSlots][H];              // merged 1 / S (kApply)
+  __shared__ int s_cnt[kSlots];
+  __shared__ volatile int s_done[kSlots];
+  __shared__ int64_t s_rp[kRows + 1];
+  __shared__ int s_long[kRows];
   __shared__ int s_nlong;
-  __shared__ double s_red[kStatWarps][H];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  if (tid == 0) s_nlong = 0;
-  __syncthreads();
-  const int64_t rbase = (int64_t)blockIdx.x * kStatWarps * kStatRPW;
-  {
-    float *T = s_tile[warp];
-    const int64_t r0 = rbase + warp * kStatRPW;
-    const int64_t bl = (lane <= kStatRPW) ? __ldg(rp + min(r0 + lane, n_rows)) : 0;
-    int64_t B[kStatRPW + 1];
-#pragma unroll
-    for (int k = 0; k <= kStatRPW; ++k) B[k] = __shfl_sync(0xffffffffu, bl, k);
-    const bool together = B[kStatRPW] - B[0] <= kTile;
-    if (together) stat_load<H, kScores>(T, B[0], (int)(B[kStatRPW] - B[0]), col, er, logits, lane);
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < kStatRPW; ++k) {
-      const int64_t d = B[k + 1] - B[k];
-      if (d == 0) continue;
-      if (d > kTile) {
-        if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp * kStatRPW + k;
-        continue;
-      }
-      float *Tk = T;
-      if (together) {
-        Tk = T + (B[k] - B[0]) * H;
-      } else {
-        __syncwarp();
-        stat_load<H, kScores>(T, B[k], (int)d, col, er, logits, lane);
-        __syncwarp();
-      }
-      stat_row<H, kScores, kApply>(Tk, r0 + k, B[k], (int)d, el, slope, st, alpha, lane);
-    }
+  const int h = lane % H, part = lane / H;
+  const int64_t rbase = (int64_t)blockIdx.x * kRows;
+  // the CTA's row pointers and its long rows, once (nobody is busy yet)
+  if (tid <= kRows) s_rp[tid] = __ldg(rp + min(rbase + tid, n_rows));
+  if (tid < kSlots) {
+    s_cnt[tid] = 0;
+    s_done[tid] = 0;
   }
   __syncthreads();
-  // long rows: the whole CTA; warp w takes tile-sized chunks w, w+8, ... of
-  // the row (same tile loads and lane layout as short rows), partials of the
-  // 8 warps combined in warp order
+  if (warp == 0) {
+    const bool lg = (s_rp[lane + 1] - s_rp[lane]) > kTile;
+    const unsigned bl = __ballot_sync(0xffffffffu, lg);
+    if (lg) s_long[__popc(bl & ((1u << lane) - 1u))] = lane;
+    if (lane == 0) s_nlong = __popc(bl);
+  }
+  __syncthreads();
   const int nlong = s_nlong;
   float *T = s_tile[warp];
-  constexpr int P = 32 / H;
-  const int h = lane % H, part = lane / H;
-  for (int k = 0; k < nlong; ++k) {
-    const int64_t r = rbase + s_long[k];
-    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-    const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-    const bool resident = (e1 - b) <= (int64_t)kStatWarps * kTile;  // one chunk per warp: no reloads
-    double m = -INFINITY, sum = 0.0;
-    for (int pass = 0; pass < (kApply ? 3 : 2); ++pass) {
-      const float inv_s = pass == 2 ? (float)(1.0 / sum) : 0.0f;
-      double acc = pass == 0 ? -INFINITY : 0.0;
+  // ---- 1. long rows: per-warp partials, merged by the last warp to arrive
+  for (int k0 = 0; k0 < nlong; k0 += kSlots) {
+    const int kn = min(kSlots, nlong - k0);
+    if (k0 > 0) {  // slots are reused: every merge of the previous batch is complete
+      __syncthreads();
+      if (tid < kSlots) {
+        s_cnt[tid] = 0;
+        s_done[tid] = 0;
+      }
+      __syncthreads();
+    }
+    for (int k = 0; k < kn; ++k) {
+      const int lr = s_long[k0 + k];
+      const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
+      const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
+      double m = -INFINITY, sum = 0.0;
       for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
         const int cnt = (int)min((int64_t)kTile, e1 - c0);
-        if (pass == 0 || !resident) {  // a row of <= 8 tiles keeps each warp's chunk in its tile
+        __syncwarp();
+        stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
+        __syncwarp();
+        float mr = -INFINITY;  // exact chunk max of the scores via the stored values (monotone, see stat_row)
+        for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
+#pragma unroll
+        for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+        double mc = stat_score<kScores>(mr, el_u, slope);
+        if (kScores && !(slope >= 0.0)) {
+          mc = -INFINITY;
+          for (int j = part; j < cnt; j += P) mc = fmax(mc, stat_score<kScores>(T[j * H + h], el_u, slope));
+#pragma unroll
+          for (int off = H; off < 32; off <<= 1) mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+        }
+        double sc = 0.0;
+        for (int j = part; j < cnt; j += P) sc += (double)expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - mc));
+#pragma unroll
+        for (int off = H; off < 32; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
+        // fold the chunk into the warp's partial (chunks in increasing order)
+        if (mc > m) {
+          sum = (m == -INFINITY) ? sc : sum * exp(m - mc) + sc;
+          m = mc;
+        } else if (mc != -INFINITY) {
+          sum += sc * exp(mc - m);
+        } else {
+          sum += sc;  // NaN propagates; empty chunks do not occur
+        }
+      }
+      if (part == 0) {
+        s_pm[k][warp][h] = m;
+        s_ps[k][warp][h] = sum;
+      }
+      __threadfence_block();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&s_cnt[k], 1) == kStatWarps - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {  // merge the 8 partials in warp order
+        __threadfence_block();
+        if (lane < H) {
+          double M = -INFINITY;
+          for (int w = 0; w < kStatWarps; ++w) M = fmax(M, s_pm[k][w][lane]);
+          double S = 0.0;
+          for (int w = 0; w < kStatWarps; ++w) {
+            const double mw = s_pm[k][w][lane];
+            if (mw != -INFINITY) S += s_ps[k][w][lane] * exp(mw - M);
+            else S += s_ps[k][w][lane];
+          }
+          if (kApply) {
+            s_M[k][lane] = M;
+            s_inv[k][lane] = (float)(1.0 / S);
+          } else {
+            GatStat g;
+            g.m = M;
+            g.inv_s = (float)(1.0 / S);
+            g.pad = 0.f;
+            st[r * H + lane] = g;
+          }
+        }
+        if (kApply) {
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) s_done[k] = 1;
+        }
+      }
+    }
+    // ---- 2. short rows (first batch only), while the other warps finish their long chunks
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
+    // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
+    if (kApply) {
+      for (int k = 0; k < kn; ++k) {
+        const int lr = s_long[k0 + k];
+        const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
+        if (b + (int64_t)warp * kTile >= e1) continue;
+        const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
+        while (s_done[k] == 0) {
+        }
+        __threadfence_block();
+        const double M = s_M[k][h];
+        const float inv_s = s_inv[k][h];
+        for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
+          const int cnt = (int)min((int64_t)kTile, e1 - c0);
           __syncwarp();
           stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
           __syncwarp();
-        }
-        if (pass == 0) {  // max of the stored values, then of the scores (monotone, see stat_row)
-          float mr = -INFINITY;
-          for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
-          if (mr != -INFINITY) acc = fmax(acc, stat_score<kScores>(mr, el_u, slope));
-          if (kScores && !(slope >= 0.0))
-            for (int j = part; j < cnt; j += P) acc = fmax(acc, stat_score<kScores>(T[j * H + h], el_u, slope));
-          continue;
-        }
-        for (int j = part; j < cnt; j += P) {
-          const double sc = stat_score<kScores>(T[j * H + h], el_u, slope);
-          if (pass == 1) acc += (double)expf((float)(sc - m));
-          else alpha[(c0 + j) * H + h] = expf((float)(sc - m)) * inv_s;
+          for (int j = part; j < cnt; j += P)
+            alpha[(c0 + j) * H + h] = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
         }
       }
-      if (pass == 2) break;
-#pragma unroll
-      for (int off = H; off < 32; off <<= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, acc, off);
-        acc = pass == 0 ? fmax(acc, o) : acc + o;
-      }
-      if (part == 0) s_red[warp][h] = acc;
-      __syncthreads();
-      double x = s_red[0][h];
-      for (int w = 1; w < kStatWarps; ++w) x = pass == 0 ? fmax(x, s_red[w][h]) : x + s_red[w][h];
-      __syncthreads();
-      if (pass == 0) m = x;
-      else sum = x;
-    }
-    if (!kApply && warp == 0 && part == 0) {
-      GatStat g;
-      g.m = m;
-      g.inv_s = (float)(1.0 / sum);
-      g.pad = 0.f;
-      st[r * H + h] = g;
     }
   }
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.

@@ -23,7 +23,8 @@ def main():
         name = r["Kernel Name"]
         if not name.startswith("ncu|"):
             continue
-        _, wl, op = name.split("|", 2)
+        _, wl, rest = name.split("|", 2)
+        op, kern = rest.split("/", 1) if "/" in rest else (rest, "")
         try:
             v = float(r["Metric Value"].replace(",", ""))
         except ValueError:
@@ -31,9 +32,11 @@ def main():
         unit = r["Metric Unit"]
         v *= SCALE.get(unit, 1.0)
         per[(wl, op)][r["ID"]][r["Metric Name"]] = v
+        per[(wl, op)][r["ID"]]["kernel"] = kern
     out = []
     for (wl, op), launches in sorted(per.items()):
-        L = list(launches.values())
+        L = [dict(m) for m in launches.values()]
+        kern = [m.pop("kernel", "") for m in L]
         dur = sum(m.get("gpu__time_duration.sum", 0.0) for m in L)
         rd = sum(m.get("dram__bytes_read.sum", 0.0) for m in L)
         wr = sum(m.get("dram__bytes_write.sum", 0.0) for m in L)
@@ -45,7 +48,7 @@ def main():
                     "dram_bytes": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                     "dram_GB/s_under_ncu": (rd + wr) / dur / 1e9 if dur else None,
                     "l2_bytes": lts, "l2_hit_pct": hit,
-                    "per_launch": [{k.split("__")[-1] if False else k: v for k, v in m.items()} for m in L]})
+                    "per_launch": [dict(m, kernel=k) for m, k in zip(L, kern)]})
     json.dump({"tool": "ncu --nvtx --print-nvtx-rename kernel --clock-control none --cache-control all --metrics ...",
                "driver": "tools/ncu_ops.py", "head": sys.argv[3] if len(sys.argv) > 3 else None,
                "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()), "rows": out}, open(dst, "w"), indent=1)
