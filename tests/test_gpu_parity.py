@@ -611,19 +611,27 @@ def test_gcn_inference_sampled_rows_c4():
         assert_within(out[r:r + 1], y2, c2, rel=_lin_rel(128), what=f"layer2 row {r}")
 
 
-def test_gat_inference_end_to_end_small(built):
+@pytest.mark.parametrize("hidden", [128, 512], ids=["4x32", "4x128"])
+def test_gat_inference_end_to_end_small(built, hidden):
     """2-layer GAT through inference.gat_inference vs the oracle composed from
     the GPU's own layer-1 intermediates (linear, attention projection, fused
-    aggregate with ELU; output layer with one 41-wide head)."""
+    aggregate with ELU; output layer with one 41-wide head).  Both readings of
+    A20 ("hidden size 128 ... 4 attention heads"): 4 x 32 and 4 x 128."""
     from paper_2103_00959_b200.inference import GATParams, gat_inference, _padded
     go, gg, _, _ = built["cl4000"]
     n = go.n
+    d1 = hidden // 4
     x = uniform((n, 50), seed=1)
-    p = GATParams.init(50, 128, 4, 41, DEV, seed=2)
+    p = GATParams.init(50, hidden, 4, 41, DEV, seed=2)
     out = host(gat_inference(gg, dev(x), p))
-    z1 = G.gsp_linear(dev(x), p.w1, y=_padded(n, 128, DEV))
-    el1, er1 = G.gsp_attn_project(z1, p.al1, p.ar1, 4, 32)
-    h1 = G.gsp_gat_aggregate_bias_act(gg, el1, er1, z1, 4, 32, p.b1, "elu", y=_padded(n, 128, DEV))
+    z1 = G.gsp_linear(dev(x), p.w1, y=_padded(n, hidden, DEV))
+    el1, er1 = G.gsp_attn_project(z1, p.al1, p.ar1, 4, d1)
+    # layer 1 against the oracle on the GPU's own z1, el1, er1
+    s1 = orc.gat_scores(go.row_ptr, go.col, host(el1), host(er1), 4)
+    a1 = orc.edge_softmax(go.row_ptr, s1, 4)
+    y1r, c1 = orc.multihead_spmm(go.row_ptr, go.col, a1, host(z1), 4, d1)
+    h1 = G.gsp_gat_aggregate_bias_act(gg, el1, er1, z1, 4, d1, p.b1, "elu", y=_padded(n, hidden, DEV))
+    assert_within(host(h1), orc.bias_act(y1r, host(p.b1), "elu"), c1, what=f"gat layer 1 ({hidden})")
     z2 = G.gsp_linear(h1, p.w2, y=_padded(n, 41, DEV))
     el2, er2 = G.gsp_attn_project(z2, p.al2, p.ar2, 1, 41)
     s = orc.gat_scores(go.row_ptr, go.col, host(el2), host(er2), 1)
