@@ -381,8 +381,10 @@ def gcn_rows(ctx, key, full_parity, budget_1t, budget_nt, with_build=False):
                                 "csr_bit_exact": host["csr_bit_exact"]}))
     del st, dt
     x_host = features(n, f, cfg.ld, seed=2)
-    x = torch.from_numpy(x_host).to(ctx.dev)
-    y = torch.empty((n, f), dtype=torch.float32, device=ctx.dev)
+    # the library's feature layout: rows on whole 128-byte L2 lines
+    x = G.empty_features(n, f, ctx.dev)
+    x.copy_(torch.from_numpy(x_host[:, :f]))
+    y = G.empty_features(n, f, ctx.dev)
 
     def step():
         G.gsp_spmm(gn, x, f=f, y=y)
@@ -431,7 +433,7 @@ def gat_rows(ctx, key, H, D, full_parity, budget_1t, budget_nt):
     al = torch.from_numpy(al_h.reshape(-1)).to(ctx.dev)
     ar = torch.from_numpy(ar_h.reshape(-1)).to(ctx.dev)
     el, er = G.gsp_attn_project(z, al, ar, H, D)
-    y = torch.empty((n, H * D), dtype=torch.float32, device=ctx.dev)
+    y = G.empty_features(n, H * D, ctx.dev)
     ws = torch.empty(G.gsp_gat_workspace(g, H), dtype=torch.uint8, device=ctx.dev)
     reps = max(10, a.steps // 2)
     t_ap = ctx.timer.cold(lambda: G.gsp_attn_project(z, al, ar, H, D, el=el, er=er), a.warmup, reps)
@@ -538,8 +540,9 @@ def secondaries(ctx, c4, c3):
         "note": "x stored in fp16, converted exactly, fp32 products and sums (gsp_spmm_f16); not the headline"}
     del x16
     fk, K = 41, 10
-    xk = torch.from_numpy(features(n, fk, 44, seed=9)).to(ctx.dev)
-    yk = torch.empty((n, fk), dtype=torch.float32, device=ctx.dev)
+    xk = G.empty_features(n, fk, ctx.dev)
+    xk.copy_(torch.from_numpy(features(n, fk, fk, seed=9)))
+    yk = G.empty_features(n, fk, ctx.dev)
     th = [0.1 * 0.9 ** k for k in range(K + 1)]
     tk = ctx.timer.cold(lambda: G.gsp_propagate(gn, xk, th, f=fk, y=yk), a.warmup, 5)
     out["NEXT4_C4_appnp_K10_f41"] = {"ms": float(np.median(tk)), "GE/s": K * nnz * fk / (np.median(tk) * 1e-3),
@@ -570,7 +573,8 @@ def secondaries(ctx, c4, c3):
             sk, dk = graph_for(cfg_k, seed=1)
             gk = G.gsp_sym_normalize(G.gsp_coo_to_csr(cfg_k.n, torch.from_numpy(sk).to(ctx.dev),
                                                       torch.from_numpy(dk).to(ctx.dev), None, True, 1.0))
-        xk = torch.from_numpy(features(cfg_k.n, fin, (fin + 3) // 4 * 4, seed=2)).to(ctx.dev)[:, :fin]
+        xk = G.empty_features(cfg_k.n, fin, ctx.dev)
+        xk.copy_(torch.from_numpy(features(cfg_k.n, fin, fin, seed=2)))
         pg = GCNParams.init(fin, 128, ncls, ctx.dev, seed=1)
         pa = GATParams.init(fin, 128, 4, ncls, ctx.dev, seed=1)
         pa4 = GATParams.init(fin, 512, 4, ncls, ctx.dev, seed=1)
@@ -598,7 +602,7 @@ def e2e_single(ctx, c4):
     n, f = cfg.n, cfg.f
     xh = torch.from_numpy(x_host).pin_memory()
     yh = torch.empty((n, cfg.ld), dtype=torch.float32).pin_memory()
-    hs = HostSpMM(gn, f, cfg.ld, device=ctx.dev)
+    hs = HostSpMM(gn, f, G.feature_ld(f), device=ctx.dev)
     st = torch.cuda.current_stream()
     ts = []
     for i in range(a.warmup + max(3, a.steps // 3)):
@@ -682,7 +686,8 @@ def main_single(args):
         "ms_per_step_min": float(np.min(times)), "ms_per_step_p90": float(np.percentile(times, 90)),
         "ms_per_step_warm_no_flush": warm, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ld": cfg.ld,
+        "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ldx": x.stride(0), "ldy": y.stride(0),
+                   "layout": "row-major fp32, rows padded to whole 128-byte lines (G.feature_ld)",
                    "graph": f"chung-lu gamma=2.5 seed=1 ({cfg.note}; node/pair counts P:18-26)",
                    "l2": "flushed before every step (256 MB memset, untimed); X (562 MB) > L2 as well",
                    "parallelism": "single GPU",
@@ -762,7 +767,7 @@ def main_dist(args):
     op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev)
     xs = torch.from_numpy(np.ascontiguousarray(x_host[op.r0:op.r1, :f])).to(dev)
     op.load_shard(xs)
-    y = torch.empty((op.rows, f), dtype=torch.float32, device=dev)
+    y = G.empty_features(op.rows, f, dev)
     timer = Timer(dev)
 
     def step():
@@ -796,7 +801,8 @@ def main_dist(args):
     t_comm = allmax(float(np.median(timer.cold(lambda: [op.exchange(k) for k in range(nch)], 2, 5))))
     t_comp = allmax(float(np.median(timer.cold(lambda: [op._local(k, y) for k in range(nch)], 2, 5))))
     # bitwise check of this rank's rows against the single-GPU gsp_spmm
-    xfull = torch.from_numpy(x_host).to(dev)
+    xfull = G.empty_features(n, f, dev)
+    xfull.copy_(torch.from_numpy(x_host[:, :f]))
     step()
     torch.cuda.synchronize()
     y1 = G.gsp_spmm(gn, xfull, f=f)
@@ -849,7 +855,8 @@ def main_dist(args):
         "metric": METRIC, "value": ge / (t_max * 1e-3), "unit": "GE/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ld": cfg.ld,
+        "config": {"workload": cfg.name, "n": n, "nnz": nnz, "f": f, "ldy": y.stride(0),
+                   "layout": "row-major fp32, rows padded to whole 128-byte lines (G.feature_ld); shards chunk-packed",
                    "graph": f"chung-lu gamma=2.5 seed=1 ({cfg.note})",
                    "l2": "flushed before every step (256 MB memset, untimed)",
                    "parallelism": f"row partition x{world} (nnz-balanced) + NCCL all-gather of X, "

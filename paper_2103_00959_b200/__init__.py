@@ -161,6 +161,38 @@ def _mat(t: torch.Tensor, name: str):
     return t, ld
 
 
+# Feature rows are laid out on whole 128-byte L2 lines: a row-slab the SpMM
+# gathers then fills whole lines, so one slab of X occupies exactly its bytes
+# of L2 (C4: 5.39 -> 4.6 ms for ld 604 -> 608, tools/ld_probe.py).
+FEATURE_ALIGN_BYTES = 128
+
+
+def feature_ld(f: int, dtype=torch.float32) -> int:
+    """Row stride (elements) of a feature matrix of width f in the library's
+    layout: rows of >= 128 bytes padded to whole 128-byte lines; narrower rows
+    to the next power of two of bytes (>= 16), so rows tile lines exactly."""
+    es = torch.empty((), dtype=dtype).element_size()
+    b = max(int(f), 1) * es
+    if b >= FEATURE_ALIGN_BYTES:
+        b = (b + FEATURE_ALIGN_BYTES - 1) // FEATURE_ALIGN_BYTES * FEATURE_ALIGN_BYTES
+    else:
+        p = 16
+        while p < b:
+            p *= 2
+        b = p
+    return b // es
+
+
+def empty_features(n: int, f: int, device, dtype=torch.float32) -> torch.Tensor:
+    """[n, f] view of an [n, feature_ld(f)] buffer (128-byte aligned rows, the
+    padding columns zeroed: kernels may read them, gsp.h)."""
+    ld = feature_ld(f, dtype)
+    buf = torch.empty((n, ld), dtype=dtype, device=device)
+    if ld > f:
+        buf[:, f:].zero_()
+    return buf[:, :f]
+
+
 def _rows(t: torch.Tensor, n: int, name: str):
     """The C ABI cannot see tensor extents: catch caller shape mistakes here."""
     if t.shape[0] < n:
@@ -276,7 +308,7 @@ def gsp_spmm(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[torch
     x, ldx = _mat(x, "x")
     f = x.shape[1] if f is None else int(f)
     if y is None:
-        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+        y = empty_features(a.n_rows, f, x.device)
     y, ldy = _mat(y, "y")
     _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
@@ -301,7 +333,7 @@ def gsp_spmm_f16(a: CSR, x: torch.Tensor, f: Optional[int] = None, y: Optional[t
         raise TypeError("x must be a 2-D float16 tensor with unit column stride")
     f = x.shape[1] if f is None else f
     if y is None:
-        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+        y = empty_features(a.n_rows, f, x.device)
     y, ldy = _mat(y, "y")
     _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
@@ -315,7 +347,7 @@ def gsp_gspmm(a: CSR, x: torch.Tensor, reduce: str = "sum", f: Optional[int] = N
     x, ldx = _mat(x, "x")
     f = x.shape[1] if f is None else int(f)
     if y is None:
-        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+        y = empty_features(a.n_rows, f, x.device)
     y, ldy = _mat(y, "y")
     _rows(x, a.n_cols, "x"), _rows(y, a.n_rows, "y"), _width(x, f, "x"), _width(y, f, "y")
     v = a.view()
@@ -360,7 +392,7 @@ def gsp_multihead_spmm(a: CSR, alpha: torch.Tensor, z: torch.Tensor, heads: int,
     _vec(alpha, torch.float32, "alpha")
     z, ldz = _mat(z, "z")
     if y is None:
-        y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device)
+        y = empty_features(a.n_rows, heads * d, z.device)
     y, ldy = _mat(y, "y")
     _numel(alpha, a.nnz * heads, "alpha"), _rows(z, a.n_cols, "z"), _rows(y, a.n_rows, "y")
     _width(z, heads * d, "z"), _width(y, heads * d, "y")
@@ -411,7 +443,7 @@ def gsp_gat_aggregate(a: CSR, el: torch.Tensor, er: torch.Tensor, z: torch.Tenso
     _vec(er, torch.float32, "er")
     z, ldz = _mat(z, "z")
     if y is None:
-        y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device)
+        y = empty_features(a.n_rows, heads * d, z.device)
     y, ldy = _mat(y, "y")
     want = alpha_out is not None
     if alpha_out is True:
@@ -481,7 +513,7 @@ def gsp_propagate(a: CSR, x: torch.Tensor, theta, f: Optional[int] = None, y: Op
     f = x.shape[1] if f is None else int(f)
     th = (ctypes.c_double * len(theta))(*[float(t) for t in theta])
     if y is None:
-        y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device)
+        y = empty_features(a.n_rows, f, x.device)
     y, ldy = _mat(y, "y")
     n = ctypes.c_size_t(0)
     v = a.view()
@@ -549,7 +581,7 @@ def gsp_gat_aggregate_backward(a: CSR, at: CSR, perm: torch.Tensor, el: torch.Te
     """(dz, d_el, d_er) of gsp_gat_aggregate's output gradient dy."""
     z, ldz = _mat(z, "z")
     dy, lddy = _mat(dy, "dy")
-    dz = torch.empty((a.n_cols, heads * d), dtype=torch.float32, device=z.device)
+    dz = empty_features(a.n_cols, heads * d, z.device)
     d_el = torch.empty((a.n_rows, heads), dtype=torch.float32, device=z.device)
     d_er = torch.empty((a.n_cols, heads), dtype=torch.float32, device=z.device)
     n = ctypes.c_size_t(0)
@@ -558,7 +590,7 @@ def gsp_gat_aggregate_backward(a: CSR, at: CSR, perm: torch.Tensor, el: torch.Te
     ws = _ws(n.value, z.device)
     _check(lib().gsp_gat_aggregate_backward(ctypes.byref(v), ctypes.byref(vt), _ptr(perm), heads, _ptr(el),
                                             _ptr(er), float(negative_slope), _ptr(z), d, ldz, _ptr(dy), lddy,
-                                            _ptr(dz), heads * d, _ptr(d_el), _ptr(d_er), _aligned(ws), n.value,
+                                            _ptr(dz), dz.stride(0), _ptr(d_el), _ptr(d_er), _aligned(ws), n.value,
                                             _stream(stream)), "gsp_gat_aggregate_backward")
     return dz, d_el, d_er
 
@@ -596,7 +628,7 @@ def gsp_linear(x: torch.Tensor, w: torch.Tensor, y: Optional[torch.Tensor] = Non
     w, ldw = _mat(w, "w")
     n, f_in = x.shape
     f_out = w.shape[1]
-    y = torch.empty((n, f_out), dtype=torch.float32, device=x.device) if y is None else y
+    y = empty_features(n, f_out, x.device) if y is None else y
     y, ldy = _mat(y, "y")
     if tensor_cores:
         nb = ctypes.c_size_t(0)
@@ -614,7 +646,7 @@ def gsp_spmm_bias_act(a: CSR, x: torch.Tensor, bias: Optional[torch.Tensor] = No
                       f: Optional[int] = None, y: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     x, ldx = _mat(x, "x")
     f = x.shape[1] if f is None else int(f)
-    y = torch.empty((a.n_rows, f), dtype=torch.float32, device=x.device) if y is None else y
+    y = empty_features(a.n_rows, f, x.device) if y is None else y
     y, ldy = _mat(y, "y")
     v = a.view()
     _check(lib().gsp_spmm_bias_act(ctypes.byref(v), _ptr(x), f, ldx, _ptr(bias), ACT[act], _ptr(y), ldy,
@@ -627,7 +659,7 @@ def gsp_gcn_layer(a: CSR, x: torch.Tensor, w: torch.Tensor, bias: Optional[torch
     """y = act(A (x w) + bias)  (Eq. gcn_layer)."""
     x, ldx = _mat(x, "x")
     f_in, f_out = w.shape
-    y = torch.empty((a.n_rows, f_out), dtype=torch.float32, device=x.device) if y is None else y
+    y = empty_features(a.n_rows, f_out, x.device) if y is None else y
     y, ldy = _mat(y, "y")
     nb = ctypes.c_size_t(0)
     _check(lib().gsp_gcn_layer_workspace(a.n_cols, f_in, f_out, ctypes.byref(nb)), "gsp_gcn_layer_workspace")
@@ -645,7 +677,7 @@ def gsp_gat_aggregate_bias_act(a: CSR, el: torch.Tensor, er: torch.Tensor, z: to
                                single_launch: bool = False, stream=None) -> torch.Tensor:
     """gsp_gat_aggregate with act(Y + bias) fused; ws / single_launch as there."""
     z, ldz = _mat(z, "z")
-    y = torch.empty((a.n_rows, heads * d), dtype=torch.float32, device=z.device) if y is None else y
+    y = empty_features(a.n_rows, heads * d, z.device) if y is None else y
     y, ldy = _mat(y, "y")
     _numel(el, a.n_rows * heads, "el"), _numel(er, a.n_cols * heads, "er"), _rows(z, a.n_cols, "z")
     _rows(y, a.n_rows, "y"), _width(z, heads * d, "z"), _width(y, heads * d, "y")

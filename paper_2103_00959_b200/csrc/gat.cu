@@ -8,20 +8,18 @@ namespace gsp {
 
 // ------------------------------------------------------------------------
 // Row statistics: m[u,h] = max_e s[e,h] (fp64) and 1 / sum_e exp(s - m),
-// all heads of a row at once ("warp level intrinsic ... find the max
-// ... reduce ... the sum").  H (heads, dividing 32) is a template parameter.
-// Grid: one CTA of 8 warps per 32 rows; warp w owns rows 4w .. 4w+3 of them.
-//  * SHORT rows (<= kTile = 1024 / H entries): the entries of the warp's 4
-//    rows (contiguous in CSR) are loaded into the warp's shared tile
-//    T[kTile][H] in one sweep when they fit (else row by row); each lane
-//    issues all of its loads before the first use (kU entries in flight).
-//    Then, per row, lane l reduces head h = l % H over the row's entries
-//    part, part + P, ... (part = l / H, P = 32 / H) and an xor tree over
-//    lanes of equal head finishes the max and the sum.  exp(s - m) stays in
-//    the tile for the apply pass.
-//  * LONG rows: the whole CTA, after the short rows.  Warp w takes the
-//    tile-sized chunks w, w+8, ... of the row (same tile and lane layout),
-//    then the xor tree per warp and the 8 warps' partials in warp order.
+// all heads of a row at once (P:653-656 edge-wise softmax: "find the max
+// value ... subtract ... exponent ... reduce ... the sum").  H (heads,
+// dividing 32) is a template parameter.  Grid: one CTA of 8 warps per
+// 8 * 32 / H rows; warp w owns RPW = 32 / H consecutive rows.
+//  * SHORT rows (<= kTile = 1024 / H entries): lane l owns (row l / H,
+//    head l % H) and reduces it sequentially in column order; the warp's
+//    rows are staged in its 4 KB shared tile T[j][H] by cp.async (no
+//    registers in flight), as many consecutive rows at a time as fit.
+//  * LONG rows: cut into tile-sized chunks; warp w takes chunks w, w+8, ...
+//    and folds them into a partial (own max m_w, fp64 sum of exp(s - m_w));
+//    the last warp to arrive merges the 8 partials in warp order (no CTA
+//    barrier per long row; see row_stats_warp).
 // Every order depends on the row alone (deterministic, partition-invariant).
 // ------------------------------------------------------------------------
 // kScores: s from el/er (GAT) or s = logits (edge softmax).
@@ -30,14 +28,10 @@ namespace gsp {
 #ifndef GSP_STAT_WARPS
 #define GSP_STAT_WARPS 8
 #endif
-#ifndef GSP_STAT_RPW
-#define GSP_STAT_RPW 4
-#endif
 #ifndef GSP_STAT_MINB
 #define GSP_STAT_MINB 4
 #endif
 constexpr int kStatWarps = GSP_STAT_WARPS;  // warps per CTA
-constexpr int kStatRPW = GSP_STAT_RPW;      // rows per warp
 constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
 
 template <bool kScores>
@@ -61,10 +55,11 @@ __device__ __forceinline__ void cp_async(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // entries [e0, e0 + cnt) of the CSR -> T[j][H] (er rows of their columns, or
-// logits rows) by cp.async; the caller's __syncwarp after it publishes T
+// logits rows) by cp.async, issued only (stat_load waits for them); the
+// caller's __syncwarp after the wait publishes T
 template <int H, bool kScores>
-__device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
-                                          const float *__restrict__ er, const float *logits, int lane) {
+__device__ __forceinline__ void stat_load_async(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
+                                                const float *__restrict__ er, const float *logits, int lane) {
   if (kScores) {
     constexpr int kV = H >= 4 ? 4 : H;  // floats per copy (er rows are 4 / 8 / 16-byte aligned, launch_stats)
     constexpr int kU = 8;               // column indices in flight per lane
@@ -89,76 +84,162 @@ __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const i
     const int nf = cnt * H;
     for (int k = lane; k < nf; k += 32) cp_async<4>(T + k, src + k);
   }
+}
+
+// the entries of nb rows -> T back to back: row i's cnt_i entries (CSR start
+// tab_start[i]) at tile offset tab_off[i]; tab_off[nb] = tot.  Every position
+// is looked up (nb <= 32 / H rows), all column loads of a round are issued
+// before their cp.async copies, and all copies before the one wait.
+template <int H, bool kScores>
+__device__ __forceinline__ void stat_load_rows(float *T, const int *tab_off, const int64_t *tab_start, int nb, int tot,
+                                               const int32_t *__restrict__ col, const float *__restrict__ er,
+                                               const float *logits, int lane) {
+  auto src = [&](int p) {  // CSR entry of tile position p
+    int i = 0;
+    while (i + 1 < nb && tab_off[i + 1] <= p) ++i;
+    return tab_start[i] + (p - tab_off[i]);
+  };
+  if (kScores) {
+    constexpr int kV = H >= 4 ? 4 : H;
+    constexpr int kU = 4;
+    for (int b0 = 0; b0 < tot; b0 += 32 * kU) {
+      int c[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int p = b0 + lane + 32 * u;
+        c[u] = p < tot ? __ldg(col + src(p)) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int p = b0 + lane + 32 * u;
+        if (p < tot) {
+#pragma unroll
+          for (int q = 0; q < H; q += kV) cp_async<kV * 4>(T + p * H + q, er + (int64_t)c[u] * H + q);
+        }
+      }
+    }
+  } else {
+    for (int k = lane; k < tot * H; k += 32) cp_async<4>(T + k, logits + src(k / H) * H + (k % H));
+  }
   cp_async_wait_all();
 }
 
-// reduce one short row held in T[0 .. d) and write its statistics or alpha
+template <int H, bool kScores>
+__device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
+                                          const float *__restrict__ er, const float *logits, int lane) {
+  stat_load_async<H, kScores>(T, e0, cnt, col, er, logits, lane);
+  cp_async_wait_all();
+}
+
+// Short rows (<= kTile entries): lane l of warp w owns (row w * RPW + l / H,
+// head l % H), RPW = 32 / H rows per warp, and reduces its row and head
+// SEQUENTIALLY in column order -- no shuffles, the warp's rows in parallel.
+// The rows' entries (contiguous in CSR) are staged in the warp's tile by
+// cp.async, as many consecutive short rows at a time as fit.  The row max of
+// the fp64 scores is the score of the fp32 max of the stored values (LeakyReLU
+// with slope >= 0 and IEEE rounding are monotone) -- exactly; slope < 0 takes
+// the fp64 max of the scores.
 template <int H, bool kScores, bool kApply>
-__device__ __forceinline__ void stat_row(float *T, int64_t r, int64_t b, int d, const float *__restrict__ el,
-                                         double slope, GatStat *__restrict__ st, float *alpha, int lane) {
-  constexpr int P = 32 / H;
-  const int h = lane % H, part = lane / H;
-  const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-  // the score is monotone non-decreasing in the stored value (LeakyReLU with
-  // slope >= 0 and IEEE RN are monotone), so the row max of the fp64 scores is
-  // the score of the fp32 max -- exactly (slope < 0: fp64 max of the scores)
-  float mr = -INFINITY;
-  for (int j = part; j < d; j += P) mr = fmaxf(mr, T[j * H + h]);
-#pragma unroll
-  for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
-  double m = stat_score<kScores>(mr, el_u, slope);
-  if (kScores && !(slope >= 0.0)) {
-    m = -INFINITY;
-    for (int j = part; j < d; j += P) m = fmax(m, stat_score<kScores>(T[j * H + h], el_u, slope));
-#pragma unroll
-    for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-  }
-  double s = 0.0;
-  for (int j = part; j < d; j += P) {
-    const float ex = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - m));
-    s += (double)ex;
-    if (kApply) T[j * H + h] = ex;  // own slot: no other lane reads it
-  }
-#pragma unroll
-  for (int off = H; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  const float inv_s = (float)(1.0 / s);
-  if (kApply) {
-    for (int j = part; j < d; j += P) alpha[(b + j) * H + h] = T[j * H + h] * inv_s;  // lane-contiguous
-  } else if (part == 0) {
-    GatStat g;
-    g.m = m;
-    g.inv_s = inv_s;
-    g.pad = 0.f;
-    st[r * H + h] = g;
+__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, const uint8_t *s_ord, int64_t rbase,
+                                                int64_t n_rows, const int32_t *__restrict__ col,
+                                                const float *__restrict__ el, const float *__restrict__ er,
+                                                const float *logits, double slope, GatStat *__restrict__ st,
+                                                float *alpha, int warp, int lane, int *tab_off,
+                                                int64_t *tab_start) {
+  constexpr int kTile = kStatTileFloats / H;
+  constexpr int RPW = 32 / H;
+  const int rl = lane / H, h = lane % H;
+  const int base = warp * RPW;  // the warp's rows are s_ord[base .. base + RPW)
+  int k = 0;
+  while (k < RPW) {
+    // rows k .. k2-1 of the warp's (degree-sorted) rows that fit the tile
+    // together; their entries are staged back to back (row k at offset 0)
+    int k2 = k, tot = 0, off = 0;
+    while (k2 < RPW) {
+      const int q = s_ord[base + k2];
+      const int d = (int)(s_rp[q + 1] - s_rp[q]);
+      if (d > kTile) break;  // sorted: every later row is long too (own path)
+      if (tot + d > kTile) break;
+      if (k2 == rl) off = tot;
+      tot += d;
+      ++k2;
+    }
+    if (k2 == k) break;  // only long rows remain
+    // stage the batch: lane i < k2 - k publishes row i's (tile offset, CSR
+    // start); every position of the batch is then one load of one lane, all
+    // issued before the single wait (rows are not contiguous in CSR)
+    __syncwarp();
+    if (lane < k2 - k) {
+      const int q = s_ord[base + k + lane];
+      tab_start[lane] = s_rp[q];
+      int o = 0;
+      for (int i = k; i < k + lane; ++i) o += (int)(s_rp[s_ord[base + i] + 1] - s_rp[s_ord[base + i]]);
+      tab_off[lane] = o;
+    }
+    if (lane == 0) tab_off[k2 - k] = tot;
+    __syncwarp();
+    stat_load_rows<H, kScores>(T, tab_off, tab_start, k2 - k, tot, col, er, logits, lane);
+    __syncwarp();
+    if (rl >= k && rl < k2) {
+      const int q = s_ord[base + rl];
+      const int64_t grow = rbase + q, b = s_rp[q];
+      const int d = (int)(s_rp[q + 1] - b);
+      if (d > 0 && grow < n_rows) {
+        float *Tr = T + off * H + h;
+        const double el_u = kScores ? (double)__ldg(el + grow * H + h) : 0.0;
+        float mr = -INFINITY;
+        for (int j = 0; j < d; ++j) mr = fmaxf(mr, Tr[j * H]);
+        double m = stat_score<kScores>(mr, el_u, slope);
+        if (kScores && !(slope >= 0.0)) {
+          m = -INFINITY;
+          for (int j = 0; j < d; ++j) m = fmax(m, stat_score<kScores>(Tr[j * H], el_u, slope));
+        }
+        double sum = 0.0;
+        for (int j = 0; j < d; ++j) {
+          const float ex = expf((float)(stat_score<kScores>(Tr[j * H], el_u, slope) - m));
+          sum += (double)ex;
+          if (kApply) Tr[j * H] = ex;  // own slot: no other lane reads it
+        }
+        const float inv_s = (float)(1.0 / sum);
+        if (kApply) {
+          for (int j = 0; j < d; ++j) alpha[(b + j) * H + h] = Tr[j * H] * inv_s;
+        } else {
+          GatStat g;
+          g.m = m;
+          g.inv_s = inv_s;
+          g.pad = 0.f;
+          st[grow * H + h] = g;
+        }
+      }
+    }
+    k = k2;
   }
 }
 
-// rows of <= kTile entries: warp w owns rows 4w .. 4w+3 of the CTA (contiguous
-// in CSR, loaded into its tile in one sweep when they fit together)
-template <int H, bool kScores, bool kApply>
-__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
-                                                const int32_t *__restrict__ col, const float *__restrict__ el,
-                                                const float *__restrict__ er, const float *logits, double slope,
-                                                GatStat *__restrict__ st, float *alpha, int warp, int lane) {
-  constexpr int kTile = kStatTileFloats / H;
-  const int64_t r0 = rbase + warp * kStatRPW;
-  const int64_t B0 = s_rp[warp * kStatRPW], BN = s_rp[warp * kStatRPW + kStatRPW];
-  const bool together = BN - B0 <= kTile;
-  __syncwarp();
-  if (together) stat_load<H, kScores>(T, B0, (int)(BN - B0), col, er, logits, lane);
-  __syncwarp();
-  for (int k = 0; k < kStatRPW; ++k) {
-    const int64_t bk = s_rp[warp * kStatRPW + k], d = s_rp[warp * kStatRPW + k + 1] - bk;
-    if (d == 0 || d > kTile || r0 + k >= n_rows) continue;
-    float *Tk = T;
-    if (together) {
-      Tk = T + (bk - B0) * H;
-    } else {
-      __syncwarp();
-      stat_load<H, kScores>(T, bk, (int)d, col, er, logits, lane);
-      __syncwarp();
+// Sort the CTA's rows by degree in groups of 32 (warp bitonic sort on
+// (degree, index) -- unique keys, so the order is deterministic): the warps
+// then get rows of similar length and the lanes of a warp (one per (row,
+// head)) finish together.  Long rows sort last.
+__device__ __forceinline__ void stat_sort_rows(const int64_t *s_rp, uint8_t *s_ord, int kRows, int lane) {
+  for (int g = 0; g < kRows; g += 32) {
+    const int idx = g + lane;
+    long long key = idx < kRows ? (long long)(s_rp[idx + 1] - s_rp[idx]) : (1ll << 62);
+    int id = idx;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const long long ok = __shfl_xor_sync(0xffffffffu, key, j);
+        const int oi = __shfl_xor_sync(0xffffffffu, id, j);
+        const bool other_less = ok < key || (ok == key && oi < id);
+        const bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
+        if (keep_min ? other_less : !other_less) {
+          key = ok;
+          id = oi;
+        }
+      }
     }
-    stat_row<H, kScores, kApply>(Tk, r0 + k, bk, (int)d, el, slope, st, alpha, lane);
+    if (idx < kRows) s_ord[idx] = (uint8_t)id;
   }
 }
 
@@ -184,7 +265,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
                                                                   double slope, int64_t n_rows,
                                                                   GatStat *__restrict__ st, float *alpha) {
   constexpr int kTile = kStatTileFloats / H;
-  constexpr int kRows = kStatWarps * kStatRPW;  // rows per CTA
+  constexpr int kRows = kStatWarps * (32 / H);  // rows per CTA (32 / H per warp: lane = (row, head))
   constexpr int kSlots = StatSlots<H>::kSlots;
   constexpr int P = 32 / H;
   __shared__ __align__(16) float s_tile[kStatWarps][kStatTileFloats];
@@ -196,22 +277,30 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   __shared__ volatile int s_done[kSlots];
   __shared__ int64_t s_rp[kRows + 1];
   __shared__ int s_long[kRows];
+  __shared__ uint8_t s_ord[kRows];
+  __shared__ int s_tab_off[kStatWarps][32 / H + 1];
+  __shared__ int64_t s_tab_start[kStatWarps][32 / H];
   __shared__ int s_nlong;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int h = lane % H, part = lane / H;
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
   // the CTA's row pointers and its long rows, once (nobody is busy yet)
-  if (tid <= kRows) s_rp[tid] = __ldg(rp + min(rbase + tid, n_rows));
+  for (int i = tid; i <= kRows; i += kStatWarps * 32) s_rp[i] = __ldg(rp + min(rbase + i, n_rows));
   if (tid < kSlots) {
     s_cnt[tid] = 0;
     s_done[tid] = 0;
   }
   __syncthreads();
   if (warp == 0) {
-    const bool lg = (s_rp[lane + 1] - s_rp[lane]) > kTile;
-    const unsigned bl = __ballot_sync(0xffffffffu, lg);
-    if (lg) s_long[__popc(bl & ((1u << lane) - 1u))] = lane;
-    if (lane == 0) s_nlong = __popc(bl);
+    int nl = 0;
+    for (int r0 = 0; r0 < kRows; r0 += 32) {
+      const bool lg = r0 + lane < kRows && (s_rp[r0 + lane + 1] - s_rp[r0 + lane]) > kTile;
+      const unsigned bl = __ballot_sync(0xffffffffu, lg);
+      if (lg) s_long[nl + __popc(bl & ((1u << lane) - 1u))] = r0 + lane;
+      nl += __popc(bl);
+    }
+    if (lane == 0) s_nlong = nl;
+    stat_sort_rows(s_rp, s_ord, kRows, lane);
   }
   __syncthreads();
   const int nlong = s_nlong;
@@ -301,7 +390,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, s_ord, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane, s_tab_off[warp], s_tab_start[warp]);
     // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
     if (kApply) {
       for (int k = 0; k < kn; ++k) {
@@ -325,7 +414,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
   }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, s_ord, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane, s_tab_off[warp], s_tab_start[warp]);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.
@@ -371,7 +460,7 @@ static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *e
   const float *vsrc = kScores ? er : logits;
   const bool vec_ok = H < 4 ? (H == 1 || aligned8(vsrc)) : aligned16(vsrc);
   if (32 % H == 0 && (vec_ok || !kScores)) {
-    const unsigned blocks = (unsigned)ceil_div(a->n_rows, kStatWarps * kStatRPW);
+    const unsigned blocks = (unsigned)ceil_div(a->n_rows, kStatWarps * (32 / H));
 #define GSP_STATS_H(HH)                                                                                       \
   case HH:                                                                                                   \
     row_stats_warp<HH, kScores, kApply><<<blocks, kStatWarps * 32, 0, s>>>(a->row_ptr, a->col_idx, el, er,     \

@@ -25,7 +25,7 @@ from typing import Callable, List, Optional
 
 import torch
 
-from . import CSR, gsp_attn_project, gsp_csr_slice, gsp_gat_aggregate, gsp_partition_rows, gsp_spmm
+from . import CSR, feature_ld, gsp_attn_project, gsp_csr_slice, gsp_gat_aggregate, gsp_partition_rows, gsp_spmm
 
 
 class GpuOps:
@@ -79,17 +79,18 @@ class RowPartitionedSpMM:
         self.cols = chunk_bounds(f, chunks)
         self.device = torch.device(device) if device is not None else a.row_ptr.device
         self.all_gather = all_gather or (lambda out, inp: torch.distributed.all_gather_into_tensor(out, inp))
-        # chunk-packed shard and gathered buffers (each chunk contiguous, ld = chunk width)
-        self.shard = [torch.zeros((self.npad, c1 - c0), dtype=torch.float32, device=self.device)
+        # chunk-packed shard and gathered buffers (each chunk contiguous; rows
+        # padded to whole 128-byte lines, the library's feature layout)
+        self.shard = [torch.zeros((self.npad, feature_ld(c1 - c0)), dtype=torch.float32, device=self.device)
                       for c0, c1 in zip(self.cols[:-1], self.cols[1:])]
-        self.gathered = [torch.empty((world * self.npad, c1 - c0), dtype=torch.float32, device=self.device)
-                         for c0, c1 in zip(self.cols[:-1], self.cols[1:])]
+        self.gathered = [torch.empty((world * self.npad, feature_ld(c1 - c0)), dtype=torch.float32,
+                                     device=self.device) for c0, c1 in zip(self.cols[:-1], self.cols[1:])]
         self.comm = torch.cuda.Stream(device=self.device) if self.device.type == "cuda" else None
 
     def load_shard(self, x_rows: torch.Tensor):
         """x_rows: [rows, f] features of this rank's nodes."""
         for k, (c0, c1) in enumerate(zip(self.cols[:-1], self.cols[1:])):
-            self.shard[k][:self.rows].copy_(x_rows[:, c0:c1])
+            self.shard[k][:self.rows, :c1 - c0].copy_(x_rows[:, c0:c1])
 
     def exchange(self, k: int):
         self.all_gather(self.gathered[k], self.shard[k])
@@ -120,7 +121,7 @@ class RowPartitionedSpMM:
     def _local(self, k: int, y: torch.Tensor):
         c0, c1 = self.cols[k], self.cols[k + 1]
         if self.rows:
-            self.ops.spmm(self.local, self.gathered[k], c1 - c0, y[:, c0:c1])
+            self.ops.spmm(self.local, self.gathered[k][:, :c1 - c0], c1 - c0, y[:, c0:c1])
 
 
 class RowPartitionedPropagate(RowPartitionedSpMM):
@@ -138,14 +139,14 @@ class RowPartitionedPropagate(RowPartitionedSpMM):
             raise ValueError("theta needs K >= 1 (len >= 2)")
         if y is None:
             y = torch.empty((self.rows, self.f), dtype=torch.float32, device=self.device)
-        x0 = [s[:self.rows].clone() for s in self.shard]  # theta_0 x term of step 1
+        x0 = [s[:self.rows, :c1 - c0].clone() for s, c0, c1 in zip(self.shard, self.cols[:-1], self.cols[1:])]
         nch = len(self.cols) - 1
         for k in range(1, K + 1):
             def local(c):
                 c0, c1 = self.cols[c], self.cols[c + 1]
                 if self.rows:
-                    gsp_spmm_accumulate(self.local, self.gathered[c], y[:, c0:c1], float(theta[k]), f=c1 - c0,
-                                        t=self.shard[c][:self.rows] if k < K else None,
+                    gsp_spmm_accumulate(self.local, self.gathered[c][:, :c1 - c0], y[:, c0:c1], float(theta[k]),
+                                        f=c1 - c0, t=self.shard[c][:self.rows, :c1 - c0] if k < K else None,
                                         src=x0[c] if k == 1 else None, src_coef=float(theta[0]))
             if self.comm is None:
                 for c in range(nch):

@@ -20,19 +20,14 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import (CSR, gsp_attn_project, gsp_gat_aggregate_bias_act, gsp_gcn_layer, gsp_linear)
+from . import (CSR, empty_features, gsp_attn_project, gsp_gat_aggregate_bias_act, gsp_gcn_layer, gsp_linear)
 
 
 def _padded(n: int, cols: int, device) -> torch.Tensor:
-    """[n, cols] view of an [n, round_up(cols, 4)] buffer: rows stay 16-byte
-    aligned so the engine's float4 path applies to any width.  The padding
-    columns are zeroed once: the next layer's gathers may read them (gsp.h: x
-    is [n][ld]; their sums are never stored) and they stay defined."""
-    ld = (cols + 3) // 4 * 4
-    buf = torch.empty((n, ld), dtype=torch.float32, device=device)
-    if ld > cols:
-        buf[:, cols:].zero_()
-    return buf[:, :cols]
+    """[n, cols] view of a buffer in the library's feature layout (rows on
+    whole 128-byte lines, padding columns zeroed: the next layer's gathers may
+    read them and they stay defined) -- gsp.h, DESIGN.md §2."""
+    return empty_features(n, cols, device)
 
 
 def _glorot(shape, rng):

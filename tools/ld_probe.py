@@ -40,11 +40,14 @@ for key in (sys.argv[1:] or ["C4", "C5"]):
     f = cfg.f
     x0 = torch.from_numpy(features(cfg.n, f, f, seed=2)).to(dev)
     yref = None
-    for ld in sorted({(f + 3) // 4 * 4, (f + 31) // 32 * 32, (f + 63) // 64 * 64}):
+    lds = [int(v) for v in os.environ.get("LDS", "").split(",") if v] or \
+        sorted({(f + 3) // 4 * 4, (f + 31) // 32 * 32, (f + 63) // 64 * 64})
+    slabs = [int(v) for v in os.environ.get("SLABS", "0,64,32").split(",")]
+    for ld in lds:
         buf = torch.zeros((cfg.n, ld), device=dev)
         buf[:, :f] = x0
         x = buf[:, :f]
-        for slab in (0, 64, 32):
+        for slab in slabs:
             y = torch.empty((cfg.n, f), device=dev)
             ms = t(lambda: G.gsp_spmm(gn, x, f=f, y=y, slab_cols=slab))
             if yref is None:

@@ -59,8 +59,9 @@ def gcn(key, with_build=False):
         g = G.gsp_coo_to_csr(cfg.n, st, dt, None, True, 1.0)
         gn = G.gsp_sym_normalize(g)
     del st, dt
-    x = torch.from_numpy(features(cfg.n, cfg.f, cfg.ld, seed=2)).to(dev)
-    y = torch.empty((cfg.n, cfg.f), dtype=torch.float32, device=dev)
+    x = G.empty_features(cfg.n, cfg.f, dev)
+    x.copy_(torch.from_numpy(features(cfg.n, cfg.f, cfg.f, seed=2)))
+    y = G.empty_features(cfg.n, cfg.f, dev)
     G.gsp_spmm(gn, x, f=cfg.f, y=y)
     with rng(f"ncu|{cfg.name}|a3_spmm"):
         G.gsp_spmm(gn, x, f=cfg.f, y=y)
