@@ -86,44 +86,6 @@ __device__ __forceinline__ void stat_load_async(float *T, int64_t e0, int cnt, c
   }
 }
 
-// the entries of nb rows -> T back to back: row i's cnt_i entries (CSR start
-// tab_start[i]) at tile offset tab_off[i]; tab_off[nb] = tot.  Every position
-// is looked up (nb <= 32 / H rows), all column loads of a round are issued
-// before their cp.async copies, and all copies before the one wait.
-template <int H, bool kScores>
-__device__ __forceinline__ void stat_load_rows(float *T, const int *tab_off, const int64_t *tab_start, int nb, int tot,
-                                               const int32_t *__restrict__ col, const float *__restrict__ er,
-                                               const float *logits, int lane) {
-  auto src = [&](int p) {  // CSR entry of tile position p
-    int i = 0;
-    while (i + 1 < nb && tab_off[i + 1] <= p) ++i;
-    return tab_start[i] + (p - tab_off[i]);
-  };
-  if (kScores) {
-    constexpr int kV = H >= 4 ? 4 : H;
-    constexpr int kU = 4;
-    for (int b0 = 0; b0 < tot; b0 += 32 * kU) {
-      int c[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int p = b0 + lane + 32 * u;
-        c[u] = p < tot ? __ldg(col + src(p)) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int p = b0 + lane + 32 * u;
-        if (p < tot) {
-#pragma unroll
-          for (int q = 0; q < H; q += kV) cp_async<kV * 4>(T + p * H + q, er + (int64_t)c[u] * H + q);
-        }
-      }
-    }
-  } else {
-    for (int k = lane; k < tot * H; k += 32) cp_async<4>(T + k, logits + src(k / H) * H + (k % H));
-  }
-  cp_async_wait_all();
-}
-
 template <int H, bool kScores>
 __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const int32_t *__restrict__ col,
                                           const float *__restrict__ er, const float *logits, int lane) {
@@ -140,52 +102,34 @@ __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const i
 // with slope >= 0 and IEEE rounding are monotone) -- exactly; slope < 0 takes
 // the fp64 max of the scores.
 template <int H, bool kScores, bool kApply>
-__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, const uint8_t *s_ord, int64_t rbase,
-                                                int64_t n_rows, const int32_t *__restrict__ col,
-                                                const float *__restrict__ el, const float *__restrict__ er,
-                                                const float *logits, double slope, GatStat *__restrict__ st,
-                                                float *alpha, int warp, int lane, int *tab_off,
-                                                int64_t *tab_start) {
+__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
+                                                const int32_t *__restrict__ col, const float *__restrict__ el,
+                                                const float *__restrict__ er, const float *logits, double slope,
+                                                GatStat *__restrict__ st, float *alpha, int warp, int lane) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int RPW = 32 / H;
   const int rl = lane / H, h = lane % H;
-  const int base = warp * RPW;  // the warp's rows are s_ord[base .. base + RPW)
+  const int base = warp * RPW;  // CTA-local index of the warp's first row
+  auto deg = [&](int k) { return s_rp[base + k + 1] - s_rp[base + k]; };
   int k = 0;
   while (k < RPW) {
-    // rows k .. k2-1 of the warp's (degree-sorted) rows that fit the tile
-    // together; their entries are staged back to back (row k at offset 0)
-    int k2 = k, tot = 0, off = 0;
-    while (k2 < RPW) {
-      const int q = s_ord[base + k2];
-      const int d = (int)(s_rp[q + 1] - s_rp[q]);
-      if (d > kTile) break;  // sorted: every later row is long too (own path)
-      if (tot + d > kTile) break;
-      if (k2 == rl) off = tot;
-      tot += d;
-      ++k2;
+    if (deg(k) > kTile) {  // a long row: its own path
+      ++k;
+      continue;
     }
-    if (k2 == k) break;  // only long rows remain
-    // stage the batch: lane i < k2 - k publishes row i's (tile offset, CSR
-    // start); every position of the batch is then one load of one lane, all
-    // issued before the single wait (rows are not contiguous in CSR)
+    // rows k .. k2-1: consecutive short rows whose entries (contiguous in CSR) fit the tile
+    const int64_t B0 = s_rp[base + k];
+    int k2 = k + 1;
+    while (k2 < RPW && deg(k2) <= kTile && s_rp[base + k2 + 1] - B0 <= kTile) ++k2;
     __syncwarp();
-    if (lane < k2 - k) {
-      const int q = s_ord[base + k + lane];
-      tab_start[lane] = s_rp[q];
-      int o = 0;
-      for (int i = k; i < k + lane; ++i) o += (int)(s_rp[s_ord[base + i] + 1] - s_rp[s_ord[base + i]]);
-      tab_off[lane] = o;
-    }
-    if (lane == 0) tab_off[k2 - k] = tot;
+    stat_load<H, kScores>(T, B0, (int)(s_rp[base + k2] - B0), col, er, logits, lane);
     __syncwarp();
-    stat_load_rows<H, kScores>(T, tab_off, tab_start, k2 - k, tot, col, er, logits, lane);
-    __syncwarp();
-    if (rl >= k && rl < k2) {
-      const int q = s_ord[base + rl];
-      const int64_t grow = rbase + q, b = s_rp[q];
-      const int d = (int)(s_rp[q + 1] - b);
-      if (d > 0 && grow < n_rows) {
-        float *Tr = T + off * H + h;
+    const int64_t grow = rbase + base + rl;
+    if (rl >= k && rl < k2 && grow < n_rows) {
+      const int64_t b = s_rp[base + rl];
+      const int d = (int)(s_rp[base + rl + 1] - b);
+      if (d > 0) {
+        float *Tr = T + (b - B0) * H + h;
         const double el_u = kScores ? (double)__ldg(el + grow * H + h) : 0.0;
         float mr = -INFINITY;
         for (int j = 0; j < d; ++j) mr = fmaxf(mr, Tr[j * H]);
@@ -213,33 +157,6 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, c
       }
     }
     k = k2;
-  }
-}
-
-// Sort the CTA's rows by degree in groups of 32 (warp bitonic sort on
-// (degree, index) -- unique keys, so the order is deterministic): the warps
-// then get rows of similar length and the lanes of a warp (one per (row,
-// head)) finish together.  Long rows sort last.
-__device__ __forceinline__ void stat_sort_rows(const int64_t *s_rp, uint8_t *s_ord, int kRows, int lane) {
-  for (int g = 0; g < kRows; g += 32) {
-    const int idx = g + lane;
-    long long key = idx < kRows ? (long long)(s_rp[idx + 1] - s_rp[idx]) : (1ll << 62);
-    int id = idx;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const long long ok = __shfl_xor_sync(0xffffffffu, key, j);
-        const int oi = __shfl_xor_sync(0xffffffffu, id, j);
-        const bool other_less = ok < key || (ok == key && oi < id);
-        const bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
-        if (keep_min ? other_less : !other_less) {
-          key = ok;
-          id = oi;
-        }
-      }
-    }
-    if (idx < kRows) s_ord[idx] = (uint8_t)id;
   }
 }
 
@@ -276,11 +193,6 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   __shared__ int s_cnt[kSlots];
   __shared__ volatile int s_done[kSlots];
   __shared__ int64_t s_rp[kRows + 1];
-  __shared__ int s_long[kRows];
-  __shared__ uint8_t s_ord[kRows];
-  __shared__ int s_tab_off[kStatWarps][32 / H + 1];
-  __shared__ int64_t s_tab_start[kStatWarps][32 / H];
-  __shared__ int s_nlong;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int h = lane % H, part = lane / H;
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
@@ -291,19 +203,26 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
     s_done[tid] = 0;
   }
   __syncthreads();
-  if (warp == 0) {
-    int nl = 0;
-    for (int r0 = 0; r0 < kRows; r0 += 32) {
-      const bool lg = r0 + lane < kRows && (s_rp[r0 + lane + 1] - s_rp[r0 + lane]) > kTile;
-      const unsigned bl = __ballot_sync(0xffffffffu, lg);
-      if (lg) s_long[nl + __popc(bl & ((1u << lane) - 1u))] = r0 + lane;
-      nl += __popc(bl);
-    }
-    if (lane == 0) s_nlong = nl;
-    stat_sort_rows(s_rp, s_ord, kRows, lane);
+  // every warp finds the CTA's long rows itself (ballots over s_rp): no second
+  // CTA barrier before the warps start working
+  constexpr int kMasks = (kRows + 31) / 32;
+  unsigned lm[kMasks];
+  int nlong = 0;
+#pragma unroll
+  for (int q = 0; q < kMasks; ++q) {
+    const int r = q * 32 + lane;
+    lm[q] = __ballot_sync(0xffffffffu, r < kRows && (s_rp[r + 1] - s_rp[r]) > kTile);
+    nlong += __popc(lm[q]);
   }
-  __syncthreads();
-  const int nlong = s_nlong;
+  auto long_row = [&](int k) {  // CTA-local index of the k-th long row (index order)
+#pragma unroll
+    for (int q = 0; q < kMasks; ++q) {
+      const int c = __popc(lm[q]);
+      if (k < c) return q * 32 + (int)__fns(lm[q], 0, k + 1);
+      k -= c;
+    }
+    return 0;
+  };
   float *T = s_tile[warp];
   // ---- 1. long rows: per-warp partials, merged by the last warp to arrive
   for (int k0 = 0; k0 < nlong; k0 += kSlots) {
@@ -317,7 +236,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       __syncthreads();
     }
     for (int k = 0; k < kn; ++k) {
-      const int lr = s_long[k0 + k];
+      const int lr = long_row(k0 + k);
       const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
       const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
       double m = -INFINITY, sum = 0.0;
@@ -390,11 +309,11 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, s_ord, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane, s_tab_off[warp], s_tab_start[warp]);
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
     // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
     if (kApply) {
       for (int k = 0; k < kn; ++k) {
-        const int lr = s_long[k0 + k];
+        const int lr = long_row(k0 + k);
         const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
         if (b + (int64_t)warp * kTile >= e1) continue;
         const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
@@ -414,7 +333,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
   }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, s_ord, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane, s_tab_off[warp], s_tab_start[warp]);
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.

@@ -46,5 +46,16 @@ for f in (5, 128, 300):
     xh = torch.from_numpy(features(n, f, (f + 3) // 4 * 4, seed=f)).to(dev).half()
     G.gsp_spmm_f16(gn, xh, f=f)
 G.gsp_gat_aggregate(g, el, er, z, H, D, single_launch=True)
+# round 2: single-head / 2-head softmax with long rows (partial merge path), validate mode,
+# normalisation without deg_out, the 128-byte feature layout
+for hh in (1, 2, 16):
+    G.gsp_edge_softmax(g, torch.from_numpy(uniform((g.nnz, hh), seed=hh)).to(dev), hh)
+G.gsp_set_flags(G.GSP_VALIDATE)
+G.gsp_gat_aggregate(g, el, er, z, H, D)
+G.gsp_set_flags(0)
+G.gsp_sym_normalize(g, keep_deg=False)
+xa = G.empty_features(n, 602, dev)
+xa.copy_(torch.from_numpy(features(n, 602, 602, seed=9)))
+G.gsp_spmm(gn, xa)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
