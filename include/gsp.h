@@ -279,21 +279,27 @@ gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, const float *z,
  *   s[e,h]  = LeakyReLU(el[u,h] + er[v,h]; negative_slope)     e = (u,v), A13
  *   alpha   = edge softmax of s over row u, per head
  *   Y[u,h,:] = sum_e alpha[e,h] Z[v,h,:]
- * Two schedules, same result up to fp rounding of the statistics:
- *  - ws given (>= gsp_gat_workspace bytes, 16-byte aligned, heads | 32): a
- *    statistics launch (one warp per row for all heads: max and sum of exp
- *    in fp64 with warp-shuffle xor trees) writes (m, 1/S) per (row,
- *    head) into ws, then the aggregate launch forms alpha on the fly;
+ * Three schedules, same result up to fp rounding of the statistics, chosen
+ * by the workspace (16-byte aligned; heads | 32 for the first two):
+ *  - ws >= gsp_gat_workspace bytes (128-byte aligned) and alpha_out NULL:
+ *    "staged".  A statistics launch (lane per (row, head); long rows as
+ *    per-warp partials merged in warp order) writes alpha HEAD-MAJOR
+ *    into ws ([H][round_up(nnz, 32)] fp32); the aggregate launch stages the
+ *    alpha runs of its slab's heads with the CSR window (TMA bulk copies) and
+ *    gathers Z with weights read from shared memory;
+ *  - ws >= n_rows * heads * 16 bytes (or alpha_out requested): the statistics
+ *    launch writes (m, 1/S) per (row, head) and the aggregate forms alpha on
+ *    the fly (several whole heads per team);
  *  - ws NULL (or too small): ONE launch; the team that owns a (row, head)
  *    first reduces the row's statistics (hub rows: the whole CTA) and then
  *    runs the fused score -> softmax -> aggregate pass.
- * Per-edge scores and alpha are never materialised unless alpha_out is
- * non-NULL.
+ * Per-edge messages (alpha * Z rows) are never materialised; per-edge alpha
+ * only in the staged schedule's workspace or when alpha_out is non-NULL.
  *   el  device fp32 [a->n_rows][heads];  er device fp32 [a->n_cols][heads]
  *   z   device fp32 [a->n_cols][ldz] ([H][D]);  y device fp32 [a->n_rows][ldy]
  *   alpha_out  device fp32 [nnz][heads] or NULL
- *   ws  NULL, or device workspace of gsp_gat_workspace(a, heads) bytes
- *       (= n_rows * heads * 16: fp64 max + fp32 1/S per (row, head))
+ *   ws  NULL, or device workspace of up to gsp_gat_workspace(a, heads) bytes
+ *       (= max(n_rows * heads * 16, heads * round_up(nnz, 32) * 4))
  * The score is formed in fp64 (el + er, slope multiply, minus the row max) and
  * rounded once before the fp32 exponential.
  */

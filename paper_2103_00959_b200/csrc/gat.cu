@@ -105,7 +105,8 @@ template <int H, bool kScores, bool kApply>
 __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
                                                 const int32_t *__restrict__ col, const float *__restrict__ el,
                                                 const float *__restrict__ er, const float *logits, double slope,
-                                                GatStat *__restrict__ st, float *alpha, int warp, int lane) {
+                                                GatStat *__restrict__ st, float *alpha, int64_t ahs, float *winv,
+                                                int warp, int lane) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int RPW = 32 / H;
   const int rl = lane / H, h = lane % H;
@@ -146,7 +147,11 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
         }
         const float inv_s = (float)(1.0 / sum);
         if (kApply) {
-          for (int j = 0; j < d; ++j) alpha[(b + j) * H + h] = Tr[j * H] * inv_s;
+          if (ahs == 0) {
+            for (int j = 0; j < d; ++j) alpha[(b + j) * H + h] = Tr[j * H] * inv_s;
+          } else {
+            winv[lane] = inv_s;  // head-major: written below, one (row, head) run per instruction
+          }
         } else {
           GatStat g;
           g.m = m;
@@ -154,6 +159,17 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
           g.pad = 0.f;
           st[grow * H + h] = g;
         }
+      }
+    }
+    if (kApply && ahs != 0) {  // head-major alpha [H][ahs]: coalesced runs per (row, head)
+      __syncwarp();
+      for (int q = k * H; q < k2 * H; ++q) {
+        const int rr = q / H, hh = q % H;
+        const int64_t b = s_rp[base + rr];
+        const int d = (int)(s_rp[base + rr + 1] - b);
+        if (rbase + base + rr >= n_rows) continue;
+        const float iv = winv[q];
+        for (int j = lane; j < d; j += 32) alpha[hh * ahs + b + j] = T[(b - B0 + j) * H + hh] * iv;
       }
     }
     k = k2;
@@ -180,7 +196,8 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
                                                                   const float *__restrict__ el,
                                                                   const float *__restrict__ er, const float *logits,
                                                                   double slope, int64_t n_rows,
-                                                                  GatStat *__restrict__ st, float *alpha) {
+                                                                  GatStat *__restrict__ st, float *alpha,
+                                                                  int64_t ahs) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int kRows = kStatWarps * (32 / H);  // rows per CTA (32 / H per warp: lane = (row, head))
   constexpr int kSlots = StatSlots<H>::kSlots;
@@ -193,6 +210,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   __shared__ int s_cnt[kSlots];
   __shared__ volatile int s_done[kSlots];
   __shared__ int64_t s_rp[kRows + 1];
+  __shared__ float s_winv[kStatWarps][32];  // per warp: 1 / S of its (row, head) lanes (head-major apply)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int h = lane % H, part = lane / H;
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
@@ -309,7 +327,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, s_winv[warp], warp, lane);
     // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
     if (kApply) {
       for (int k = 0; k < kn; ++k) {
@@ -328,19 +346,21 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
           stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
           __syncwarp();
           for (int j = part; j < cnt; j += P)
-            alpha[(c0 + j) * H + h] = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
+            alpha[ahs ? h * ahs + c0 + j : (c0 + j) * H + h] =
+                expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
         }
       }
     }
   }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, warp, lane);
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, s_winv[warp], warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.
 template <bool kScores, bool kApply>
 __global__ void row_stats_thread(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                                  const float *__restrict__ el, const float *__restrict__ er, const float *logits,
-                                 double slope, int H, int64_t n_rows, GatStat *__restrict__ st, float *alpha) {
+                                 double slope, int H, int64_t n_rows, GatStat *__restrict__ st, float *alpha,
+                                 int64_t ahs) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_rows * H) return;
   const int64_t r = t / H;
@@ -362,7 +382,7 @@ __global__ void row_stats_thread(const int64_t *__restrict__ rp, const int32_t *
   for (int64_t e = b; e < e1; ++e) s += (double)expf((float)(score(e) - m));
   if (kApply) {
     const float inv_s = (float)(1.0 / s);
-    for (int64_t e = b; e < e1; ++e) alpha[e * H + h] = expf((float)(score(e) - m)) * inv_s;
+    for (int64_t e = b; e < e1; ++e) alpha[ahs ? h * ahs + e : e * H + h] = expf((float)(score(e) - m)) * inv_s;
     return;
   }
   GatStat g;
@@ -374,7 +394,7 @@ __global__ void row_stats_thread(const int64_t *__restrict__ rp, const int32_t *
 
 template <bool kScores, bool kApply>
 static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *er, const float *logits, double slope,
-                               int H, GatStat *st, float *alpha, cudaStream_t s) {
+                               int H, GatStat *st, float *alpha, cudaStream_t s, int64_t ahs = 0) {
   if (a->n_rows == 0) return GSP_OK;
   const float *vsrc = kScores ? er : logits;
   const bool vec_ok = H < 4 ? (H == 1 || aligned8(vsrc)) : aligned16(vsrc);
@@ -383,7 +403,7 @@ static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *e
 #define GSP_STATS_H(HH)                                                                                       \
   case HH:                                                                                                   \
     row_stats_warp<HH, kScores, kApply><<<blocks, kStatWarps * 32, 0, s>>>(a->row_ptr, a->col_idx, el, er,     \
-                                                                         logits, slope, a->n_rows, st, alpha); \
+                                                                         logits, slope, a->n_rows, st, alpha, ahs); \
     break;
     switch (H) {
       GSP_STATS_H(1) GSP_STATS_H(2) GSP_STATS_H(4) GSP_STATS_H(8) GSP_STATS_H(16) GSP_STATS_H(32)
@@ -392,7 +412,7 @@ static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *e
   } else {
     const int64_t blocks = ceil_div(a->n_rows * H, 256);
     row_stats_thread<kScores, kApply><<<(unsigned)blocks, 256, 0, s>>>(a->row_ptr, a->col_idx, el, er, logits,
-                                                                        slope, H, a->n_rows, st, alpha);
+                                                                        slope, H, a->n_rows, st, alpha, ahs);
   }
   return check_launch("row_stats");
 }
@@ -575,10 +595,18 @@ extern "C" gsp_status gsp_attn_project(int64_t n, int32_t heads, int64_t d, cons
   return check_launch("attn_project");
 }
 
+// alpha head-major [H][ahs] for the two-launch staged schedule: ahs = nnz rounded
+// up to 32 entries, so every head's run starts 128-byte aligned (TMA bulk copies)
+static int64_t gat_ahs(const gsp_csr *a) { return (std::max<int64_t>(a->nnz, 1) + 31) / 32 * 32; }
+static size_t gat_hm_bytes(const gsp_csr *a, int heads) { return (size_t)gat_ahs(a) * heads * 4; }
+static size_t gat_stat_bytes(const gsp_csr *a, int heads) {
+  return (size_t)std::max<int64_t>(a->n_rows, 0) * heads * sizeof(GatStat);  // (m, 1/S) per (row, head)
+}
+
 extern "C" gsp_status gsp_gat_workspace(const gsp_csr *a, int32_t heads, size_t *ws_bytes) {
   clear_detail();
   if (!a || heads <= 0 || !ws_bytes) return fail(GSP_ERR_INVALID_ARG, "gsp_gat_workspace: bad argument");
-  *ws_bytes = (size_t)std::max<int64_t>(a->n_rows, 0) * heads * sizeof(GatStat);  // (m, 1/S) per (row, head)
+  *ws_bytes = std::max(gat_stat_bytes(a, heads), gat_hm_bytes(a, heads));
   return GSP_OK;
 }
 
@@ -611,11 +639,32 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   // for all heads, then the aggregate, several whole heads per team);
   // otherwise one launch with the statistics reduced inside the aggregate
   // kernel, one head per team (fp64 row state in registers)
-  const size_t need = (size_t)a->n_rows * heads * sizeof(GatStat);
-  const bool pre = ws && ws_bytes >= need && aligned16(ws) && 32 % heads == 0;
+  //   three schedules, by workspace:
+  //  * >= gat_hm_bytes (the size gsp_gat_workspace reports), no alpha_out:
+  //    the statistics launch writes alpha head-major [H][ahs]; the aggregate
+  //    stages the slab's heads of it with the CSR window (TMA) and gathers
+  //    with weights read from shared memory (WeightAlphaHM);
+  //  * >= gat_stat_bytes: statistics (m, 1/S) only, alpha formed in the
+  //    aggregate (WeightGatPre) -- also the schedule that writes alpha_out;
+  //  * otherwise one launch (WeightGat).
+  const bool hm = ws && ws_bytes >= gat_hm_bytes(a, heads) && reinterpret_cast<uintptr_t>(ws) % 128 == 0 &&
+                  !alpha_out && 32 % heads == 0 && aligned16(a->col_idx) && a->nnz > 0;
+  const bool pre = !hm && ws && ws_bytes >= gat_stat_bytes(a, heads) && aligned16(ws) && 32 % heads == 0;
   EngineLaunch L;
-  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, pre ? kMaxHpt : 1);
+  st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, (pre || hm) ? kMaxHpt : 1);
   if (st) return st;
+  if (hm) {
+    // keep the staged window (col + hpt weight runs) within ~42 KB so four
+    // CTAs still fit on an SM (the 64-register budget allows four)
+    const int hpt = engine_hpt(L, d, heads);
+    const int64_t win_max = 43008 / (4 * (1 + hpt));
+    int64_t c = ((win_max - kHub - 8) / 512) * 512;
+    if (c < 512) c = 512;
+    if (c < L.block_nnz) {
+      st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, (int32_t)c, &L, kMaxHpt);
+      if (st) return st;
+    }
+  }
   EngineParams p;
   p.row_ptr = a->row_ptr;
   p.col = a->col_idx;
@@ -634,6 +683,18 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   p.bias = bias;
   p.act = act;
   if ((st = engine_ldxv(p, L, a->n_cols, ldz))) return st;
+  if (hm) {
+    float *alpha_hm = static_cast<float *>(ws);
+    const int64_t ahs = gat_ahs(a);
+    if ((st = launch_stats<true, true>(a, el, er, nullptr, negative_slope, heads, nullptr, alpha_hm, s, ahs)))
+      return st;
+    if (p.stage) {
+      p.stage_hm = alpha_hm;
+      p.stage_hm_stride = ahs;
+      p.stage_heads = p.hpt;
+    }
+    return engine_launch(L, p, WeightAlphaHM{alpha_hm, ahs}, s);
+  }
   if (pre) {
     GatStat *stat = static_cast<GatStat *>(ws);
     if ((st = launch_stats<true, false>(a, el, er, nullptr, negative_slope, heads, stat, nullptr, s))) return st;

@@ -36,6 +36,8 @@
 
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gsp {
@@ -258,6 +260,8 @@ __device__ __forceinline__ void store_cols(float *p, const float (&r)[V], int nv
 struct Window {
   const int32_t *scol;
   const float *sval;  // NULL when values are not staged
+  const float *swt;   // per-head weights [hpt][cap] staged by TMA (WeightAlphaHM), else NULL
+  int64_t cap;        // window capacity (entries)
   int64_t wb, we;
   __device__ __forceinline__ bool in(int64_t e) const { return e >= wb && e < we; }
   __device__ __forceinline__ int col(const int32_t *g, int64_t e) const { return in(e) ? scol[e - wb] : __ldcs(g + e); }
@@ -324,6 +328,31 @@ struct WeightAlpha {  // multi-head SpMM with given alpha [nnz][H]
   };
   __device__ __forceinline__ Row row(int64_t, int h, bool, void *) const { return Row{alpha, heads, h}; }
 };
+
+// Multi-head SpMM with alpha HEAD-MAJOR [H][ahs] (the fused GAT's two-launch
+// schedule writes it so; ahs = nnz rounded up to 32): the window's weights of
+// the slab's hpt heads are staged by the TMA engine with the column indices
+// (one contiguous run per head), so the gather loop reads weights from shared
+// memory with no per-segment loads; hub rows beyond the window read them from
+// global memory.
+struct WeightAlphaHM {
+  const float *alpha;
+  int64_t ahs;
+  struct Row {
+    static constexpr bool kUnit = false, kComputed = false, kStagedVal = false, kMultiHead = true, kInStats = false;
+    static constexpr bool kStagedHeads = true;
+    const float *alpha;
+    int64_t ahs;
+    int h;  // first head of the team's slab
+    __device__ __forceinline__ float w(int64_t e, int, int hh) const { return __ldcs(alpha + (h + hh) * ahs + e); }
+  };
+  __device__ __forceinline__ Row row(int64_t, int h, bool, void *) const { return Row{alpha, ahs, h}; }
+};
+
+template <class R, class = void>
+struct HasStagedHeads : std::false_type {};
+template <class R>
+struct HasStagedHeads<R, std::void_t<decltype(R::kStagedHeads)>> : std::bool_constant<R::kStagedHeads> {};
 
 struct GatStat {  // per (row, head) softmax statistics (standalone edge softmax)
   double m;       // row max of the score (fp64)
@@ -394,6 +423,9 @@ struct EngineParams {
   int y_vec_ok;      // y base and ldy allow V-wide stores
   int64_t nnz;
   const float *stage_val;  // val array to stage in smem (NULL: none)
+  const float *stage_hm;   // head-major weights to stage per slab head (WeightAlphaHM), NULL: none
+  int64_t stage_hm_stride; // elements between heads of stage_hm
+  int stage_heads;         // heads staged per slab (= hpt) when stage_hm
   int stage;               // 1: stage col (and stage_val) in shared memory
   int win_cap;             // window capacity in entries (multiple of 4)
   int mean;                // GSpMM mean: divide the row sum by the row's entry count
@@ -570,6 +602,7 @@ __device__ __forceinline__ void row_segments(const EngineParams &p, const Window
     if (seg_in) {
       sc = win.scol + (e0 - win.wb);
       if (Row::kStagedVal && win.sval) sw = win.sval + (e0 - win.wb);
+      else if (HasStagedHeads<Row>::value && win.swt) sw = win.swt + hl * win.cap + (e0 - win.wb);
       else scratch = !Row::kUnit;
     } else {
       sc = tc;
@@ -732,6 +765,10 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
   const int64_t rend = (blk == p.nblk - 1) ? p.n_rows : s_rb[1];
   int32_t *s_col = reinterpret_cast<int32_t *>(s_dyn);
   float *s_val = reinterpret_cast<float *>(s_dyn + (size_t)p.win_cap * 4);
+  // staged per-head weights (WeightAlphaHM): [stage_heads][win_cap] after col (and val)
+  float *s_wt = reinterpret_cast<float *>(s_dyn + (size_t)p.win_cap * 4 * (p.stage_val ? 2 : 1));
+  const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
+  const int nst = (p.stage && p.stage_hm) ? p.stage_heads : 0;         // weight arrays staged per chunk
 
   // 0. TMA: stage the CSR window [wb, we) -- every non-hub row of this block
   //    lies inside [row_ptr[rbeg], row_ptr[rbeg] + block_nnz + kHub)
@@ -747,11 +784,14 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
       for (int k = 0; k < kStageChunks; ++k) {
         const int64_t c0 = wb + k * ch, c1 = min(we, c0 + ch);
         const uint32_t n = c1 > c0 ? (uint32_t)(c1 - c0) : 0u;
-        const uint32_t bytes = n * 4u * (p.stage_val ? 2u : 1u);
+        const uint32_t bytes = n * 4u * ((p.stage_val ? 2u : 1u) + (uint32_t)nst);
         mbar_arrive_expect_tx(&s_bar[k], bytes);
         if (n) {
           bulk_g2s(s_col + (c0 - wb), p.col + c0, n * 4u, &s_bar[k]);
           if (p.stage_val) bulk_g2s(s_val + (c0 - wb), p.stage_val + c0, n * 4u, &s_bar[k]);
+          for (int hh = 0; hh < nst; ++hh)
+            bulk_g2s(s_wt + (size_t)hh * p.win_cap + (c0 - wb), p.stage_hm + (int64_t)(head + hh) * p.stage_hm_stride + c0,
+                     n * 4u, &s_bar[k]);
         }
       }
     }
@@ -768,7 +808,6 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
   const int64_t last_vec = p.f > 0 ? ((p.f - 1) / V) * V : 0;  // first column of the last valid vector
   const auto *xb = reinterpret_cast<const typename XE::Ptr *>(reinterpret_cast<const typename XE::Elem *>(p.x) +
                                                                 (active ? col0 : last_vec));
-  const int head = p.head_dim ? (int)((slab * SW) / p.head_dim) : 0;  // first head of the slab
   const int hl = (kMH && p.hpt > 1) ? (int)((gl * V) / p.head_dim) : 0;  // this lane's head offset
   const bool first_slab = p.head_dim ? ((slab * SW) % p.head_dim) == 0 : true;
 
@@ -782,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocksFor<W, XE>::value) engine_k
   }
   __syncthreads();
   const int nhub = s_nhub;  // <= kMaxHubPerBlock by the host's block_nnz cap
-  const Window win{s_col, p.stage_val ? s_val : nullptr, s_win[0], s_win[1]};
+  const Window win{s_col, p.stage_val ? s_val : nullptr, nst ? s_wt : nullptr, p.win_cap, s_win[0], s_win[1]};
   const int64_t wchunk = s_win[2];
   int ready = 0;  // chunks this thread has seen complete
 #ifndef GSP_WINDOW_PER_ROW_WAIT
@@ -957,6 +996,9 @@ inline void engine_stage(EngineParams &p, const EngineLaunch &L, int64_t nnz, co
   p.stage = (nnz > 0 && aligned16(col)) ? 1 : 0;
   p.stage_val = (p.stage && val && aligned16(val)) ? val : nullptr;
   p.win_cap = (int)(((L.block_nnz + kHub + 8) + 3) & ~int64_t(3));
+  p.stage_hm = nullptr;
+  p.stage_hm_stride = 0;
+  p.stage_heads = 0;
   p.mean = 0;
   p.hpt = 1;
   p.acc = nullptr;
@@ -973,7 +1015,8 @@ gsp_status engine_launch_vg(const EngineLaunch &L, const EngineParams &p, const 
   const int64_t grid = L.nslab * L.nblk;
   if (grid <= 0) return GSP_OK;
   if (grid >= (int64_t(1) << 31)) return fail(GSP_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", (long long)grid);
-  const size_t smem = p.stage ? (size_t)p.win_cap * (p.stage_val ? 8 : 4) : 0;
+  const size_t smem =
+      p.stage ? (size_t)p.win_cap * 4 * ((p.stage_val ? 2 : 1) + (p.stage_hm ? p.stage_heads : 0)) : 0;
   if (smem > 0) {  // static + dynamic may exceed the 48 KB default: raise the cap once per device
     static std::atomic<int> granted[64];  // per device: largest dynamic smem already granted
     int dev = 0;
@@ -1057,6 +1100,7 @@ gsp_status engine_launch_f16(const EngineLaunch &L, const EngineParams &p, const
   X(WeightVal, RedMin, maxmin)  \
   X(WeightOne, RedMin, maxmin)  \
   X(WeightAlpha, RedSum, alpha) \
+  X(WeightAlphaHM, RedSum, alpha) \
   X(WeightGat, RedSum, gat)     \
   X(WeightGatPre, RedSum, gat)
 #ifndef GSP_ENGINE_INSTANTIATE
