@@ -178,17 +178,32 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
 
 // Long rows (> kTile entries) are cut into tile-sized chunks; warp w takes
 // chunks w, w + 8, ... and reduces them to a partial (m_w, s_w) with its OWN
-// maximum m_w (s_w = sum of exp(s - m_w), fp64).  The last warp to arrive
-// merges the 8 partials in warp order -- M = max m_w, S = sum_w s_w exp(m_w - M)
-// (fp64) -- so no warp ever waits at a CTA barrier for a long row: long rows
-// are processed first, the warps then continue with their short rows, and
-// only the alpha writes of a long row (kApply) wait for its merged (M, S).
+// maximum m_w (s_w = sum of exp(s - m_w), fp64).  Warp k % 8 merges long row
+// k's 8 partials in warp order -- M = max m_w, S = sum_w s_w exp(m_w - M)
+// (fp64) -- after a named barrier the other warps only ARRIVE at, so they go
+// on with the next long row and their short rows; only the alpha writes of a
+// long row (kApply) wait (second named barrier) for its merged (M, S).
 // Partials of up to kSlots long rows live in shared memory; a CTA with more
 // long rows processes them in batches separated by a CTA barrier.
-template <int H>
+// Slots: <= 8 KB of partials (48 KB static smem) and one named barrier per
+// long row (two with kApply) out of the 15 a CTA has besides barrier 0.
+template <int H, bool kApply>
 struct StatSlots {
-  static constexpr int kSlots = (64 / H) < 16 ? (64 / H) : 16;  // <= 8 KB of partials (48 KB static smem)
+  static constexpr int kMem = (64 / H) < 16 ? (64 / H) : 16;
+  static constexpr int kBar = kApply ? 7 : 15;
+  static constexpr int kSlots = kMem < kBar ? kMem : kBar;
 };
+
+// named CTA barriers (bar.sync / bar.arrive over `n` threads): the warps that
+// produce a long row's partials arrive without waiting; only the warp that
+// merges them (and, with kApply, the warps that then need the merged result)
+// wait -- ordered for the memory model and for compute-sanitizer's racecheck
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 template <int H, bool kScores, bool kApply>
 __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp(const int64_t *__restrict__ rp,
@@ -200,15 +215,13 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
                                                                   int64_t ahs) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int kRows = kStatWarps * (32 / H);  // rows per CTA (32 / H per warp: lane = (row, head))
-  constexpr int kSlots = StatSlots<H>::kSlots;
+  constexpr int kSlots = StatSlots<H, kApply>::kSlots;
   constexpr int P = 32 / H;
   __shared__ __align__(16) float s_tile[kStatWarps][kStatTileFloats];
   __shared__ double s_pm[kSlots][kStatWarps][H];  // partial max (score) per slot, warp, head
   __shared__ double s_ps[kSlots][kStatWarps][H];  // partial sum of exp(s - m_w)
   __shared__ double s_M[kSlots][H];               // merged max (kApply)
   __shared__ float s_inv[kSlots][H];              // merged 1 / S (kApply)
-  __shared__ int s_cnt[kSlots];
-  __shared__ volatile int s_done[kSlots];
   __shared__ int64_t s_rp[kRows + 1];
   __shared__ float s_winv[kStatWarps][32];  // per warp: 1 / S of its (row, head) lanes (head-major apply)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -216,10 +229,6 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
   // the CTA's row pointers and its long rows, once (nobody is busy yet)
   for (int i = tid; i <= kRows; i += kStatWarps * 32) s_rp[i] = __ldg(rp + min(rbase + i, n_rows));
-  if (tid < kSlots) {
-    s_cnt[tid] = 0;
-    s_done[tid] = 0;
-  }
   __syncthreads();
   // every warp finds the CTA's long rows itself (ballots over s_rp): no second
   // CTA barrier before the warps start working
@@ -245,14 +254,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   // ---- 1. long rows: per-warp partials, merged by the last warp to arrive
   for (int k0 = 0; k0 < nlong; k0 += kSlots) {
     const int kn = min(kSlots, nlong - k0);
-    if (k0 > 0) {  // slots are reused: every merge of the previous batch is complete
-      __syncthreads();
-      if (tid < kSlots) {
-        s_cnt[tid] = 0;
-        s_done[tid] = 0;
-      }
-      __syncthreads();
-    }
+    if (k0 > 0) __syncthreads();  // slots and barrier ids are reused: the previous batch is complete
     for (int k = 0; k < kn; ++k) {
       const int lr = long_row(k0 + k);
       const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
@@ -292,38 +294,36 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
         s_pm[k][warp][h] = m;
         s_ps[k][warp][h] = sum;
       }
-      __threadfence_block();
       __syncwarp();
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&s_cnt[k], 1) == kStatWarps - 1;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {  // merge the 8 partials in warp order
-        __threadfence_block();
-        if (lane < H) {
-          double M = -INFINITY;
-          for (int w = 0; w < kStatWarps; ++w) M = fmax(M, s_pm[k][w][lane]);
-          double S = 0.0;
-          for (int w = 0; w < kStatWarps; ++w) {
-            const double mw = s_pm[k][w][lane];
-            if (mw != -INFINITY) S += s_ps[k][w][lane] * exp(mw - M);
-            else S += s_ps[k][w][lane];
-          }
-          if (kApply) {
-            s_M[k][lane] = M;
-            s_inv[k][lane] = (float)(1.0 / S);
-          } else {
-            GatStat g;
-            g.m = M;
-            g.inv_s = (float)(1.0 / S);
-            g.pad = 0.f;
-            st[r * H + lane] = g;
-          }
+      const int bar_merge = 1 + (kApply ? 2 * k : k);
+      if (warp != k % kStatWarps) {
+        named_arrive(bar_merge, kStatWarps * 32);
+        continue;
+      }
+      named_sync(bar_merge, kStatWarps * 32);  // every warp's partial of row k is written
+      if (lane < H) {  // merge the 8 partials in warp order
+        double M = -INFINITY;
+        for (int w = 0; w < kStatWarps; ++w) M = fmax(M, s_pm[k][w][lane]);
+        double S = 0.0;
+        for (int w = 0; w < kStatWarps; ++w) {
+          const double mw = s_pm[k][w][lane];
+          if (mw != -INFINITY) S += s_ps[k][w][lane] * exp(mw - M);
+          else S += s_ps[k][w][lane];
         }
         if (kApply) {
-          __threadfence_block();
-          __syncwarp();
-          if (lane == 0) s_done[k] = 1;
+          s_M[k][lane] = M;
+          s_inv[k][lane] = (float)(1.0 / S);
+        } else {
+          GatStat g;
+          g.m = M;
+          g.inv_s = (float)(1.0 / S);
+          g.pad = 0.f;
+          st[r * H + lane] = g;
         }
+      }
+      if (kApply) {
+        __syncwarp();
+        named_arrive(bar_merge + 1, kStatWarps * 32);  // (M, 1/S) of row k published
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
@@ -333,11 +333,11 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       for (int k = 0; k < kn; ++k) {
         const int lr = long_row(k0 + k);
         const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
+        // every warp but the merging one meets the publishing warp here (even
+        // without a chunk of the row: the barrier counts all 8 warps)
+        if (warp != k % kStatWarps) named_sync(1 + 2 * k + 1, kStatWarps * 32);
         if (b + (int64_t)warp * kTile >= e1) continue;
         const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-        while (s_done[k] == 0) {
-        }
-        __threadfence_block();
         const double M = s_M[k][h];
         const float inv_s = s_inv[k][h];
         for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
