@@ -751,10 +751,22 @@ def main_dist(args):
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    gloo = args.dist_backend == "gloo"
+    if gloo:  # functional check of this path on a one-GPU box: ranks share the GPUs, host-staged all-gathers
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     G.lib()
+
+    def staged_gather(out, inp):
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, inp.cpu())
+        out.copy_(torch.cat(parts, 0))
+    ag = staged_gather if gloo else None
     peak, peak_kind = hbm_peak()
     cfg = CONFIGS[args.config]
     s, d = graph_for(cfg, seed=1)
@@ -764,7 +776,7 @@ def main_dist(args):
     n, nnz, f = cfg.n, gn.nnz, cfg.f
     # each rank generates the full X deterministically and keeps its own rows
     x_host = features(n, f, cfg.ld, seed=2)
-    op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev)
+    op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev, all_gather=ag)
     xs = torch.from_numpy(np.ascontiguousarray(x_host[op.r0:op.r1, :f])).to(dev)
     op.load_shard(xs)
     y = G.empty_features(op.rows, f, dev)
@@ -792,7 +804,7 @@ def main_dist(args):
     t_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
 
     def allmax(v):
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        t = torch.tensor([v], device="cpu" if gloo else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
     t_max = allmax(t_ms)
@@ -839,7 +851,7 @@ def main_dist(args):
         z = torch.from_numpy(uniform((c3.n, H * D), seed=3)).to(dev)
         al = torch.from_numpy(uniform((H, D), seed=6).reshape(-1)).to(dev)
         ar = torch.from_numpy(uniform((H, D), seed=7).reshape(-1)).to(dev)
-        gt = RowPartitionedGAT(g3, rank, world, H, D, head_groups=1, device=dev)
+        gt = RowPartitionedGAT(g3, rank, world, H, D, head_groups=1, device=dev, all_gather=ag)
         gt.load_shard(z[gt.r0:gt.r1])
         y3 = torch.empty((gt.rows, H * D), dtype=torch.float32, device=dev)
         ts3 = timer.cold(lambda: gt(al, ar, y3), args.warmup, 10)
@@ -869,6 +881,7 @@ def main_dist(args):
                        "allgather_GB/s_per_rank": recv / (t_comm * 1e-3) / 1e9 if world > 1 else None,
                        "rows_per_rank_max": op.npad, "bounds": op.bounds},
         "bitwise_equal_to_1gpu": bitwise,
+        "dist_backend": args.dist_backend,
         "e2e": {"value": ge / (te * 1e-3), "unit": "GE/s", "ms_per_step": te,
                 "h2d_bytes_per_step": int(n * f * 4), "d2h_bytes_per_step": int(n * f * 4),
                 "api": "RowPartitionedSpMM (gsp_csr_slice + NCCL all-gather + gsp_spmm), pinned host shards"},
@@ -909,6 +922,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--chunks", type=int, default=5, help="feature chunks (128-col aligned) for comm/compute overlap")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N-rank path on fewer GPUs (functional check, host-staged all-gathers)")
     ap.add_argument("--no-rows", action="store_true", help="headline only (skip the other configs' rows)")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

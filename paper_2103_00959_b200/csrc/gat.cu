@@ -93,6 +93,22 @@ __device__ __forceinline__ void stat_load(float *T, int64_t e0, int cnt, const i
   cp_async_wait_all();
 }
 
+// copy alpha values staged in the warp's tile (T[j][H], entries e0 .. e0+cnt)
+// to global alpha: [nnz][H] (ahs == 0: one contiguous run) or head-major
+// [H][ahs] (one contiguous run per head) -- 128-byte stores either way
+template <int H>
+__device__ __forceinline__ void stat_store_alpha(const float *T, int64_t e0, int cnt, float *alpha, int64_t ahs,
+                                                 int lane) {
+  if (ahs == 0) {
+    float *dst = alpha + e0 * H;
+    for (int k = lane; k < cnt * H; k += 32) dst[k] = T[k];
+  } else {
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      for (int j = lane; j < cnt; j += 32) alpha[h * ahs + e0 + j] = T[j * H + h];
+  }
+}
+
 // Short rows (<= kTile entries): lane l of warp w owns (row w * RPW + l / H,
 // head l % H), RPW = 32 / H rows per warp, and reduces its row and head
 // SEQUENTIALLY in column order -- no shuffles, the warp's rows in parallel.
@@ -105,8 +121,8 @@ template <int H, bool kScores, bool kApply>
 __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
                                                 const int32_t *__restrict__ col, const float *__restrict__ el,
                                                 const float *__restrict__ er, const float *logits, double slope,
-                                                GatStat *__restrict__ st, float *alpha, int64_t ahs, float *winv,
-                                                int warp, int lane) {
+                                                GatStat *__restrict__ st, float *alpha, int64_t ahs, int warp,
+                                                int lane) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int RPW = 32 / H;
   const int rl = lane / H, h = lane % H;
@@ -147,11 +163,7 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
         }
         const float inv_s = (float)(1.0 / sum);
         if (kApply) {
-          if (ahs == 0) {
-            for (int j = 0; j < d; ++j) alpha[(b + j) * H + h] = Tr[j * H] * inv_s;
-          } else {
-            winv[lane] = inv_s;  // head-major: written below, one (row, head) run per instruction
-          }
+          for (int j = 0; j < d; ++j) Tr[j * H] *= inv_s;  // alpha, in the tile; stored below by the warp
         } else {
           GatStat g;
           g.m = m;
@@ -161,16 +173,9 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
         }
       }
     }
-    if (kApply && ahs != 0) {  // head-major alpha [H][ahs]: coalesced runs per (row, head)
+    if (kApply) {  // the batch's alpha (contiguous entries B0 .. B0 + tot) in 128-byte stores
       __syncwarp();
-      for (int q = k * H; q < k2 * H; ++q) {
-        const int rr = q / H, hh = q % H;
-        const int64_t b = s_rp[base + rr];
-        const int d = (int)(s_rp[base + rr + 1] - b);
-        if (rbase + base + rr >= n_rows) continue;
-        const float iv = winv[q];
-        for (int j = lane; j < d; j += 32) alpha[hh * ahs + b + j] = T[(b - B0 + j) * H + hh] * iv;
-      }
+      stat_store_alpha<H>(T, B0, (int)(s_rp[base + k2] - B0), alpha, ahs, lane);
     }
     k = k2;
   }
@@ -223,7 +228,6 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   __shared__ double s_M[kSlots][H];               // merged max (kApply)
   __shared__ float s_inv[kSlots][H];              // merged 1 / S (kApply)
   __shared__ int64_t s_rp[kRows + 1];
-  __shared__ float s_winv[kStatWarps][32];  // per warp: 1 / S of its (row, head) lanes (head-major apply)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int h = lane % H, part = lane / H;
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, s_winv[warp], warp, lane);
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
     // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
     if (kApply) {
       for (int k = 0; k < kn; ++k) {
@@ -346,13 +350,14 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
           stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
           __syncwarp();
           for (int j = part; j < cnt; j += P)
-            alpha[ahs ? h * ahs + c0 + j : (c0 + j) * H + h] =
-                expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
+            T[j * H + h] = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
+          __syncwarp();
+          stat_store_alpha<H>(T, c0, cnt, alpha, ahs, lane);
         }
       }
     }
   }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, s_winv[warp], warp, lane);
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.

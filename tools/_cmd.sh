@@ -1,4 +1,3 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r2i.log 2>&1
-bash tools/sanitize.sh > gpurun_out/sanitize_r2i.txt 2>&1
-SKIP_LAUNCH=1 bash tools/gpu_measure.sh r2i
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2i.csv python bench.py --steps 3 --warmup 3 --no-rows --no-secondary --no-e2e > gpurun_out/ncu_launch_bench_r2i.log 2>&1
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r2k.log 2>&1
+SKIP_BENCH=1 SKIP_LAUNCH=1 OPS="C3" bash tools/gpu_measure.sh r2k
+timeout 600 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "ncu|C3-flickr-gat8x64|a5-a7_gat_fused/" -o gpurun_out/prof_gat_r2k -f python tools/ncu_ops.py C3 > gpurun_out/ncu_gat_r2k.log 2>&1
