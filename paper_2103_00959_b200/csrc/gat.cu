@@ -31,6 +31,9 @@ namespace gsp {
 #ifndef GSP_STAT_MINB
 #define GSP_STAT_MINB 4
 #endif
+#ifndef GSP_STAT_COOP
+#define GSP_STAT_COOP 1
+#endif
 constexpr int kStatWarps = GSP_STAT_WARPS;  // warps per CTA
 constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
 
@@ -128,6 +131,12 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
   const int rl = lane / H, h = lane % H;
   const int base = warp * RPW;  // CTA-local index of the warp's first row
   auto deg = [&](int k) { return s_rp[base + k + 1] - s_rp[base + k]; };
+#if GSP_STAT_COOP
+  constexpr int P = RPW;
+  const int part = rl;
+  // el of the warp's rows, once: lane (r, h) holds el[row r][h]
+  const float el_l = (kScores && rbase + base + rl < n_rows) ? __ldg(el + (rbase + base + rl) * H + h) : 0.0f;
+#endif
   int k = 0;
   while (k < RPW) {
     if (deg(k) > kTile) {  // a long row: its own path
@@ -141,8 +150,51 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
     __syncwarp();
     stat_load<H, kScores>(T, B0, (int)(s_rp[base + k2] - B0), col, er, logits, lane);
     __syncwarp();
+#if GSP_STAT_COOP
+    // cooperative: the whole warp reduces one row at a time, lane (part, h)
+    // takes entries part, part + P, ... of head h (P = 32 / H), xor tree over
+    // the P parts -- no lane waits on a longer row of another lane
+    for (int q = k; q < k2; ++q) {
+      const int64_t grow = rbase + base + q;
+      if (grow >= n_rows) break;
+      const int64_t b = s_rp[base + q];
+      const int d = (int)(s_rp[base + q + 1] - b);
+      if (d == 0) continue;
+      float *Tr = T + (b - B0) * H + h;
+      const double el_u = kScores ? (double)__shfl_sync(0xffffffffu, el_l, q * H + h) : 0.0;
+      float mr = -INFINITY;
+      for (int j = part; j < d; j += P) mr = fmaxf(mr, Tr[j * H]);
+#pragma unroll
+      for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+      double m = stat_score<kScores>(mr, el_u, slope);
+      if (kScores && !(slope >= 0.0)) {
+        m = -INFINITY;
+        for (int j = part; j < d; j += P) m = fmax(m, stat_score<kScores>(Tr[j * H], el_u, slope));
+#pragma unroll
+        for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+      }
+      double sum = 0.0;
+      for (int j = part; j < d; j += P) {
+        const float ex = expf((float)(stat_score<kScores>(Tr[j * H], el_u, slope) - m));
+        sum += (double)ex;
+        if (kApply) Tr[j * H] = ex;  // own slot
+      }
+#pragma unroll
+      for (int off = H; off < 32; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      const float inv_s = (float)(1.0 / sum);
+      if (kApply) {
+        for (int j = part; j < d; j += P) Tr[j * H] *= inv_s;
+      } else if (part == 0) {
+        GatStat g;
+        g.m = m;
+        g.inv_s = inv_s;
+        g.pad = 0.f;
+        st[grow * H + h] = g;
+      }
+    }
+#endif
     const int64_t grow = rbase + base + rl;
-    if (rl >= k && rl < k2 && grow < n_rows) {
+    if (!GSP_STAT_COOP && rl >= k && rl < k2 && grow < n_rows) {
       const int64_t b = s_rp[base + rl];
       const int d = (int)(s_rp[base + rl + 1] - b);
       if (d > 0) {

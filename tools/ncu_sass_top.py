@@ -12,7 +12,12 @@ i = 0
 while rows[i][0] != 'Address':
     i += 1
 hdr = rows[i]
-data = [dict(zip(hdr, r)) for r in rows[i + 1:] if len(r) == len(hdr)]
+data = []
+for r in rows[i + 1:]:
+    if r and r[0] == 'Address':
+        break  # a second kernel's section: only the first is summarised
+    if len(r) == len(hdr):
+        data.append(dict(zip(hdr, r)))
 key = 'Warp Stall Sampling (All Samples)'
 iv = lambda d, k: int(d.get(k) or 0)
 tot = sum(iv(d, key) for d in data) or 1
