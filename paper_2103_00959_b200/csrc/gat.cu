@@ -12,10 +12,10 @@ namespace gsp {
 // value ... subtract ... exponent ... reduce ... the sum").  H (heads,
 // dividing 32) is a template parameter.  Grid: one CTA of 8 warps per
 // 8 * 32 / H rows; warp w owns RPW = 32 / H consecutive rows.
-//  * SHORT rows (<= kTile = 1024 / H entries): lane l owns (row l / H,
-//    head l % H) and reduces it sequentially in column order; the warp's
-//    rows are staged in its 4 KB shared tile T[j][H] by cp.async (no
-//    registers in flight), as many consecutive rows at a time as fit.
+//  * SHORT rows (<= kTile = 1024 / H entries): staged in the warp's 4 KB
+//    shared tile T[j][H] by cp.async (no registers in flight), as many
+//    consecutive rows at a time as fit, and reduced one row at a time by the
+//    whole warp (lane = (entry slot, head), xor tree over the slots).
 //  * LONG rows: cut into tile-sized chunks; warp w takes chunks w, w+8, ...
 //    and folds them into a partial (own max m_w, fp64 sum of exp(s - m_w));
 //    the last warp to arrive merges the 8 partials in warp order (no CTA
@@ -31,11 +31,16 @@ namespace gsp {
 #ifndef GSP_STAT_MINB
 #define GSP_STAT_MINB 4
 #endif
-#ifndef GSP_STAT_COOP
-#define GSP_STAT_COOP 1
-#endif
 constexpr int kStatWarps = GSP_STAT_WARPS;  // warps per CTA
 constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
+
+constexpr double kLog2e = 1.4426950408889634074;  // log2(e)
+// 2^a, hardware approximation (max error 2 ulp; subnormal results kept)
+__device__ __forceinline__ float ex2_approx(float a) {
+  float r;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
 
 template <bool kScores>
 __device__ __forceinline__ double stat_score(float t, double el_u, double slope) {
@@ -44,6 +49,20 @@ __device__ __forceinline__ double stat_score(float t, double el_u, double slope)
     return x >= 0.0 ? x : slope * x;
   }
   return (double)t;
+}
+
+// exp(s - m) for a stored value t (er of the column, or the logit), as the
+// short rows form it (see stat_short_rows): 2^((s - m) log2 e)
+template <bool kScores>
+__device__ __forceinline__ float stat_exp(float t, double el_u, double slope_l2e, double m) {
+  float a;
+  if (kScores) {
+    const double x = el_u + (double)t;
+    a = (float)fma(x, x >= 0.0 ? kLog2e : slope_l2e, -(m * kLog2e));
+  } else {
+    a = (t - (float)m) * (float)kLog2e;
+  }
+  return ex2_approx(a);
 }
 
 // global -> shared asynchronous copies (LDGSTS): the data never passes through
@@ -85,7 +104,12 @@ __device__ __forceinline__ void stat_load_async(float *T, int64_t e0, int cnt, c
   } else {
     const float *src = logits + e0 * H;  // cnt rows of H logits are contiguous
     const int nf = cnt * H;
-    for (int k = lane; k < nf; k += 32) cp_async<4>(T + k, src + k);
+    int k0 = 0;
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {  // T is 16-byte aligned: 16-byte copies, scalar tail
+      k0 = nf & ~3;
+      for (int k = 4 * lane; k < k0; k += 128) cp_async<16>(T + k, src + k);
+    }
+    for (int k = k0 + lane; k < nf; k += 32) cp_async<4>(T + k, src + k);
   }
 }
 
@@ -104,7 +128,27 @@ __device__ __forceinline__ void stat_store_alpha(const float *T, int64_t e0, int
                                                  int lane) {
   if (ahs == 0) {
     float *dst = alpha + e0 * H;
-    for (int k = lane; k < cnt * H; k += 32) dst[k] = T[k];
+    const int nf = cnt * H;
+    int k0 = 0;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {  // 16-byte stores, scalar tail
+      k0 = nf & ~3;
+      for (int k = 4 * lane; k < k0; k += 128)
+        *reinterpret_cast<float4 *>(dst + k) = *reinterpret_cast<const float4 *>(T + k);
+    }
+    for (int k = k0 + lane; k < nf; k += 32) dst[k] = T[k];
+  } else if constexpr (H % 4 == 0) {
+    // transpose through registers: lane k reads float4 k of the tile (entry
+    // k / Q, heads 4 (k % Q) .. + 3; conflict-free) and writes one value into
+    // each of those 4 head runs -- a store instruction covers 4 Q-entry runs
+    constexpr int Q = H / 4;
+    for (int k = lane; k < cnt * Q; k += 32) {
+      const float4 v = reinterpret_cast<const float4 *>(T)[k];
+      float *dst = alpha + (int64_t)(4 * (k % Q)) * ahs + e0 + k / Q;
+      dst[0] = v.x;
+      dst[ahs] = v.y;
+      dst[2 * ahs] = v.z;
+      dst[3 * ahs] = v.w;
+    }
   } else {
 #pragma unroll
     for (int h = 0; h < H; ++h)
@@ -112,58 +156,117 @@ __device__ __forceinline__ void stat_store_alpha(const float *T, int64_t e0, int
   }
 }
 
-// Short rows (<= kTile entries): lane l of warp w owns (row w * RPW + l / H,
-// head l % H), RPW = 32 / H rows per warp, and reduces its row and head
-// SEQUENTIALLY in column order -- no shuffles, the warp's rows in parallel.
-// The rows' entries (contiguous in CSR) are staged in the warp's tile by
-// cp.async, as many consecutive short rows at a time as fit.  The row max of
+// Short rows (<= kTile entries): warp w owns rows w * RPW .. + RPW - 1 (RPW =
+// 32 / H).  The rows' entries (contiguous in CSR) are staged in the warp's
+// tile by cp.async, as many consecutive short rows at a time as fit, and the
+// warp reduces them one row at a time: lane (part, h) takes entries part,
+// part + P, ... of head h (P = 32 / H), an xor tree over the P parts
+// finishes -- no lane waits on a longer row of another lane.  The row max of
 // the fp64 scores is the score of the fp32 max of the stored values (LeakyReLU
 // with slope >= 0 and IEEE rounding are monotone) -- exactly; slope < 0 takes
 // the fp64 max of the scores.
+// alpha of a batch: T holds exp(s - m) per entry and head, row_of[j] the
+// batch row of entry j and inv[q * H + h] its 1 / S -- scaled on the way out
+template <int H>
+__device__ __forceinline__ float stat_scale(const float *T, const uint8_t *row_of, const float *inv, int f) {
+  return T[f] * inv[row_of[f / H] * H + f % H];
+}
+template <int H>
+__device__ __forceinline__ void stat_store_scaled(const float *T, const uint8_t *row_of, const float *inv, int64_t e0,
+                                                  int cnt, float *alpha, int64_t ahs, int lane) {
+  const int nf = cnt * H;
+  if (ahs == 0 || H % 4 != 0) {
+    // [nnz][H]: one contiguous run (head-major with H % 4 != 0: per head)
+    if (ahs == 0) {
+      float *dst = alpha + e0 * H;
+      int k0 = 0;
+      if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        k0 = nf & ~3;
+        for (int f = 4 * lane; f < k0; f += 128)
+          *reinterpret_cast<float4 *>(dst + f) =
+              make_float4(stat_scale<H>(T, row_of, inv, f), stat_scale<H>(T, row_of, inv, f + 1),
+                          stat_scale<H>(T, row_of, inv, f + 2), stat_scale<H>(T, row_of, inv, f + 3));
+      }
+      for (int f = k0 + lane; f < nf; f += 32) dst[f] = stat_scale<H>(T, row_of, inv, f);
+    } else {
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        for (int j = lane; j < cnt; j += 32) alpha[h * ahs + e0 + j] = stat_scale<H>(T, row_of, inv, j * H + h);
+    }
+  } else {
+    // head-major [H][ahs], H % 4 == 0: lane reads float4 k of the tile (entry
+    // k / Q, heads 4 (k % Q) .. + 3; conflict-free) and writes one value into
+    // each of those 4 head runs -- a store instruction covers 4 Q-entry runs
+    constexpr int Q = H / 4;
+    for (int k = lane; k < cnt * Q; k += 32) {
+      const int j = k / Q, h0 = 4 * (k % Q);
+      const float4 v = reinterpret_cast<const float4 *>(T)[k];
+      const float4 w = *reinterpret_cast<const float4 *>(inv + row_of[j] * H + h0);
+      float *dst = alpha + (int64_t)h0 * ahs + e0 + j;
+      dst[0] = v.x * w.x;
+      dst[ahs] = v.y * w.y;
+      dst[2 * ahs] = v.z * w.z;
+      dst[3 * ahs] = v.w * w.w;
+    }
+  }
+}
+
+// Short rows (<= kTile entries): warp w owns rows w * RPW .. + RPW - 1 (RPW =
+// 32 / H).  The rows' entries (contiguous in CSR) are staged in the warp's
+// tile by cp.async, as many consecutive short rows at a time as fit (a
+// BATCH), and the warp reduces them one row at a time: lane (part, h) takes
+// entries part, part + P, ... of head h (P = 32 / H), an xor tree over the P
+// parts finishes -- no lane waits on a longer row of another lane.  The row
+// max of the fp64 scores is the score of the fp32 max of the stored values
+// (LeakyReLU with slope >= 0 and IEEE rounding are monotone) -- exactly;
+// slope < 0 takes the fp64 max of the scores.  kApply: the tile keeps
+// exp(s - m), the batch's rows' 1 / S go to `inv`, and alpha = exp * (1 / S)
+// is formed by the store.
 template <int H, bool kScores, bool kApply>
-__device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, int64_t rbase, int64_t n_rows,
-                                                const int32_t *__restrict__ col, const float *__restrict__ el,
-                                                const float *__restrict__ er, const float *logits, double slope,
-                                                GatStat *__restrict__ st, float *alpha, int64_t ahs, int warp,
-                                                int lane) {
+__device__ __forceinline__ void stat_short_rows(float *T, uint8_t *row_of, float *inv, const int64_t *s_rp,
+                                                int64_t rbase, int64_t n_rows, const int32_t *__restrict__ col,
+                                                const float *__restrict__ el, const float *__restrict__ er,
+                                                const float *logits, double slope, GatStat *__restrict__ st,
+                                                float *alpha, int64_t ahs, int warp, int lane) {
   constexpr int kTile = kStatTileFloats / H;
   constexpr int RPW = 32 / H;
-  const int rl = lane / H, h = lane % H;
-  const int base = warp * RPW;  // CTA-local index of the warp's first row
-  auto deg = [&](int k) { return s_rp[base + k + 1] - s_rp[base + k]; };
-#if GSP_STAT_COOP
   constexpr int P = RPW;
-  const int part = rl;
+  const int part = lane / H, h = lane % H;
+  const int base = warp * RPW;  // CTA-local index of the warp's first row
+  const double slope_l2e = slope * kLog2e;
+  const int nr = (int)max((int64_t)0, min((int64_t)RPW, n_rows - (rbase + base)));
+  // lane r (< nr) holds row r's start and end; batches are found by ballots
+  const int64_t rp_lo = s_rp[base + min(lane, RPW)], rp_hi = s_rp[base + min(lane + 1, RPW)];
+  const unsigned short_rows = __ballot_sync(0xffffffffu, lane < nr && rp_hi - rp_lo <= kTile);
   // el of the warp's rows, once: lane (r, h) holds el[row r][h]
-  const float el_l = (kScores && rbase + base + rl < n_rows) ? __ldg(el + (rbase + base + rl) * H + h) : 0.0f;
-#endif
-  int k = 0;
-  while (k < RPW) {
-    if (deg(k) > kTile) {  // a long row: its own path
-      ++k;
-      continue;
-    }
-    // rows k .. k2-1: consecutive short rows whose entries (contiguous in CSR) fit the tile
-    const int64_t B0 = s_rp[base + k];
-    int k2 = k + 1;
-    while (k2 < RPW && deg(k2) <= kTile && s_rp[base + k2 + 1] - B0 <= kTile) ++k2;
+  const float el_l = (kScores && part < nr) ? __ldg(el + (rbase + base + part) * H + h) : 0.0f;
+  unsigned todo = short_rows;
+  while (todo) {
+    const int k = __ffs(todo) - 1;
+    // rows k .. k2-1: consecutive short rows whose entries fit the tile
+    const int64_t B0 = __shfl_sync(0xffffffffu, rp_lo, k);
+    const unsigned fits = __ballot_sync(0xffffffffu, rp_hi - B0 <= kTile) & short_rows;
+    const unsigned run = ~(fits >> k);  // first row >= k that does not fit / is not short
+    const int k2 = k + (run ? __ffs(run) - 1 : 32 - k);
+    todo &= ~(((k2 >= 32) ? 0xffffffffu : ((1u << k2) - 1u)));
+    const int64_t B1 = __shfl_sync(0xffffffffu, rp_hi, k2 - 1);
     __syncwarp();
-    stat_load<H, kScores>(T, B0, (int)(s_rp[base + k2] - B0), col, er, logits, lane);
+    stat_load<H, kScores>(T, B0, (int)(B1 - B0), col, er, logits, lane);
     __syncwarp();
-#if GSP_STAT_COOP
-    // cooperative: the whole warp reduces one row at a time, lane (part, h)
-    // takes entries part, part + P, ... of head h (P = 32 / H), xor tree over
-    // the P parts -- no lane waits on a longer row of another lane
     for (int q = k; q < k2; ++q) {
-      const int64_t grow = rbase + base + q;
-      if (grow >= n_rows) break;
-      const int64_t b = s_rp[base + q];
-      const int d = (int)(s_rp[base + q + 1] - b);
+      const int64_t b = __shfl_sync(0xffffffffu, rp_lo, q);
+      const int d = (int)(__shfl_sync(0xffffffffu, rp_hi, q) - b);
       if (d == 0) continue;
       float *Tr = T + (b - B0) * H + h;
+      if (kApply && h == 0)
+        for (int j = part; j < d; j += P) row_of[b - B0 + j] = (uint8_t)q;
       const double el_u = kScores ? (double)__shfl_sync(0xffffffffu, el_l, q * H + h) : 0.0;
       float mr = -INFINITY;
-      for (int j = part; j < d; j += P) mr = fmaxf(mr, Tr[j * H]);
+      {
+        int j = part;
+        for (; j + P < d; j += 2 * P) mr = fmaxf(mr, fmaxf(Tr[j * H], Tr[(j + P) * H]));
+        if (j < d) mr = fmaxf(mr, Tr[j * H]);
+      }
 #pragma unroll
       for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
       double m = stat_score<kScores>(mr, el_u, slope);
@@ -173,63 +276,61 @@ __device__ __forceinline__ void stat_short_rows(float *T, const int64_t *s_rp, i
 #pragma unroll
         for (int off = H; off < 32; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
       }
-      double sum = 0.0;
-      for (int j = part; j < d; j += P) {
-        const float ex = expf((float)(stat_score<kScores>(Tr[j * H], el_u, slope) - m));
-        sum += (double)ex;
-        if (kApply) Tr[j * H] = ex;  // own slot
+      // exp(s - m) = 2^((s - m) log2 e): the argument is formed exactly enough
+      // that its one rounding to fp32 dominates (<= |s - m| u), then ex2.approx
+      // (<= 2 ulp).  Scores: s - m = x f - m with x = el + er exact in fp64 and
+      // f = 1 or slope, so (s - m) log2e = fma(x, f log2e, -m log2e) in fp64.
+      // Logits: t - t_max in fp32 is one rounding of the exact difference.
+      // fp32 sums: every term is in (0, 1] and one is exactly 1 (the max), a
+      // lane adds <= kTile / P = 32 of them -- relative error <= 37 u
+      const double mm = m * kLog2e;
+      auto ex_of = [&](float t) {
+        float a;
+        if (kScores) {
+          const double x = el_u + (double)t;
+          a = (float)fma(x, x >= 0.0 ? kLog2e : slope_l2e, -mm);
+        } else {
+          a = (t - mr) * (float)kLog2e;
+        }
+        return ex2_approx(a);
+      };
+      float sum = 0.0f;
+      {
+        int j = part;
+        for (; j + P < d; j += 2 * P) {
+          const float e0 = ex_of(Tr[j * H]), e1 = ex_of(Tr[(j + P) * H]);
+          sum += e0;
+          sum += e1;
+          if (kApply) {
+            Tr[j * H] = e0;  // own slots
+            Tr[(j + P) * H] = e1;
+          }
+        }
+        if (j < d) {
+          const float e0 = ex_of(Tr[j * H]);
+          sum += e0;
+          if (kApply) Tr[j * H] = e0;
+        }
       }
 #pragma unroll
       for (int off = H; off < 32; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      const float inv_s = (float)(1.0 / sum);
-      if (kApply) {
-        for (int j = part; j < d; j += P) Tr[j * H] *= inv_s;
-      } else if (part == 0) {
-        GatStat g;
-        g.m = m;
-        g.inv_s = inv_s;
-        g.pad = 0.f;
-        st[grow * H + h] = g;
-      }
-    }
-#endif
-    const int64_t grow = rbase + base + rl;
-    if (!GSP_STAT_COOP && rl >= k && rl < k2 && grow < n_rows) {
-      const int64_t b = s_rp[base + rl];
-      const int d = (int)(s_rp[base + rl + 1] - b);
-      if (d > 0) {
-        float *Tr = T + (b - B0) * H + h;
-        const double el_u = kScores ? (double)__ldg(el + grow * H + h) : 0.0;
-        float mr = -INFINITY;
-        for (int j = 0; j < d; ++j) mr = fmaxf(mr, Tr[j * H]);
-        double m = stat_score<kScores>(mr, el_u, slope);
-        if (kScores && !(slope >= 0.0)) {
-          m = -INFINITY;
-          for (int j = 0; j < d; ++j) m = fmax(m, stat_score<kScores>(Tr[j * H], el_u, slope));
-        }
-        double sum = 0.0;
-        for (int j = 0; j < d; ++j) {
-          const float ex = expf((float)(stat_score<kScores>(Tr[j * H], el_u, slope) - m));
-          sum += (double)ex;
-          if (kApply) Tr[j * H] = ex;  // own slot: no other lane reads it
-        }
-        const float inv_s = (float)(1.0 / sum);
+      const float inv_s = __frcp_rn(sum);
+      if (part == 0) {
         if (kApply) {
-          for (int j = 0; j < d; ++j) Tr[j * H] *= inv_s;  // alpha, in the tile; stored below by the warp
+          inv[q * H + h] = inv_s;
         } else {
           GatStat g;
           g.m = m;
           g.inv_s = inv_s;
           g.pad = 0.f;
-          st[grow * H + h] = g;
+          st[(rbase + base + q) * H + h] = g;
         }
       }
     }
-    if (kApply) {  // the batch's alpha (contiguous entries B0 .. B0 + tot) in 128-byte stores
+    if (kApply) {  // the batch's alpha (contiguous entries B0 .. B1) in 128-byte stores
       __syncwarp();
-      stat_store_alpha<H>(T, B0, (int)(s_rp[base + k2] - B0), alpha, ahs, lane);
+      stat_store_scaled<H>(T, row_of, inv, B0, (int)(B1 - B0), alpha, ahs, lane);
     }
-    k = k2;
   }
 }
 
@@ -262,6 +363,17 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+#if GSP_STAT_TRACE
+// tuning probe only (-DGSP_STAT_TRACE): per CTA start / end (globaltimer, ns),
+// SM id and long-row count of the last row_stats_warp launch
+constexpr int kTraceMax = 1 << 16;
+__device__ unsigned long long g_stat_trace[4][kTraceMax];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 template <int H, bool kScores, bool kApply>
 __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp(const int64_t *__restrict__ rp,
                                                                   const int32_t *__restrict__ col,
@@ -280,9 +392,26 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
   __shared__ double s_M[kSlots][H];               // merged max (kApply)
   __shared__ float s_inv[kSlots][H];              // merged 1 / S (kApply)
   __shared__ int64_t s_rp[kRows + 1];
+  __shared__ uint8_t s_rowof[kApply ? kStatWarps : 1][kApply ? kTile : 1];            // batch row of an entry
+  __shared__ __align__(16) float s_invw[kApply ? kStatWarps : 1][kApply ? 32 : 1];   // 1 / S per (batch row, head)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int h = lane % H, part = lane / H;
+  const double slope_l2e = slope * kLog2e;
   const int64_t rbase = (int64_t)blockIdx.x * kRows;
+#if GSP_STAT_TRACE
+  if (tid == 0 && blockIdx.x < kTraceMax) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_stat_trace[0][blockIdx.x] = gtimer();
+    g_stat_trace[2][blockIdx.x] = smid;
+  }
+  struct TraceEnd {
+    int lane;
+    __device__ ~TraceEnd() {
+      if (lane == 0 && blockIdx.x < kTraceMax) atomicMax(&g_stat_trace[1][blockIdx.x], gtimer());
+    }
+  } trace_end{(int)(threadIdx.x & 31)};
+#endif
   // the CTA's row pointers and its long rows, once (nobody is busy yet)
   for (int i = tid; i <= kRows; i += kStatWarps * 32) s_rp[i] = __ldg(rp + min(rbase + i, n_rows));
   __syncthreads();
@@ -297,6 +426,9 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
     lm[q] = __ballot_sync(0xffffffffu, r < kRows && (s_rp[r + 1] - s_rp[r]) > kTile);
     nlong += __popc(lm[q]);
   }
+#if GSP_STAT_TRACE
+  if (tid == 0 && blockIdx.x < kTraceMax) g_stat_trace[3][blockIdx.x] = nlong;
+#endif
   auto long_row = [&](int k) {  // CTA-local index of the k-th long row (index order)
 #pragma unroll
     for (int q = 0; q < kMasks; ++q) {
@@ -332,10 +464,11 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
 #pragma unroll
           for (int off = H; off < 32; off <<= 1) mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, off));
         }
-        double sc = 0.0;
-        for (int j = part; j < cnt; j += P) sc += (double)expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - mc));
+        float scf = 0.0f;  // <= kTile / P = 32 terms in (0, 1] per lane (as the short rows)
+        for (int j = part; j < cnt; j += P) scf += stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, mc);
 #pragma unroll
-        for (int off = H; off < 32; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
+        for (int off = H; off < 32; off <<= 1) scf += __shfl_xor_sync(0xffffffffu, scf, off);
+        const double sc = (double)scf;
         // fold the chunk into the warp's partial (chunks in increasing order)
         if (mc > m) {
           sum = (m == -INFINITY) ? sc : sum * exp(m - mc) + sc;
@@ -383,7 +516,7 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
       }
     }
     // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
+    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rowof[kApply ? warp : 0], s_invw[kApply ? warp : 0], s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
     // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
     if (kApply) {
       for (int k = 0; k < kn; ++k) {
@@ -402,14 +535,14 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
           stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
           __syncwarp();
           for (int j = part; j < cnt; j += P)
-            T[j * H + h] = expf((float)(stat_score<kScores>(T[j * H + h], el_u, slope) - M)) * inv_s;
+            T[j * H + h] = stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, M) * inv_s;
           __syncwarp();
           stat_store_alpha<H>(T, c0, cnt, alpha, ahs, lane);
         }
       }
     }
   }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
+  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rowof[kApply ? warp : 0], s_invw[kApply ? warp : 0], s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.
@@ -777,3 +910,13 @@ extern "C" gsp_status gsp_gat_aggregate_bias_act(const gsp_csr *a, int32_t heads
   return gat_aggregate_impl(a, heads, el, er, negative_slope, z, d, ldz, y, ldy, nullptr, bias, (int)act, ws, ws_bytes,
                             cs(stream), "gsp_gat_aggregate_bias_act");
 }
+
+#if GSP_STAT_TRACE
+extern "C" int gsp_debug_stat_trace(void *dst, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(dst, gsp::g_stat_trace, std::min(bytes, sizeof(gsp::g_stat_trace)));
+}
+extern "C" int gsp_debug_stat_trace_reset() {
+  static unsigned long long zero[4][gsp::kTraceMax];
+  return (int)cudaMemcpyToSymbol(gsp::g_stat_trace, zero, sizeof(zero));
+}
+#endif

@@ -9,8 +9,11 @@ build() { python paper_2103_00959_b200/_build.py --force --out=variants/libgsp_$
 for v in "$@"; do
   case $v in
     base) build base ;;
-    nocoop) build nocoop -DGSP_STAT_COOP=0 ;;
-    hotcold) build hotcold -DGSP_HOTCOLD=1 ;;
+    rpw4) build rpw4 -DGSP_STAT_RPW=4 ;;
+    rpw8) build rpw8 -DGSP_STAT_RPW=8 ;;
+    med1) build med1 -DGSP_STAT_MED_TILES=1 ;;
+    rpw32) build rpw32 -DGSP_STAT_RPW=32 ;;
+    w4rpw32) build w4rpw32 -DGSP_STAT_WARPS=4 -DGSP_STAT_RPW=32 -DGSP_STAT_MINB=8 ;;
     *) echo "unknown variant $v"; exit 1 ;;
   esac
 done
