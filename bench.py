@@ -3,7 +3,7 @@
 
 Headline (BASELINE.json metric): C4, a Chung-Lu power-law
 graph with Reddit's node / edge counts (232,965 nodes, 11,606,919 undirected
-pairs -> nnz(A^) = 23,446,803), 602 fp32 features (ld 604).  One STEP is
+pairs -> nnz(A^) = 23,446,803), 602 fp32 features (ld 608, rows on whole 128-byte lines).  One STEP is
 Y = A^ X through gsp_spmm; A^ is built (gsp_coo_to_csr) and normalised
 (gsp_sym_normalize) once before timing (reported as rows a1 / a2).
 
@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_GATHER_PEAK_GBS = 20264.7  # profiles/r1_probes.txt: ldg U=8, x_MB=17 (random 512-B row gathers from L2)
 FALLBACK_HBM = 6650.0   # GB/s, B200_PROFILING.md fallback
 NOMINAL_HBM = 8000.0    # GB/s, B200 nominal
 
@@ -680,6 +681,15 @@ def main_single(args):
         roof["achieved"] = None
         roof["frac"] = None
         roof["achieved_kind"] = "no committed ncu capture for this workload"
+    l2b = nc.get("l2_bytes") if nc else None
+    if l2b:
+        # the gather path's own ceiling: L2 -> SM bytes against the measured rate
+        # of random 512-byte row gathers from an L2-resident X (8 LDG.128 in
+        # flight per lane, 32 warps/SM; profiles/r1_probes.txt, tools/probe_gather4.cu)
+        roof["l2"] = {"achieved": l2b / (t_ms * 1e-3) / 1e9, "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
+                      "frac": l2b / (t_ms * 1e-3) / 1e9 / L2_GATHER_PEAK_GBS,
+                      "bytes_kind": "ncu lts__t_bytes.sum of this kernel per launch",
+                      "peak_kind": "measured random 512-B row-gather rate, X L2-resident (profiles/r1_probes.txt)"}
     out = {
         "metric": METRIC, "value": ge / (t_ms * 1e-3), "unit": "GE/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms, "ms_per_step_median": float(np.median(times)),

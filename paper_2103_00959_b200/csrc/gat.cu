@@ -175,6 +175,7 @@ template <int H>
 __device__ __forceinline__ void stat_store_scaled(const float *T, const uint8_t *row_of, const float *inv, int64_t e0,
                                                   int cnt, float *alpha, int64_t ahs, int lane) {
   const int nf = cnt * H;
+  constexpr int Q = H % 4 == 0 ? H / 4 : 1;  // float4s per entry (head-major transpose)
   if (ahs == 0 || H % 4 != 0) {
     // [nnz][H]: one contiguous run (head-major with H % 4 != 0: per head)
     if (ahs == 0) {
@@ -197,7 +198,6 @@ __device__ __forceinline__ void stat_store_scaled(const float *T, const uint8_t 
     // head-major [H][ahs], H % 4 == 0: lane reads float4 k of the tile (entry
     // k / Q, heads 4 (k % Q) .. + 3; conflict-free) and writes one value into
     // each of those 4 head runs -- a store instruction covers 4 Q-entry runs
-    constexpr int Q = H / 4;
     for (int k = lane; k < cnt * Q; k += 32) {
       const int j = k / Q, h0 = 4 * (k % Q);
       const float4 v = reinterpret_cast<const float4 *>(T)[k];

@@ -456,6 +456,10 @@ __device__ __forceinline__ void load_cols(float (&r)[V], const float *p, int nva
 template <int V>
 __device__ __forceinline__ void epilogue(const EngineParams &p, int64_t r, int64_t col0, const float (&out_in)[V],
                                          int nvalid) {
+  if (!p.bias && p.act == 0 && !p.acc) {  // plain Y = A X (uniform branch)
+    if (!p.skip_y) store_cols<V>(p.y + r * p.ldy + col0, out_in, nvalid, p.y_vec_ok);
+    return;
+  }
   float out[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
