@@ -32,6 +32,10 @@ namespace gsp {
 #define GSP_STAT_MINB 4
 #endif
 constexpr int kStatWarps = GSP_STAT_WARPS;  // warps per CTA
+#ifndef GSP_STAT_LONG_SLICE
+#define GSP_STAT_LONG_SLICE 128
+#endif
+constexpr int kLongSlice = GSP_STAT_LONG_SLICE;  // rows a long CTA scans for long rows (<= 256)
 constexpr int kStatTileFloats = 1024;  // per warp: kTile = 1024 / H entries x H heads (4 KB)
 
 constexpr double kLog2e = 1.4426950408889634074;  // log2(e)
@@ -334,35 +338,6 @@ __device__ __forceinline__ void stat_short_rows(float *T, uint8_t *row_of, float
   }
 }
 
-// Long rows (> kTile entries) are cut into tile-sized chunks; warp w takes
-// chunks w, w + 8, ... and reduces them to a partial (m_w, s_w) with its OWN
-// maximum m_w (s_w = sum of exp(s - m_w), fp64).  Warp k % 8 merges long row
-// k's 8 partials in warp order -- M = max m_w, S = sum_w s_w exp(m_w - M)
-// (fp64) -- after a named barrier the other warps only ARRIVE at, so they go
-// on with the next long row and their short rows; only the alpha writes of a
-// long row (kApply) wait (second named barrier) for its merged (M, S).
-// Partials of up to kSlots long rows live in shared memory; a CTA with more
-// long rows processes them in batches separated by a CTA barrier.
-// Slots: <= 8 KB of partials (48 KB static smem) and one named barrier per
-// long row (two with kApply) out of the 15 a CTA has besides barrier 0.
-template <int H, bool kApply>
-struct StatSlots {
-  static constexpr int kMem = (64 / H) < 16 ? (64 / H) : 16;
-  static constexpr int kBar = kApply ? 7 : 15;
-  static constexpr int kSlots = kMem < kBar ? kMem : kBar;
-};
-
-// named CTA barriers (bar.sync / bar.arrive over `n` threads): the warps that
-// produce a long row's partials arrive without waiting; only the warp that
-// merges them (and, with kApply, the warps that then need the merged result)
-// wait -- ordered for the memory model and for compute-sanitizer's racecheck
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 #if GSP_STAT_TRACE
 // tuning probe only (-DGSP_STAT_TRACE): per CTA start / end (globaltimer, ns),
 // SM id and long-row count of the last row_stats_warp launch
@@ -374,6 +349,150 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 #endif
+// Long rows (> kTile entries) of a long CTA's slice, kSlots at a time: the
+// group's chunks (kTile entries each) are numbered back to back, c = pre_k + j
+// for chunk j of row k, and warp w takes c = w, w + 8, ...  Chunk j belongs to
+// RESIDUE q = j % 8 of its row; whichever warp computes it (w = (pre_k + j) % 8)
+// folds the row's residue-q chunks in increasing j into a partial with its own
+// max m_q (s_q = sum of exp(s - m_q), fp64), and the residues are merged in q
+// order -- M = max m_q, S = sum_q s_q exp(m_q - M) -- so the order depends on
+// the row alone.  kApply then writes alpha chunk by chunk the same way.
+template <int H>
+struct LongSlots {
+  static constexpr int kSlots = (32 / H) > 8 ? 8 : ((32 / H) > 1 ? 32 / H : 1);  // rows per group (<= 2 KB of partials per array)
+};
+
+template <int H, bool kScores, bool kApply>
+__device__ __forceinline__ void stat_long_group(float *T, double (*s_pm)[kStatWarps][H],
+                                                double (*s_ps)[kStatWarps][H], double (*s_M)[H], float (*s_inv)[H],
+                                                const int64_t *s_lr, const int64_t *s_lb, const int *s_pre, int nk,
+                                                const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                const float *__restrict__ el, const float *__restrict__ er,
+                                                const float *logits, double slope, double slope_l2e,
+                                                GatStat *__restrict__ st, float *alpha, int64_t ahs, int warp,
+                                                int lane, int tid) {
+  constexpr int kTile = kStatTileFloats / H;
+  constexpr int P = 32 / H;
+  const int h = lane % H, part = lane / H;
+  for (int i = tid; i < nk * kStatWarps * H; i += kStatWarps * 32) {
+    (&s_pm[0][0][0])[i] = -INFINITY;
+    (&s_ps[0][0][0])[i] = 0.0;
+  }
+  __syncthreads();
+  const int total = s_pre[nk];
+  int k = 0;
+  double m = -INFINITY, sum = 0.0;  // running partial of (row k, this warp's residue)
+  auto flush = [&]() {
+    if (m != -INFINITY || sum != 0.0) {
+      const int q = (int)(((warp - s_pre[k]) % kStatWarps + kStatWarps) % kStatWarps);
+      if (part == 0) {
+        s_pm[k][q][h] = m;
+        s_ps[k][q][h] = sum;
+      }
+    }
+    m = -INFINITY;
+    sum = 0.0;
+  };
+  double el_u = 0.0;
+  int el_k = -1;
+  for (int c = warp; c < total; c += kStatWarps) {
+    int kk = k;
+    while (kk + 1 < nk && s_pre[kk + 1] <= c) ++kk;
+    if (kk != k) {
+      flush();
+      k = kk;
+    }
+    if (kScores && el_k != k) {
+      el_u = (double)__ldg(el + s_lr[k] * H + h);
+      el_k = k;
+    }
+    const int64_t e1 = s_lb[k + 1 + nk];  // row end (see caller's layout)
+    const int64_t c0 = s_lb[k] + (int64_t)(c - s_pre[k]) * kTile;
+    const int cnt = (int)min((int64_t)kTile, e1 - c0);
+    __syncwarp();
+    stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
+    __syncwarp();
+    float mr = -INFINITY;  // exact chunk max of the scores via the stored values (monotone)
+    for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
+#pragma unroll
+    for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+    double mc = stat_score<kScores>(mr, el_u, slope);
+    if (kScores && !(slope >= 0.0)) {
+      mc = -INFINITY;
+      for (int j = part; j < cnt; j += P) mc = fmax(mc, stat_score<kScores>(T[j * H + h], el_u, slope));
+#pragma unroll
+      for (int off = H; off < 32; off <<= 1) mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, off));
+    }
+    float scf = 0.0f;  // <= kTile / P = 32 terms in (0, 1] per lane (as the short rows)
+    for (int j = part; j < cnt; j += P) scf += stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, mc);
+#pragma unroll
+    for (int off = H; off < 32; off <<= 1) scf += __shfl_xor_sync(0xffffffffu, scf, off);
+    const double sc = (double)scf;
+    // fold the chunk into the residue's partial (its chunks in increasing order)
+    if (mc > m) {
+      sum = (m == -INFINITY) ? sc : sum * exp(m - mc) + sc;
+      m = mc;
+    } else if (mc != -INFINITY) {
+      sum += sc * exp(mc - m);
+    } else {
+      sum += sc;  // NaN propagates; empty chunks do not occur
+    }
+  }
+  if (total > warp) flush();
+  __syncthreads();
+  for (int i = tid; i < nk * H; i += kStatWarps * 32) {  // merge the residues in order
+    const int kq = i / H, hh = i % H;
+    double M = -INFINITY;
+    for (int q = 0; q < kStatWarps; ++q) M = fmax(M, s_pm[kq][q][hh]);
+    double S = 0.0;
+    for (int q = 0; q < kStatWarps; ++q) {
+      const double mq = s_pm[kq][q][hh];
+      if (mq != -INFINITY) S += s_ps[kq][q][hh] * exp(mq - M);
+      else S += s_ps[kq][q][hh];
+    }
+    if (kApply) {
+      s_M[kq][hh] = M;
+      s_inv[kq][hh] = (float)(1.0 / S);
+    } else {
+      GatStat g;
+      g.m = M;
+      g.inv_s = (float)(1.0 / S);
+      g.pad = 0.f;
+      st[s_lr[kq] * H + hh] = g;
+    }
+  }
+  __syncthreads();
+  if (kApply) {
+    k = 0;
+    el_k = -1;
+    for (int c = warp; c < total; c += kStatWarps) {
+      while (k + 1 < nk && s_pre[k + 1] <= c) ++k;
+      if (kScores && el_k != k) {
+        el_u = (double)__ldg(el + s_lr[k] * H + h);
+        el_k = k;
+      }
+      const int64_t e1 = s_lb[k + 1 + nk];
+      const int64_t c0 = s_lb[k] + (int64_t)(c - s_pre[k]) * kTile;
+      const int cnt = (int)min((int64_t)kTile, e1 - c0);
+      const double M = s_M[k][h];
+      const float inv_s = s_inv[k][h];
+      __syncwarp();
+      stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
+      __syncwarp();
+      for (int j = part; j < cnt; j += P) T[j * H + h] = stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, M) * inv_s;
+      __syncwarp();
+      stat_store_alpha<H>(T, c0, cnt, alpha, ahs, lane);
+    }
+  }
+  __syncthreads();  // the group's shared arrays are rewritten by the next group
+}
+
+// Grid: n_long LONG CTAs first, then the SHORT CTAs.
+//  * long CTA c scans rows [c * long_rows, (c + 1) * long_rows) for rows of
+//    more than kTile entries and reduces each with the whole CTA (they start
+//    first, so the power-law tail overlaps the bulk of the short rows);
+//  * short CTA b owns rows [b * kRows, (b + 1) * kRows) and reduces their
+//    short rows, warp by warp (stat_short_rows); its long rows are skipped.
 template <int H, bool kScores, bool kApply>
 __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp(const int64_t *__restrict__ rp,
                                                                   const int32_t *__restrict__ col,
@@ -381,29 +500,23 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
                                                                   const float *__restrict__ er, const float *logits,
                                                                   double slope, int64_t n_rows,
                                                                   GatStat *__restrict__ st, float *alpha,
-                                                                  int64_t ahs) {
+                                                                  int64_t ahs, int n_long, int64_t long_rows) {
   constexpr int kTile = kStatTileFloats / H;
-  constexpr int kRows = kStatWarps * (32 / H);  // rows per CTA (32 / H per warp: lane = (row, head))
-  constexpr int kSlots = StatSlots<H, kApply>::kSlots;
-  constexpr int P = 32 / H;
+  constexpr int kRows = kStatWarps * (32 / H);  // rows per short CTA (32 / H per warp)
   __shared__ __align__(16) float s_tile[kStatWarps][kStatTileFloats];
-  __shared__ double s_pm[kSlots][kStatWarps][H];  // partial max (score) per slot, warp, head
-  __shared__ double s_ps[kSlots][kStatWarps][H];  // partial sum of exp(s - m_w)
-  __shared__ double s_M[kSlots][H];               // merged max (kApply)
-  __shared__ float s_inv[kSlots][H];              // merged 1 / S (kApply)
   __shared__ int64_t s_rp[kRows + 1];
   __shared__ uint8_t s_rowof[kApply ? kStatWarps : 1][kApply ? kTile : 1];            // batch row of an entry
   __shared__ __align__(16) float s_invw[kApply ? kStatWarps : 1][kApply ? 32 : 1];   // 1 / S per (batch row, head)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  const int h = lane % H, part = lane / H;
   const double slope_l2e = slope * kLog2e;
-  const int64_t rbase = (int64_t)blockIdx.x * kRows;
+  float *T = s_tile[warp];
 #if GSP_STAT_TRACE
   if (tid == 0 && blockIdx.x < kTraceMax) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     g_stat_trace[0][blockIdx.x] = gtimer();
     g_stat_trace[2][blockIdx.x] = smid;
+    g_stat_trace[3][blockIdx.x] = (int)blockIdx.x < n_long;
   }
   struct TraceEnd {
     int lane;
@@ -412,137 +525,47 @@ __global__ void __launch_bounds__(kStatWarps * 32, GSP_STAT_MINB) row_stats_warp
     }
   } trace_end{(int)(threadIdx.x & 31)};
 #endif
-  // the CTA's row pointers and its long rows, once (nobody is busy yet)
+  if ((int)blockIdx.x < n_long) {
+    constexpr int kSl = LongSlots<H>::kSlots;
+    __shared__ double s_pm[kSl][kStatWarps][H], s_ps[kSl][kStatWarps][H], s_M[kSl][H];
+    __shared__ float s_inv[kSl][H];
+    __shared__ int64_t s_lr[kSl], s_lb[2 * kSl + 1];  // rows; starts [0, kSl), ends at [1 + nk + k]
+    __shared__ int s_pre[kSl + 1], s_list[kThreads], s_cnt;
+    const int64_t r0 = (int64_t)blockIdx.x * long_rows, r1 = min(n_rows, r0 + long_rows);
+    for (int64_t base = r0; base < r1; base += kThreads) {
+      if (tid == 0) s_cnt = 0;
+      __syncthreads();
+      const int64_t r = base + tid;
+      if (r < r1 && __ldg(rp + r + 1) - __ldg(rp + r) > kTile) s_list[atomicAdd(&s_cnt, 1)] = tid;
+      __syncthreads();
+      const int cnt = s_cnt;
+      for (int g0 = 0; g0 < cnt; g0 += kSl) {
+        const int nk = min(kSl, cnt - g0);
+        if (tid == 0) {  // the group's rows, their extents and chunk offsets
+          int pre = 0;
+          for (int k = 0; k < nk; ++k) {
+            const int64_t rr = base + s_list[g0 + k], b = __ldg(rp + rr), e = __ldg(rp + rr + 1);
+            s_lr[k] = rr;
+            s_lb[k] = b;
+            s_lb[1 + nk + k] = e;
+            s_pre[k] = pre;
+            pre += (int)((e - b + kTile - 1) / kTile);
+          }
+          s_pre[nk] = pre;
+        }
+        __syncthreads();
+        stat_long_group<H, kScores, kApply>(T, s_pm, s_ps, s_M, s_inv, s_lr, s_lb, s_pre, nk, rp, col, el, er,
+                                            logits, slope, slope_l2e, st, alpha, ahs, warp, lane, tid);
+      }
+      __syncthreads();  // s_list / s_cnt are rewritten
+    }
+    return;
+  }
+  const int64_t rbase = (int64_t)(blockIdx.x - n_long) * kRows;
   for (int i = tid; i <= kRows; i += kStatWarps * 32) s_rp[i] = __ldg(rp + min(rbase + i, n_rows));
   __syncthreads();
-  // every warp finds the CTA's long rows itself (ballots over s_rp): no second
-  // CTA barrier before the warps start working
-  constexpr int kMasks = (kRows + 31) / 32;
-  unsigned lm[kMasks];
-  int nlong = 0;
-#pragma unroll
-  for (int q = 0; q < kMasks; ++q) {
-    const int r = q * 32 + lane;
-    lm[q] = __ballot_sync(0xffffffffu, r < kRows && (s_rp[r + 1] - s_rp[r]) > kTile);
-    nlong += __popc(lm[q]);
-  }
-#if GSP_STAT_TRACE
-  if (tid == 0 && blockIdx.x < kTraceMax) g_stat_trace[3][blockIdx.x] = nlong;
-#endif
-  auto long_row = [&](int k) {  // CTA-local index of the k-th long row (index order)
-#pragma unroll
-    for (int q = 0; q < kMasks; ++q) {
-      const int c = __popc(lm[q]);
-      if (k < c) return q * 32 + (int)__fns(lm[q], 0, k + 1);
-      k -= c;
-    }
-    return 0;
-  };
-  float *T = s_tile[warp];
-  // ---- 1. long rows: per-warp partials, merged by the last warp to arrive
-  for (int k0 = 0; k0 < nlong; k0 += kSlots) {
-    const int kn = min(kSlots, nlong - k0);
-    if (k0 > 0) __syncthreads();  // slots and barrier ids are reused: the previous batch is complete
-    for (int k = 0; k < kn; ++k) {
-      const int lr = long_row(k0 + k);
-      const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
-      const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-      double m = -INFINITY, sum = 0.0;
-      for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
-        const int cnt = (int)min((int64_t)kTile, e1 - c0);
-        __syncwarp();
-        stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
-        __syncwarp();
-        float mr = -INFINITY;  // exact chunk max of the scores via the stored values (monotone, see stat_row)
-        for (int j = part; j < cnt; j += P) mr = fmaxf(mr, T[j * H + h]);
-#pragma unroll
-        for (int off = H; off < 32; off <<= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, off));
-        double mc = stat_score<kScores>(mr, el_u, slope);
-        if (kScores && !(slope >= 0.0)) {
-          mc = -INFINITY;
-          for (int j = part; j < cnt; j += P) mc = fmax(mc, stat_score<kScores>(T[j * H + h], el_u, slope));
-#pragma unroll
-          for (int off = H; off < 32; off <<= 1) mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, off));
-        }
-        float scf = 0.0f;  // <= kTile / P = 32 terms in (0, 1] per lane (as the short rows)
-        for (int j = part; j < cnt; j += P) scf += stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, mc);
-#pragma unroll
-        for (int off = H; off < 32; off <<= 1) scf += __shfl_xor_sync(0xffffffffu, scf, off);
-        const double sc = (double)scf;
-        // fold the chunk into the warp's partial (chunks in increasing order)
-        if (mc > m) {
-          sum = (m == -INFINITY) ? sc : sum * exp(m - mc) + sc;
-          m = mc;
-        } else if (mc != -INFINITY) {
-          sum += sc * exp(mc - m);
-        } else {
-          sum += sc;  // NaN propagates; empty chunks do not occur
-        }
-      }
-      if (part == 0) {
-        s_pm[k][warp][h] = m;
-        s_ps[k][warp][h] = sum;
-      }
-      __syncwarp();
-      const int bar_merge = 1 + (kApply ? 2 * k : k);
-      if (warp != k % kStatWarps) {
-        named_arrive(bar_merge, kStatWarps * 32);
-        continue;
-      }
-      named_sync(bar_merge, kStatWarps * 32);  // every warp's partial of row k is written
-      if (lane < H) {  // merge the 8 partials in warp order
-        double M = -INFINITY;
-        for (int w = 0; w < kStatWarps; ++w) M = fmax(M, s_pm[k][w][lane]);
-        double S = 0.0;
-        for (int w = 0; w < kStatWarps; ++w) {
-          const double mw = s_pm[k][w][lane];
-          if (mw != -INFINITY) S += s_ps[k][w][lane] * exp(mw - M);
-          else S += s_ps[k][w][lane];
-        }
-        if (kApply) {
-          s_M[k][lane] = M;
-          s_inv[k][lane] = (float)(1.0 / S);
-        } else {
-          GatStat g;
-          g.m = M;
-          g.inv_s = (float)(1.0 / S);
-          g.pad = 0.f;
-          st[r * H + lane] = g;
-        }
-      }
-      if (kApply) {
-        __syncwarp();
-        named_arrive(bar_merge + 1, kStatWarps * 32);  // (M, 1/S) of row k published
-      }
-    }
-    // ---- 2. short rows (first batch only), while the other warps finish their long chunks
-    if (k0 == 0) stat_short_rows<H, kScores, kApply>(T, s_rowof[kApply ? warp : 0], s_invw[kApply ? warp : 0], s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
-    // ---- 3. kApply: alpha of this batch's long rows, once their (M, S) are merged
-    if (kApply) {
-      for (int k = 0; k < kn; ++k) {
-        const int lr = long_row(k0 + k);
-        const int64_t r = rbase + lr, b = s_rp[lr], e1 = s_rp[lr + 1];
-        // every warp but the merging one meets the publishing warp here (even
-        // without a chunk of the row: the barrier counts all 8 warps)
-        if (warp != k % kStatWarps) named_sync(1 + 2 * k + 1, kStatWarps * 32);
-        if (b + (int64_t)warp * kTile >= e1) continue;
-        const double el_u = kScores ? (double)__ldg(el + r * H + h) : 0.0;
-        const double M = s_M[k][h];
-        const float inv_s = s_inv[k][h];
-        for (int64_t c0 = b + (int64_t)warp * kTile; c0 < e1; c0 += (int64_t)kStatWarps * kTile) {
-          const int cnt = (int)min((int64_t)kTile, e1 - c0);
-          __syncwarp();
-          stat_load<H, kScores>(T, c0, cnt, col, er, logits, lane);
-          __syncwarp();
-          for (int j = part; j < cnt; j += P)
-            T[j * H + h] = stat_exp<kScores>(T[j * H + h], el_u, slope_l2e, M) * inv_s;
-          __syncwarp();
-          stat_store_alpha<H>(T, c0, cnt, alpha, ahs, lane);
-        }
-      }
-    }
-  }
-  if (nlong == 0) stat_short_rows<H, kScores, kApply>(T, s_rowof[kApply ? warp : 0], s_invw[kApply ? warp : 0], s_rp, rbase, n_rows, col, el, er, logits, slope, st, alpha, ahs, warp, lane);
+  stat_short_rows<H, kScores, kApply>(T, s_rowof[kApply ? warp : 0], s_invw[kApply ? warp : 0], s_rp, rbase, n_rows,
+                                      col, el, er, logits, slope, st, alpha, ahs, warp, lane);
 }
 
 // Fallback for H not dividing 32: one thread per (row, head), sequential.
@@ -589,11 +612,14 @@ static gsp_status launch_stats(const gsp_csr *a, const float *el, const float *e
   const float *vsrc = kScores ? er : logits;
   const bool vec_ok = H < 4 ? (H == 1 || aligned8(vsrc)) : aligned16(vsrc);
   if (32 % H == 0 && (vec_ok || !kScores)) {
-    const unsigned blocks = (unsigned)ceil_div(a->n_rows, kStatWarps * (32 / H));
+    // long CTAs (a slice of kLongSlice rows each) come first in the grid
+    const int64_t long_rows = kLongSlice;
+    const int n_long = (int)ceil_div(a->n_rows, long_rows);
+    const unsigned blocks = (unsigned)(n_long + ceil_div(a->n_rows, kStatWarps * (32 / H)));
 #define GSP_STATS_H(HH)                                                                                       \
   case HH:                                                                                                   \
-    row_stats_warp<HH, kScores, kApply><<<blocks, kStatWarps * 32, 0, s>>>(a->row_ptr, a->col_idx, el, er,     \
-                                                                         logits, slope, a->n_rows, st, alpha, ahs); \
+    row_stats_warp<HH, kScores, kApply><<<blocks, kStatWarps * 32, 0, s>>>(                                   \
+        a->row_ptr, a->col_idx, el, er, logits, slope, a->n_rows, st, alpha, ahs, n_long, long_rows);         \
     break;
     switch (H) {
       GSP_STATS_H(1) GSP_STATS_H(2) GSP_STATS_H(4) GSP_STATS_H(8) GSP_STATS_H(16) GSP_STATS_H(32)

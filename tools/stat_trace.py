@@ -36,15 +36,18 @@ def trace(fn):
 
 
 def report(name, g, buf, ncta):
-    st, en, sm, nl = (buf[i, :ncta].astype(np.int64) for i in range(4))
+    st, en, sm, nl = (buf[i, :ncta].astype(np.int64) for i in range(4))  # nl: 1 for a long-row CTA
     t0 = st.min()
     st, en = (st - t0) / 1e3, (en - t0) / 1e3  # us
     dur = en - st
     rp = g.row_ptr.cpu().numpy()
     deg = np.diff(rp)
     kr = RPW * WARPS
-    cta_max = np.array([deg[i * kr:(i + 1) * kr].max(initial=0) for i in range(ncta)])
-    cta_nnz = np.array([deg[i * kr:(i + 1) * kr].sum() for i in range(ncta)])
+    nlong = int(nl.sum())
+    lr = int(os.environ.get("LONG_SLICE", "128"))
+    span = lambda i: slice(i * lr, (i + 1) * lr) if i < nlong else slice((i - nlong) * kr, (i - nlong + 1) * kr)
+    cta_max = np.array([deg[span(i)].max(initial=0) for i in range(ncta)])
+    cta_nnz = np.array([deg[span(i)].sum() for i in range(ncta)])
     bins = np.arange(0, en.max() + 1, 1.0)
     active = [int(((st <= b) & (en > b)).sum()) for b in bins]
     out = {"graph": name, "ctas": int(ncta), "span_us": round(float(en.max()), 2),
@@ -52,7 +55,7 @@ def report(name, g, buf, ncta):
            "start_us p50/max": [round(float(np.median(st)), 2), round(float(st.max()), 2)],
            "active_ctas_per_us (every 4th)": active[::4],
            "slowest": [{"cta": int(i), "dur_us": round(float(dur[i]), 2), "start": round(float(st[i]), 2),
-                        "nlong": int(nl[i]), "max_deg": int(cta_max[i]), "nnz": int(cta_nnz[i])}
+                        "long_cta": int(nl[i]), "max_deg": int(cta_max[i]), "nnz": int(cta_nnz[i])}
                        for i in np.argsort(-dur)[:8]],
            "corr(dur, max_deg)": round(float(np.corrcoef(dur, cta_max)[0, 1]), 3),
            "corr(dur, nnz)": round(float(np.corrcoef(dur, cta_nnz)[0, 1]), 3)}
@@ -68,7 +71,7 @@ for name, (s, d) in graphs.items():
     g = G.gsp_coo_to_csr(cfg.n, torch.from_numpy(s).to(dev), torch.from_numpy(d).to(dev))
     lg = torch.from_numpy(uniform((g.nnz, H), seed=4, low=-3, high=3)).to(dev)
     al = torch.empty_like(lg)
-    ncta = (cfg.n + RPW * WARPS - 1) // (RPW * WARPS)
+    ncta = -(-cfg.n // int(os.environ.get("LONG_SLICE", "128"))) + (cfg.n + RPW * WARPS - 1) // (RPW * WARPS)
     buf = trace(lambda: G.gsp_edge_softmax(g, lg, H, alpha=al))
     report(name + " edge_softmax", g, buf, ncta)
     el = torch.from_numpy(uniform((cfg.n, H), seed=4, low=-3, high=3)).to(dev)

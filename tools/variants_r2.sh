@@ -9,6 +9,8 @@ build() { python paper_2103_00959_b200/_build.py --force --out=variants/libgsp_$
 for v in "$@"; do
   case $v in
     base) build base ;;
+    ls64) build ls64 -DGSP_STAT_LONG_SLICE=64 ;;
+    ls256) build ls256 -DGSP_STAT_LONG_SLICE=256 ;;
     rpw4) build rpw4 -DGSP_STAT_RPW=4 ;;
     rpw8) build rpw8 -DGSP_STAT_RPW=8 ;;
     med1) build med1 -DGSP_STAT_MED_TILES=1 ;;
