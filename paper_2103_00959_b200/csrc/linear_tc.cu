@@ -4,10 +4,15 @@
 //
 // Why 3xTF32: the layer's parity bound is the fp32 one (DESIGN.md §NEXT rows:
 // (1e-5 + F_in 2^-24) cond); a single TF32 product has 2^-11 relative error.
-// With x = x_hi + x_lo (x_hi = rna_tf32(x), x_lo = x - x_hi exact in fp32) and
-// w likewise, x w ~= x_lo w_hi + x_hi w_lo + x_hi w_hi; the dropped x_lo w_lo
-// and the TF32 rounding of the lo parts are <= 2^-20 |x||w| per product, the
-// accumulation is fp32 in TMEM.
+// With x = x_hi + x_lo and w = w_hi + w_lo, x w ~= x_lo w_hi + x_hi w_lo +
+// x_hi w_hi.  W is split once (w_hi = rna_tf32(w), |w_lo| <= 2^-11 |w|).  X is
+// not rewritten: kind::tf32 reads the raw fp32 tile as x_hi = trunc_tf32(x)
+// (its top 19 bits; test_linear_tc_low_mantissa_bits fails by 2^-10 otherwise)
+// and the converter warps store only x_lo = x - trunc_tf32(x) (exact,
+// |x_lo| < 2^-10 |x|).  The MMA truncates the lo parts too; with the dropped
+// x_lo w_lo the error is <= (2^-20 + 2 * 2^-21) |x||w| = 2^-19 |x||w| per
+// product, accumulated in fp32 in TMEM.  (-DGSP_TC_RAWHI=0: x_hi = rna_tf32(x)
+// written back, 1.25 * 2^-20.)
 //
 // One CTA per (128-row tile of X, <= 256 output columns): one MMA per K step
 // covers the CTA's whole output tile (M = 128, N, K = 8); K in tiles of 16
@@ -27,6 +32,9 @@ namespace gsp {
 constexpr int kTcBM = 128, kTcBK = 16;  // K tile: 16 fp32 = 64-byte rows (SWIZZLE_64B)
 constexpr int kTcNT = 256;              // max output columns per CTA (grid.y tiles wider outputs)
 constexpr int kTcThreads = 192;
+#ifndef GSP_TC_RAWHI
+#define GSP_TC_RAWHI 1
+#endif
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -177,6 +185,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
       for (int i = 0; i < (int)(kTcBM * kTcBK / 4 / 128); ++i) {  // elementwise: same swizzled offset in hi and lo
         const int q = t + 128 * i;
         const float4 v = hi[q];
+#if GSP_TC_RAWHI
+        // the MMA reads the raw fp32 X as x_hi (kind::tf32 uses its top 19
+        // bits: truncation, tested); lo = x - trunc_tf32(x) is exact
+        float4 l;
+        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+        lo[q] = l;
+#else
         float4 h, l;
         h.x = tf32_rna(v.x); l.x = v.x - h.x;
         h.y = tf32_rna(v.y); l.y = v.y - h.y;
@@ -184,6 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
         h.w = tf32_rna(v.w); l.w = v.w - h.w;
         hi[q] = h;
         lo[q] = l;
+#endif
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core (async) proxy
       mbar_arrive(&s_split[s]);

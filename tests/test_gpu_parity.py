@@ -552,6 +552,27 @@ def test_linear_parity(n, f_in, f_out, tc):
     assert_within(y, yr, c, rel=rel, what=f"linear {n}x{f_in}x{f_out} tc={tc}")
 
 
+@pytest.mark.parametrize("pattern", ["round_up", "round_down", "random_low_bits"])
+def test_linear_tc_low_mantissa_bits(pattern):
+    """X entries whose bits below TF32 precision decide how the tensor core
+    reads them: with W = I every output is a single product x * 1, so the
+    3xTF32 result must equal x to 2^-19 relative per element -- a truncating
+    vs rounding misreading of x_hi would be off by up to 2^-10."""
+    n, f = 256, 32
+    rng = np.random.default_rng(7)
+    mant = {"round_up": 3.0 * 2.0 ** -12, "round_down": 1.0 * 2.0 ** -12}
+    if pattern in mant:
+        x = np.full((n, f), 1.0 + mant[pattern], np.float32) * rng.choice([-1.0, 1.0], (n, f)).astype(np.float32)
+    else:
+        bits = rng.integers(0, 1 << 32, size=(n, f), dtype=np.uint64).astype(np.uint32)
+        bits = (bits & np.uint32(0x807FFFFF)) | np.uint32(127 << 23)  # |x| in [1, 2), every mantissa bit random
+        x = bits.view(np.float32)
+    w = np.eye(f, dtype=np.float32)
+    y = host(G.gsp_linear(dev(x), dev(w), tensor_cores=True)).astype(np.float64)
+    err = np.abs(y - x.astype(np.float64)) / np.abs(x.astype(np.float64))
+    assert err.max() <= 2.0 ** -19, f"{pattern}: max relative error {err.max():.3e}"
+
+
 def test_linear_tc_padded_views():
     """Tensor-core GEMM on a padded X view (ld > f_in) into a padded Y view,
     and a graph-sized ragged tail (n % 128 != 0)."""

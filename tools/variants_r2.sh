@@ -11,6 +11,8 @@ for v in "$@"; do
     base) build base ;;
     ls64) build ls64 -DGSP_STAT_LONG_SLICE=64 ;;
     ls256) build ls256 -DGSP_STAT_LONG_SLICE=256 ;;
+    rawhi) build rawhi -DGSP_TC_RAWHI=1 ;;
+    rawhi8) build rawhi8 -DGSP_TC_RAWHI=1 -DGSP_TC_XS=8 ;;
     rpw4) build rpw4 -DGSP_STAT_RPW=4 ;;
     rpw8) build rpw8 -DGSP_STAT_RPW=8 ;;
     med1) build med1 -DGSP_STAT_MED_TILES=1 ;;
