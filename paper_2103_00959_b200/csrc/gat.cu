@@ -262,8 +262,8 @@ __device__ __forceinline__ void stat_short_rows(float *T, uint8_t *row_of, float
       const int d = (int)(__shfl_sync(0xffffffffu, rp_hi, q) - b);
       if (d == 0) continue;
       float *Tr = T + (b - B0) * H + h;
-      if (kApply && h == 0)
-        for (int j = part; j < d; j += P) row_of[b - B0 + j] = (uint8_t)q;
+      if (kApply)
+        for (int j = lane; j < d; j += 32) row_of[b - B0 + j] = (uint8_t)q;
       const double el_u = kScores ? (double)__shfl_sync(0xffffffffu, el_l, q * H + h) : 0.0;
       float mr = -INFINITY;
       {
