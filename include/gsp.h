@@ -360,9 +360,10 @@ gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const 
  * gsp_linear: row-major y[n][f_out] = x[n][f_in] w[f_in][f_out] (ldw >= f_out).
  *   With ws >= gsp_linear_workspace(f_in, f_out) bytes (device, any
  *   alignment), f_out <= 4096, ldx % 4 == 0 and x 16-byte aligned: tcgen05
- *   tensor cores, kind::tf32 with 3xTF32 splitting (x = hi + lo, w = hi + lo,
- *   x w ~= lo.hi + hi.lo + hi.hi, fp32 accumulation in TMEM; per-product
- *   error <= 2^-20 |x||w|), operands staged by TMA (SWIZZLE_64B: 16-float K
+ *   tensor cores, kind::tf32 with 3xTF32 splitting (x = hi + lo with hi the
+ *   MMA's truncated read of the raw fp32 x, w = hi + lo pre-split by
+ *   rounding; x w ~= lo.hi + hi.lo + hi.hi, fp32 accumulation in TMEM;
+ *   per-product error <= 2^-19 |x||w|), operands staged by TMA (SWIZZLE_64B: 16-float K
  *   tiles), one CTA per (128 rows, <= 256 output columns).  Otherwise (ws
  *   NULL / too small, wider or unaligned operands) a
  *   cuBLAS SGEMM with fp32 compute (no TF32); one cuBLAS handle per (thread,

@@ -532,8 +532,9 @@ def _lin_rel(f_in):
 
 
 def _tc_rel(f_in):
-    """3xTF32 tensor-core GEMM bound (DESIGN.md §NEXT rows): per product
-    <= 1.25 * 2^-20 |x||w| (TF32 lo parts + the dropped lo*lo term) <= 2^-19,
+    """3xTF32 tensor-core GEMM bound: per product
+    <= 2^-19 |x||w| (x_hi = the MMA's truncated read of x, the truncated lo
+    parts and the dropped lo*lo term),
     plus f_in fp32 accumulations at <= 2u each (tensor-core accumulation is
     not assumed to round to nearest)."""
     return 2.0 ** -19 + f_in * 2.0 ** -23
