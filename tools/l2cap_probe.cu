@@ -12,21 +12,22 @@
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s: %s\n", #x, cudaGetErrorString(e_)); return 1; } } while (0)
 
-__global__ void __launch_bounds__(256, 4) gather(const float4 *__restrict__ x, const uint32_t *__restrict__ idx,
+template <int MINB, int U>
+__global__ void __launch_bounds__(256, MINB) gather(const float4 *__restrict__ x, const uint32_t *__restrict__ idx,
                                                  int64_t nidx, float *out) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t base = warp * 8; base < nidx; base += nw * 8) {
-    float4 v[8];
+  for (int64_t base = warp * U; base < nidx; base += nw * U) {
+    float4 v[U];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint32_t r = idx[base + u];
       v[u] = __ldg(x + (int64_t)r * 32 + lane);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < U; ++u) {
       acc.x += v[u].x;
       acc.y += v[u].y;
       acc.z += v[u].z;
@@ -53,24 +54,33 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int sizes[] = {16, 24, 32, 40, 48, 56, 64, 72, 80, 96, 112, 128, 160, 256, 512};
-  for (int mb : sizes) {
-    const uint64_t rows = ((uint64_t)mb << 20) / 512;
-    for (int64_t i = 0; i < nidx; ++i) h[i] = (uint32_t)(rng() % rows);
-    CK(cudaMemcpy(d_idx, h.data(), nidx * 4, cudaMemcpyHostToDevice));
-    gather<<<sms * 4, 256>>>(d_x, d_idx, nidx, d_out);  // warm-up pass
-    CK(cudaDeviceSynchronize());
+  const int sizes[] = {64, 96, 119, 128, 160, 256};
+  auto run = [&](auto kern, int ctas, const char *name, int mb) {
+    kern<<<sms * ctas, 256>>>(d_x, d_idx, nidx, d_out);  // warm-up pass
+    cudaDeviceSynchronize();
     float best = 1e9f;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      gather<<<sms * 4, 256>>>(d_x, d_idx, nidx, d_out);
+      kern<<<sms * ctas, 256>>>(d_x, d_idx, nidx, d_out);
       cudaEventRecord(b);
-      CK(cudaEventSynchronize(b));
+      cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       if (ms < best) best = ms;
     }
-    printf("{\"probe\":\"l2cap\",\"x_MB\":%d,\"ms\":%.3f,\"GBps\":%.1f}\n", mb, best, nidx * 512.0 / (best * 1e-3) / 1e9);
+    printf("{\"probe\":\"l2cap\",\"kernel\":\"%s\",\"x_MB\":%d,\"ms\":%.3f,\"GBps\":%.1f}\n", name, mb, best,
+           nidx * 512.0 / (best * 1e-3) / 1e9);
+  };
+  for (int mb : sizes) {
+    const uint64_t rows = ((uint64_t)mb << 20) / 512;
+    for (int64_t i = 0; i < nidx; ++i) h[i] = (uint32_t)(rng() % rows);
+    CK(cudaMemcpy(d_idx, h.data(), nidx * 4, cudaMemcpyHostToDevice));
+    run(gather<4, 8>, 4, "4cta_u8", mb);
+    run(gather<6, 8>, 6, "6cta_u8", mb);
+    run(gather<8, 8>, 8, "8cta_u8", mb);
+    run(gather<4, 12>, 4, "4cta_u12", mb);
+    run(gather<4, 16>, 4, "4cta_u16", mb);
+    run(gather<2, 16>, 2, "2cta_u16", mb);
   }
   return 0;
 }
