@@ -75,6 +75,18 @@ def graphs_small():
         dst += list(range(base, base + dg))
         base += dg
     out.append(("hubs", base, src, dst, None, False, 1.0))
+    # many long rows (row statistics' long CTAs: several per 128-row slice,
+    # more than a group's slots, lengths at and around tile multiples for
+    # every head count) among short ones, directed
+    rng2 = np.random.default_rng(11)
+    nl = 2000
+    degs = np.where(rng2.random(nl) < 0.3, rng2.integers(30, 1300, nl), rng2.integers(0, 20, nl))
+    degs[:40] = [31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 511, 512, 513, 1023, 1024, 1025,
+                 2047, 2048, 2049, 200, 300, 400, 500, 600, 700, 800, 900, 1000, 1100, 1200, 130, 140, 150,
+                 160, 170, 180, 190, 1]
+    src = np.repeat(np.arange(nl), degs)
+    dst = rng2.integers(0, nl, src.size)
+    out.append(("longrows", nl, src, dst, None, False, 1.0))
     out.append(("star100k", 100001, [0] * 100000, list(range(1, 100001)), None, True, 1.0))
     return out
 
@@ -247,9 +259,9 @@ def test_spmm_errors(built):
 
 # ---------------------------------------------------------------- a4 - a7
 
-@pytest.mark.parametrize("H", [1, 2, 3, 4, 8, 16])
+@pytest.mark.parametrize("H", [1, 2, 3, 4, 8, 16, 32])
 def test_edge_softmax_parity(built, H):
-    for name in ("multi0", "cl4000", "hubs", "star100k"):
+    for name in ("multi0", "cl4000", "hubs", "longrows", "star100k"):
         go, gg, _, _ = built[name]
         for lo, hi in [(-3, 3), (-1e4, 1e4)]:
             lg = uniform((go.nnz, H), seed=H, low=lo, high=hi)
@@ -310,7 +322,7 @@ def test_gat_aggregate_parity(built, H, D, sched):
     with the CSR window), stats-launch ((m, 1/S) only, alpha formed in the
     aggregate; the schedule that also writes alpha_out) and single-launch
     (statistics reduced inside the aggregate)."""
-    for name in ("multi0", "cl4000", "rmat3000", "hubs"):
+    for name in ("multi0", "cl4000", "rmat3000", "hubs", "longrows"):
         go, gg, _, _ = built[name]
         n = go.n
         z = uniform((n, H * D), seed=3)
