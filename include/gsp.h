@@ -408,6 +408,31 @@ gsp_status gsp_gat_aggregate_bias_act(const gsp_csr *a, int32_t heads, const flo
  *   0), col_out int32 [slice nnz], val_out fp32 [slice nnz] (NULL to skip;
  *   ignored when a->val is NULL).
  */
+/* ---------------------------------------------------------------------------
+ * Column blocks of A for an L2-sized X footprint (a3):
+ * A = sum_k A_k with A_k the entries of A whose column lies in
+ * [col_bounds[k], col_bounds[k+1]); Y = A X is then computed as
+ * Y = A_0 X, Y += A_1 X, ... so each launch gathers from n_cols / blocks rows
+ * of X (C4: a 60 MB instead of a 119 MB slab footprint per 128 columns).
+ * gsp_csr_colblock_workspace: bytes of ws for `blocks` (1..8) blocks of a.
+ * gsp_csr_colblock: col_bounds HOST [blocks + 1], nondecreasing, col_bounds[0]
+ *   == 0, col_bounds[blocks] == n_cols.  Builds the blocks inside ws (device,
+ *   caller-owned, >= gsp_csr_colblock_workspace bytes; any alignment) and
+ *   fills the HOST array out[blocks] with CSRs that point into ws (valid as
+ *   long as ws is); each block keeps the row order and the column order of
+ *   a.  One stream sync (reads the block sizes).  A one-off per graph, like
+ *   gsp_coo_to_csr.
+ * gsp_spmm_blocked: y[:, :f] = sum_k blocks[k] x, summed in block order
+ *   (block 0 writes y, block k adds its partial with one rounding): a fixed
+ *   order per row, within the SpMM bound of gsp_spmm (one extra rounding per
+ *   block); blocks must share n_rows / n_cols.  x, y as for gsp_spmm.
+ */
+gsp_status gsp_csr_colblock_workspace(const gsp_csr *a, int32_t blocks, size_t *ws_bytes);
+gsp_status gsp_csr_colblock(const gsp_csr *a, const int64_t *col_bounds, int32_t blocks, void *ws, size_t ws_bytes,
+                            gsp_csr *out, gsp_stream stream);
+gsp_status gsp_spmm_blocked(const gsp_csr *blocks, int32_t nblocks, const float *x, int64_t f, int64_t ldx, float *y,
+                            int64_t ldy, gsp_stream stream);
+
 gsp_status gsp_partition_rows(const gsp_csr *a, int32_t parts, int64_t *row_bounds_dev,
                               int64_t *row_bounds_host, gsp_stream stream);
 gsp_status gsp_csr_slice(const gsp_csr *a, const int64_t *row_bounds, int32_t parts, int32_t rank,

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) scan_tile_kernel(const uint32_t *in, uint
   if (sums && tid == 0) sums[blockIdx.x] = total;
 }
 
-static size_t scan_ws_bytes(int64_t L) {
+size_t scan_ws_bytes(int64_t L) {
   size_t b = 0;
   while (L > kScanTile) {
     L = ceil_div(L, kScanTile);
@@ -87,7 +87,7 @@ static size_t scan_ws_bytes(int64_t L) {
 }
 
 // Exclusive scan of L uint32 (in may equal out); ws from scan_ws_bytes(L).
-static gsp_status scan_exclusive(const uint32_t *in, uint32_t *out, int64_t L, uint8_t *ws, cudaStream_t s) {
+gsp_status scan_exclusive(const uint32_t *in, uint32_t *out, int64_t L, uint8_t *ws, cudaStream_t s) {
   if (L <= 0) return GSP_OK;
   const int64_t nt = ceil_div(L, kScanTile);
   if (nt == 1) {

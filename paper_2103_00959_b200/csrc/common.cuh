@@ -40,6 +40,10 @@ inline bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes)
 
 gsp_status check_csr(const gsp_csr *a, bool need_val, const char *fn);
 
+// Exclusive scan of L uint32 (in may equal out), build.cu; ws >= scan_ws_bytes(L)
+size_t scan_ws_bytes(int64_t L);
+gsp_status scan_exclusive(const uint32_t *in, uint32_t *out, int64_t L, uint8_t *ws, cudaStream_t s);
+
 // GSP_VALIDATE mode of the calling thread (validate.cu) and the finite check
 // of logit-like inputs it enables
 bool validate_mode();

@@ -299,6 +299,25 @@ extern "C" gsp_status gsp_spmm_f16(const gsp_csr *a, const void *x, int64_t f, i
   return spmm_f16_part(a, L, xh, f, ldx, y, ldy, s);
 }
 
+extern "C" gsp_status gsp_spmm_blocked(const gsp_csr *blocks, int32_t nblocks, const float *x, int64_t f, int64_t ldx,
+                                       float *y, int64_t ldy, gsp_stream stream) {
+  const char *fn = "gsp_spmm_blocked";
+  clear_detail();
+  if (!blocks || nblocks < 1) return fail(GSP_ERR_INVALID_ARG, "%s: nblocks >= 1 blocks required", fn);
+  for (int k = 0; k < nblocks; ++k) {
+    gsp_status st = check_csr(&blocks[k], false, fn);
+    if (st) return st;
+    if (blocks[k].n_rows != blocks[0].n_rows || blocks[k].n_cols != blocks[0].n_cols)
+      return fail(GSP_ERR_INVALID_ARG, "%s: blocks must share n_rows and n_cols", fn);
+  }
+  cudaStream_t s = cs(stream);
+  // block 0 writes y, every further block adds its partial once (fixed order)
+  gsp_status st = spmm_impl(&blocks[0], x, f, ldx, y, ldy, nullptr, GSP_REDUCE_SUM, s, fn);
+  for (int k = 1; k < nblocks && !st; ++k)
+    st = spmm_acc_impl(&blocks[k], x, f, ldx, nullptr, 0, y, ldy, 1.0f, nullptr, 0, 0.0f, s, fn);
+  return st;
+}
+
 extern "C" gsp_status gsp_spmm_accumulate(const gsp_csr *a, const float *x, int64_t f, int64_t ldx, float *t,
                                           int64_t ldt, float *acc, int64_t ldacc, float coef, const float *src,
                                           int64_t ldsrc, float src_coef, gsp_stream stream) {

@@ -123,6 +123,30 @@ def test_host_validation_new_entry_points(L):
     assert n.value == max(100 * 8 * 16, 512 * 8 * 4)
 
 
+def test_colblock_host_validation(L):
+    """Column blocks: workspace query and bound checks on the host, before
+    any launch (gsp.h column blocks)."""
+    n = ctypes.c_size_t(0)
+    c = _csr(n_rows=100, n_cols=100, nnz=500)
+    assert L.gsp_csr_colblock_workspace(ctypes.byref(c), 0, ctypes.byref(n)) == 1
+    assert L.gsp_csr_colblock_workspace(ctypes.byref(c), 9, ctypes.byref(n)) == 1
+    assert L.gsp_csr_colblock_workspace(ctypes.byref(c), 2, ctypes.byref(n)) == 0
+    assert n.value >= 2 * 101 * 8 + 500 * 8  # two row_ptr, col + val once
+    out = (G.gsp_csr * 2)()
+    P = ctypes.c_void_p
+    ws = P(0x100000)
+    bad = [(0, 60, 99), (1, 60, 100), (0, 60, 40)]  # must span [0, n_cols), nondecreasing
+    for b in bad:
+        hb = (ctypes.c_int64 * 3)(*b)
+        assert L.gsp_csr_colblock(ctypes.byref(c), hb, 2, ws, n.value, out, P(0)) == 1, b
+    hb = (ctypes.c_int64 * 3)(0, 50, 100)
+    assert L.gsp_csr_colblock(ctypes.byref(c), hb, 2, ws, n.value - 1024, out, P(0)) == 6  # workspace too small
+    # gsp_spmm_blocked: no blocks / mismatched shapes
+    assert L.gsp_spmm_blocked(None, 1, P(0x1000), 4, 4, P(0x9000), 4, P(0)) == 1
+    two = (G.gsp_csr * 2)(_csr(n_rows=100, n_cols=100, nnz=500), _csr(n_rows=99, n_cols=100, nnz=500))
+    assert L.gsp_spmm_blocked(two, 2, P(0x1000), 4, 4, P(0x9000), 4, P(0)) == 1
+
+
 def test_build_workspace_query(L):
     ws = ctypes.c_size_t(0)
     nmax = ctypes.c_int64(0)

@@ -56,6 +56,28 @@ def test_c4_spmm_sampled_rows(c4):
     assert np.array_equal(y, y2)
 
 
+def test_c4_spmm_blocked_sampled_rows(c4):
+    """The column-blocked SpMM in bench.py's headline plan (G.colblock_bounds:
+    two column halves on C4) at full size: sampled rows + the 16 heaviest
+    hubs vs the oracle, the identity A^ sqrt(d) = sqrt(d) on every row, and
+    determinism."""
+    cfg, go, (deg, a64, a32), gg, gn = c4
+    bounds = G.colblock_bounds(gn, cfg.f)
+    assert len(bounds) == 3, bounds
+    blocks = G.gsp_csr_colblock(gn, bounds)
+    assert sum(blocks.nnz) == gn.nnz
+    x = G.empty_features(cfg.n, cfg.f, torch.device(DEV))
+    xh = features(cfg.n, cfg.f, cfg.f, seed=2)
+    x.copy_(dev(xh))
+    y = host(G.gsp_spmm_blocked(blocks, x, f=cfg.f))
+    for r in _sample_rows(go.row_ptr):
+        yr, cr = orc.spmm(go.row_ptr, go.col, a64, xh, f=cfg.f, r0=r, r1=r + 1)
+        assert_within(y[r:r + 1, :cfg.f], yr, cr, what=f"C4 blocked row {r}")
+    assert np.array_equal(y, host(G.gsp_spmm_blocked(blocks, x, f=cfg.f)))
+    s8 = torch.sqrt(gn.deg).float()[:, None].repeat(1, 8).contiguous()
+    np.testing.assert_allclose(host(G.gsp_spmm_blocked(blocks, s8)), np.sqrt(deg)[:, None].repeat(8, 1), rtol=3e-6)
+
+
 def test_c4_spmm_f16_sampled_rows(c4):
     """gsp_spmm_f16 at full size (bench's C4_spmm_f16_storage line) vs the oracle
     on the fp16 values, sampled rows incl. the heaviest hubs."""

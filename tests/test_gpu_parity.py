@@ -162,6 +162,37 @@ def test_normalize_in_place(built):
 FS = [1, 2, 3, 4, 5, 31, 32, 33, 127, 128, 129, 602, 1433]
 
 
+
+@pytest.mark.parametrize("kind", ["halves", "thirds", "eight", "empty-first", "single"])
+def test_colblock_structure_and_spmm(built, kind):
+    """Column blocks (gsp.h): every block is exactly the entries of A in its
+    column range, in A's order (bit-exact), and the blocked SpMM is within the
+    SpMM bound of the oracle and bitwise reproducible."""
+    for name in ("multi1", "er300-weighted", "cl4000", "rmat3000", "hubs", "longrows"):
+        go, gg, (deg, a64, a32), gn = built[name]
+        n = go.n
+        cuts = {"halves": [n // 2], "thirds": [n // 3, 2 * n // 3], "eight": [n * i // 8 for i in range(1, 8)],
+                "empty-first": [0, n // 2], "single": []}[kind]
+        bounds = [0] + cuts + [n]
+        blocks = G.gsp_csr_colblock(gn, bounds)
+        rows = np.repeat(np.arange(n), np.diff(go.row_ptr))
+        for k in range(len(bounds) - 1):
+            m = (go.col >= bounds[k]) & (go.col < bounds[k + 1])
+            rp = np.zeros(n + 1, np.int64)
+            rp[1:] = np.cumsum(np.bincount(rows[m], minlength=n))
+            b = blocks.block(k)
+            assert np.array_equal(host(b.row_ptr), rp), (name, kind, k)
+            assert np.array_equal(host(b.col), go.col[m]), (name, kind, k)
+            assert np.array_equal(host(b.val), a32[m]), (name, kind, k)
+        for f in (1, 33, 128, 300):
+            x = features(n, f, f, seed=f)
+            yref, cond = orc.spmm(go.row_ptr, go.col, a64, x, f=f)
+            y1 = G.gsp_spmm_blocked(blocks, dev(x), f=f)
+            y2 = G.gsp_spmm_blocked(blocks, dev(x), f=f)
+            assert torch.equal(y1, y2)
+            assert_within(host(y1)[:, :f], yref, cond, what=f"{name} {kind} f={f}")
+
+
 @pytest.mark.parametrize("f", FS)
 def test_spmm_parity(built, f):
     for name in ("k2", "isolated-nofill", "multi1", "multi4", "er300-weighted", "cl4000", "rmat3000", "hubs"):
