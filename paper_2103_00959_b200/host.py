@@ -18,7 +18,7 @@ from typing import List
 import torch
 from cuda.bindings import runtime as _rt
 
-from . import CSR, gsp_spmm
+from . import CSR, gsp_spmm, gsp_spmm_blocked
 
 
 def _copy2d(dst: torch.Tensor, src: torch.Tensor, kind, stream: torch.cuda.Stream):
@@ -33,8 +33,8 @@ def _copy2d(dst: torch.Tensor, src: torch.Tensor, kind, stream: torch.cuda.Strea
 class HostSpMM:
     """y_host[:, :f] = A @ x_host[:, :f] with pinned host x_host, y_host."""
 
-    def __init__(self, a: CSR, f: int, ld: int, slab: int = 128, device=None):
-        self.a, self.f, self.ld = a, f, ld
+    def __init__(self, a: CSR, f: int, ld: int, slab: int = 128, device=None, blocks=None):
+        self.a, self.f, self.ld, self.blocks = a, f, ld, blocks
         self.device = torch.device(device) if device is not None else a.row_ptr.device
         self.cols: List[int] = list(range(0, f, slab)) + [f]
         self.x = torch.empty((a.n_cols, ld), dtype=torch.float32, device=self.device)
@@ -56,7 +56,10 @@ class HostSpMM:
         for s in range(ns):
             c0, c1 = self.cols[s], self.cols[s + 1]
             main.wait_event(loaded[s])
-            gsp_spmm(self.a, self.x[:, c0:c1], f=c1 - c0, y=self.y[:, c0:c1])
+            if self.blocks is not None:  # column blocks of A (gsp_csr_colblock)
+                gsp_spmm_blocked(self.blocks, self.x[:, c0:c1], f=c1 - c0, y=self.y[:, c0:c1])
+            else:
+                gsp_spmm(self.a, self.x[:, c0:c1], f=c1 - c0, y=self.y[:, c0:c1])
             done[s].record(main)
         with torch.cuda.stream(self.d2h):
             for s in range(ns):
@@ -68,5 +71,6 @@ class HostSpMM:
 
     def launches(self) -> int:
         from . import gsp_spmm_plan_info
-        return sum(gsp_spmm_plan_info(self.a, self.x[:, c0:c1], c1 - c0)[0]
-                   for c0, c1 in zip(self.cols[:-1], self.cols[1:]))
+        mats = [self.blocks.block(k) for k in range(len(self.blocks))] if self.blocks is not None else [self.a]
+        return sum(gsp_spmm_plan_info(m, self.x[:, c0:c1], c1 - c0)[0]
+                   for m in mats for c0, c1 in zip(self.cols[:-1], self.cols[1:]))

@@ -65,6 +65,12 @@ def gcn(key, with_build=False):
     G.gsp_spmm(gn, x, f=cfg.f, y=y)
     with rng(f"ncu|{cfg.name}|a3_spmm"):
         G.gsp_spmm(gn, x, f=cfg.f, y=y)
+    bounds = G.colblock_bounds(gn, cfg.f)
+    if len(bounds) > 2:  # bench.py's headline plan (column blocks)
+        blocks = G.gsp_csr_colblock(gn, bounds)
+        G.gsp_spmm_blocked(blocks, x, f=cfg.f, y=y)
+        with rng(f"ncu|{cfg.name}|a3_spmm_colblocked"):
+            G.gsp_spmm_blocked(blocks, x, f=cfg.f, y=y)
 
 
 def gat(key, H, D):
