@@ -828,7 +828,9 @@ def main_dist(args):
     n, nnz, f = cfg.n, gn.nnz, cfg.f
     # each rank generates the full X deterministically and keeps its own rows
     x_host = features(n, f, cfg.ld, seed=2)
-    op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev, all_gather=ag)
+    cb = G.colblock_bounds(gn, f)  # the single-GPU headline's column blocks (global bounds)
+    op = RowPartitionedSpMM(gn, rank, world, f, chunks=args.chunks, device=dev, all_gather=ag,
+                            col_blocks=cb if len(cb) > 2 else None)
     xs = torch.from_numpy(np.ascontiguousarray(x_host[op.r0:op.r1, :f])).to(dev)
     op.load_shard(xs)
     y = G.empty_features(op.rows, f, dev)
@@ -869,7 +871,7 @@ def main_dist(args):
     xfull.copy_(torch.from_numpy(x_host[:, :f]))
     step()
     torch.cuda.synchronize()
-    y1 = G.gsp_spmm(gn, xfull, f=f)
+    y1 = G.gsp_spmm_blocked(G.gsp_csr_colblock(gn, cb), xfull, f=f) if len(cb) > 2 else G.gsp_spmm(gn, xfull, f=f)
     bitwise = allmax(0.0 if torch.equal(y, y1[op.r0:op.r1]) else 1.0) == 0.0
     del xfull, y1
     torch.cuda.empty_cache()

@@ -25,7 +25,8 @@ from typing import Callable, List, Optional
 
 import torch
 
-from . import CSR, feature_ld, gsp_attn_project, gsp_csr_slice, gsp_gat_aggregate, gsp_partition_rows, gsp_spmm
+from . import (CSR, feature_ld, gsp_attn_project, gsp_csr_colblock, gsp_csr_slice, gsp_gat_aggregate,
+               gsp_partition_rows, gsp_spmm, gsp_spmm_blocked)
 
 
 class GpuOps:
@@ -51,9 +52,35 @@ class GpuOps:
     def spmm(local, x, f, y):
         gsp_spmm(local, x, f=f, y=y)
 
+    @staticmethod
+    def colblock(local, bounds):
+        return gsp_csr_colblock(local, bounds)
+
+    @staticmethod
+    def spmm_blocked(blocks, x, f, y):
+        gsp_spmm_blocked(blocks, x, f=f, y=y)
+
 
 def padded_rows(bounds: List[int]) -> int:
     return max(bounds[p + 1] - bounds[p] for p in range(len(bounds) - 1))
+
+
+def remap_col_bounds(col_bounds: List[int], bounds: List[int], npad: int) -> List[int]:
+    """Global column bounds -> the gathered layout's (gsp_csr_slice: column c
+    of owner q -> q * npad + c - bounds[q]); the map is monotone, so a slice's
+    block k holds exactly the global columns [col_bounds[k], col_bounds[k+1])."""
+    world = len(bounds) - 1
+    out = []
+    for c in col_bounds:
+        if c <= 0:
+            out.append(0)
+            continue
+        if c >= bounds[world]:
+            out.append(world * npad)
+            continue
+        q = max(p for p in range(world) if bounds[p] <= c < bounds[p + 1])  # the (non-empty) owner of c
+        out.append(q * npad + (c - bounds[q]))
+    return out
 
 
 def chunk_bounds(f: int, chunks: int, align: int = 128) -> List[int]:
@@ -69,13 +96,19 @@ class RowPartitionedSpMM:
     """Y_shard = (A X)[rows of this rank] with X exchanged by all-gather."""
 
     def __init__(self, a: CSR, rank: int, world: int, f: int, chunks: int = 1,
-                 all_gather: Optional[Callable] = None, device=None, ops=GpuOps):
+                 all_gather: Optional[Callable] = None, device=None, ops=GpuOps, col_blocks=None):
         self.rank, self.world, self.f, self.ops = rank, world, f, ops
         self.bounds = [int(b) for b in ops.partition(a, world)]
         self.npad = padded_rows(self.bounds)
         self.r0, self.r1 = self.bounds[rank], self.bounds[rank + 1]
         self.rows = self.r1 - self.r0
         self.local = ops.slice(a, self.bounds, rank, self.npad)
+        # column blocks (gsp_spmm_blocked): the GLOBAL bounds mapped into the
+        # gathered layout, so each row's block partials and their sum are the
+        # single-GPU gsp_spmm_blocked's (bitwise)
+        self.col_blocks = None
+        if col_blocks is not None and len(col_blocks) > 2 and self.rows:
+            self.col_blocks = ops.colblock(self.local, remap_col_bounds(list(col_blocks), self.bounds, self.npad))
         self.cols = chunk_bounds(f, chunks)
         self.device = torch.device(device) if device is not None else a.row_ptr.device
         self.all_gather = all_gather or (lambda out, inp: torch.distributed.all_gather_into_tensor(out, inp))
@@ -120,7 +153,9 @@ class RowPartitionedSpMM:
 
     def _local(self, k: int, y: torch.Tensor):
         c0, c1 = self.cols[k], self.cols[k + 1]
-        if self.rows:
+        if self.rows and self.col_blocks is not None:
+            self.ops.spmm_blocked(self.col_blocks, self.gathered[k][:, :c1 - c0], c1 - c0, y[:, c0:c1])
+        elif self.rows:
             self.ops.spmm(self.local, self.gathered[k][:, :c1 - c0], c1 - c0, y[:, c0:c1])
 
 

@@ -186,3 +186,26 @@ def test_head_chunks():
     assert head_chunks(8, 64, 8) == [0, 2, 4, 6, 8]   # never narrower than one slab when avoidable
     assert head_chunks(4, 128, 4) == [0, 1, 2, 3, 4]
     assert head_chunks(3, 16, 2) == [0, 2, 3]
+
+
+def test_remap_col_bounds_keeps_block_membership():
+    """Column blocks under the row partition: a column's block in the gathered
+    layout (gsp_csr_slice's remap q * npad + c - b_q) is its global block."""
+    from paper_2103_00959_b200.dist import padded_rows, remap_col_bounds
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(rng.integers(5, 400))
+        world = int(rng.integers(1, 6))
+        cuts = sorted(rng.integers(0, n + 1, world - 1).tolist())
+        bounds = [0] + cuts + [n]
+        npad = max(1, padded_rows(bounds))
+        kb = int(rng.integers(1, 5))
+        cb = [0] + sorted(rng.integers(0, n + 1, kb - 1).tolist()) + [n]
+        rb = remap_col_bounds(cb, bounds, npad)
+        assert rb[0] == 0 and rb[-1] == world * npad and rb == sorted(rb)
+        for c in range(n):
+            q = max(p for p in range(world) if bounds[p] <= c < bounds[p + 1])
+            r = q * npad + c - bounds[q]
+            kg = max(k for k in range(kb) if cb[k] <= c)
+            kr = max(k for k in range(kb) if rb[k] <= r)
+            assert kg == kr, (n, bounds, cb, c)

@@ -53,6 +53,15 @@ def _worker(rank, world, port, backend, chunks, q):
         y = op()
         torch.cuda.synchronize()
         ok = torch.equal(y, y_ref[op.r0:op.r1])
+        # column blocks: global bounds mapped into each slice's gathered layout
+        # give the single-GPU gsp_spmm_blocked bitwise
+        cb = [0, n // 3, 2 * n // 3, n]
+        ob = RowPartitionedSpMM(g, rank, world, f, chunks=chunks, device=dev, col_blocks=cb,
+                                all_gather=None if backend == "nccl" else _staged_gather)
+        ob.load_shard(x[ob.r0:ob.r1, :f])
+        yb = ob()
+        torch.cuda.synchronize()
+        ok = ok and torch.equal(yb, G.gsp_spmm_blocked(G.gsp_csr_colblock(g, cb), x, f=f)[ob.r0:ob.r1])
         # K-step propagation through the same partition (NEXT-4)
         from paper_2103_00959_b200.dist import RowPartitionedPropagate
         th = [0.1 * 0.9 ** k for k in range(6)]

@@ -57,5 +57,9 @@ G.gsp_sym_normalize(g, keep_deg=False)
 xa = G.empty_features(n, 602, dev)
 xa.copy_(torch.from_numpy(features(n, 602, 602, seed=9)))
 G.gsp_spmm(gn, xa)
+# column blocks (split + blocked SpMM, incl. an empty block)
+for bnds in ([0, n // 2, n], [0, 0, n // 3, n]):
+    blocks = G.gsp_csr_colblock(gn, bnds)
+    G.gsp_spmm_blocked(blocks, xa)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
