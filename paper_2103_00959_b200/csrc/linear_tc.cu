@@ -30,11 +30,12 @@
 namespace gsp {
 
 constexpr int kTcBM = 128, kTcBK = 16;  // K tile: 16 fp32 = 64-byte rows (SWIZZLE_64B)
-constexpr int kTcNT = 256;              // max output columns per CTA (grid.y tiles wider outputs)
+constexpr int kTcNT = 256;  // max output columns per CTA (grid.y tiles wider outputs)
 constexpr int kTcThreads = 192;
 #ifndef GSP_TC_RAWHI
 #define GSP_TC_RAWHI 1
 #endif
+
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -92,6 +93,24 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
+// A operand from TMEM (lane = row of the 128-row tile, column = K element)
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -104,6 +123,11 @@ struct TcParams {
   uint32_t tmem_cols;
 };
 
+// kAT (outputs of <= 128 columns): x_hi / x_lo go to TMEM (the MMA's A
+// operand from TMEM; accumulator + 4 A stages = 256 columns, so two CTAs
+// still share an SM) and X's shared-memory slot is read once by the
+// converters instead of read + rewritten and then read by three MMAs
+template <bool kAT>
 __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
                                                                  const __grid_constant__ CUtensorMap tm_b,
                                                                  const TcParams p) {
@@ -111,10 +135,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
   __shared__ __align__(8) uint64_t s_full[4], s_split[4], s_empty[4], s_done;
   __shared__ uint32_t s_tmem;
   // 1024-byte aligned stage buffers: A_hi [128x16], A_lo [128x16], B_hi [Nx16], B_lo [Nx16] fp32
+  // (kAT: X [128x16] only -- x_hi / x_lo go to TMEM -- then B_hi, B_lo)
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = kTcBM * kTcBK * 4, b_bytes = (uint32_t)p.nt * kTcBK * 4;
   const int n0 = blockIdx.y * p.nt;  // first output column of this CTA
-  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  constexpr uint32_t kAParts = kAT ? 1 : 2;
+  const uint32_t stage_bytes = kAParts * a_bytes + 2 * b_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = (int64_t)blockIdx.x * kTcBM;
   const int S = p.stages, KT = p.kt_count;
@@ -147,8 +173,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
         uint8_t *st = base + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&s_full[s], a_bytes + 2 * b_bytes);
         tma_load_2d(st, &tm_x, kt * kTcBK, (int)m0, &s_full[s]);
-        tma_load_2d(st + 2 * a_bytes, &tm_b, kt * kTcBK, n0, &s_full[s]);
-        tma_load_2d(st + 2 * a_bytes + b_bytes, &tm_b, kt * kTcBK, p.n_pad + n0, &s_full[s]);
+        tma_load_2d(st + kAParts * a_bytes, &tm_b, kt * kTcBK, n0, &s_full[s]);
+        tma_load_2d(st + kAParts * a_bytes + b_bytes, &tm_b, kt * kTcBK, p.n_pad + n0, &s_full[s]);
       }
     }
   } else if (warp == 1) {
@@ -159,8 +185,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
         mbar_wait(&s_split[s], (uint32_t)((kt / S) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t st = smem_u32(base + (size_t)s * stage_bytes);
+        const uint64_t bhi = umma_desc_sw64(st + kAParts * a_bytes), blo = umma_desc_sw64(st + kAParts * a_bytes + b_bytes);
+        if constexpr (kAT) {
+        const uint32_t a_t = tmem + (uint32_t)(p.nt + s * 2 * kTcBK);  // x_hi columns, then x_lo
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 8; ++kk) {  // K = 8 tf32 per MMA: 8 TMEM columns of A, 32 bytes of B
+          const uint64_t o = (uint64_t)(kk * 2);
+          const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32_ta(tmem, a_t + kTcBK + kk * 8, bhi + o, idesc, acc);  // small terms first
+          mma_tf32_ta(tmem, a_t + kk * 8, blo + o, idesc, 1u);
+          mma_tf32_ta(tmem, a_t + kk * 8, bhi + o, idesc, 1u);
+        }
+        } else {
         const uint64_t ahi = umma_desc_sw64(st), alo = umma_desc_sw64(st + a_bytes);
-        const uint64_t bhi = umma_desc_sw64(st + 2 * a_bytes), blo = umma_desc_sw64(st + 2 * a_bytes + b_bytes);
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 8; ++kk) {  // K = 8 tf32 (32 bytes) per MMA: advance start by 2 (x16 B) inside the atom
           const uint64_t o = (uint64_t)(kk * 2);
@@ -169,6 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
           mma_tf32(tmem, ahi + o, blo + o, idesc, 1u);
           mma_tf32(tmem, ahi + o, bhi + o, idesc, 1u);
         }
+        }
         mma_commit(&s_empty[s]);  // stage reusable once these MMAs have read it
       }
       mma_commit(&s_done);
@@ -176,6 +214,37 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
   } else {
     // warps 2-5: split X tiles, then the epilogue
     const int t = threadIdx.x - 64;  // 0..127
+    if constexpr (kAT) {
+    // thread = one row of the tile, in this warp's TMEM lane quadrant: read the
+    // row's 16 values from the SWIZZLE_64B tile (16-byte chunk c of row r sits
+    // at chunk c ^ ((r >> 1) & 3)), store x (the MMA reads it as trunc_tf32(x))
+    // and x - trunc_tf32(x) into the stage's TMEM columns
+    (void)t;
+    const int arow = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % S;
+      mbar_wait(&s_full[s], (uint32_t)((kt / S) & 1));
+      const uint8_t *xt = base + (size_t)s * stage_bytes + (size_t)arow * 64;
+      uint32_t xh[16], xl[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 v = *reinterpret_cast<const float4 *>(xt + ((c ^ ((arow >> 1) & 3)) << 4));
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          xh[4 * c + i] = __float_as_uint(vv[i]);
+          xl[4 * c + i] = __float_as_uint(vv[i] - __uint_as_float(__float_as_uint(vv[i]) & 0xffffe000u));
+        }
+      }
+      const uint32_t acol = (uint32_t)(p.nt + s * 2 * kTcBK);
+      tmem_st16(lane_base + acol, xh);
+      tmem_st16(lane_base + acol + kTcBK, xl);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&s_split[s]);
+    }
+    } else {
     for (int kt = 0; kt < KT; ++kt) {
       const int s = kt % S;
       mbar_wait(&s_full[s], (uint32_t)((kt / S) & 1));
@@ -206,6 +275,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core (async) proxy
       mbar_arrive(&s_split[s]);
+    }
     }
     // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (rows of the tile)
     mbar_wait(&s_done, 0);
@@ -317,22 +387,27 @@ gsp_status linear_tc(int64_t n, int64_t f_in, const float *x, int64_t ldx, const
   p.n_pad = n_pad;
   p.nt = nt;
   p.kt_count = (int)((f_in + kTcBK - 1) / kTcBK);
-  uint32_t cols = 32;
-  while ((int)cols < nt) cols *= 2;
-  p.tmem_cols = cols;
-  const size_t stage = (size_t)2 * kTcBM * kTcBK * 4 + (size_t)2 * nt * kTcBK * 4;
+  const bool at = nt <= 128;  // x_hi / x_lo in TMEM (see linear_tc_kernel<true>)
+  const size_t stage = (size_t)(at ? 1 : 2) * kTcBM * kTcBK * 4 + (size_t)2 * nt * kTcBK * 4;
   int stages = (int)std::min<size_t>(4, (100u * 1024u) / stage);  // <= ~100 KB: 2 CTAs per SM
   p.stages = std::max(stages, 2);
+  uint32_t cols = 32;
+  while ((int)cols < nt + (at ? p.stages * 2 * kTcBK : 0)) cols *= 2;  // accumulator (+ A stages)
+  p.tmem_cols = cols;
   const size_t smem = (size_t)p.stages * stage + 1024;
-  static std::atomic<int> granted[64];  // per device: largest dynamic smem already granted
+  static std::atomic<int> granted[2][64];  // per kernel variant and device: largest dynamic smem already granted
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || granted[dev].load(std::memory_order_relaxed) < (int)smem) {
-    if (cudaFuncSetAttribute(linear_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(linear_tc_kernel)");
-    if (dev >= 0 && dev < 64) granted[dev].store((int)smem, std::memory_order_relaxed);
+  if (dev < 0 || dev >= 64 || granted[at][dev].load(std::memory_order_relaxed) < (int)smem) {
+    const cudaError_t e =
+        at ? cudaFuncSetAttribute(linear_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+           : cudaFuncSetAttribute(linear_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return check_launch("cudaFuncSetAttribute(linear_tc_kernel)");
+    if (dev >= 0 && dev < 64) granted[at][dev].store((int)smem, std::memory_order_relaxed);
   }
-  linear_tc_kernel<<<dim3((unsigned)ceil_div(n, kTcBM), (unsigned)ntiles), kTcThreads, smem, s>>>(tx, tb, p);
+  const dim3 grid((unsigned)ceil_div(n, kTcBM), (unsigned)ntiles);
+  if (at) linear_tc_kernel<true><<<grid, kTcThreads, smem, s>>>(tx, tb, p);
+  else linear_tc_kernel<false><<<grid, kTcThreads, smem, s>>>(tx, tb, p);
   return check_launch("linear_tc_kernel");
 }
 
