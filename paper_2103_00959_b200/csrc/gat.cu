@@ -4,6 +4,10 @@
 // softmax with warp-level max / sum reductions); readings A9-A14.
 #include "spmm_engine.cuh"
 
+#ifndef GSP_HM_WIN_BYTES
+#define GSP_HM_WIN_BYTES 43008
+#endif
+
 namespace gsp {
 
 // ------------------------------------------------------------------------
@@ -870,10 +874,10 @@ static gsp_status gat_aggregate_impl(const gsp_csr *a, int32_t heads, const floa
   st = engine_plan(a->n_rows, a->n_cols, a->nnz, f, d, vmax, 0, 0, &L, (pre || hm) ? kMaxHpt : 1);
   if (st) return st;
   if (hm) {
-    // keep the staged window (col + hpt weight runs) within ~42 KB so four
-    // CTAs still fit on an SM (the 64-register budget allows four)
+    // keep the staged window (col + hpt weight runs) within ~42 KB: smaller
+    // row blocks balance better (a 60 KB window measured 0.452 -> 0.477 ms on C3)
     const int hpt = engine_hpt(L, d, heads);
-    const int64_t win_max = 43008 / (4 * (1 + hpt));
+    const int64_t win_max = GSP_HM_WIN_BYTES / (4 * (1 + hpt));
     int64_t c = ((win_max - kHub - 8) / 512) * 512;
     if (c < 512) c = 512;
     if (c < L.block_nnz) {

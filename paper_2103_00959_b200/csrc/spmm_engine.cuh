@@ -53,6 +53,9 @@ constexpr int kVirt = 16;          // virtual ranges of a hub row
 constexpr int kMaxHubPerBlock = 64;
 constexpr int kStageChunks = 4;   // TMA bulk-copy chunks of the CSR window
 constexpr int kMaxHpt = 4;        // heads per team (multi-head modes)
+#ifndef GSP_HM_U
+#define GSP_HM_U 8
+#endif
 #ifndef GSP_MIN_BLOCKS
 #define GSP_MIN_BLOCKS 4
 #endif
@@ -522,7 +525,9 @@ __device__ __forceinline__ void seg_gather(const int32_t *sc, const float *sw, i
   constexpr int SPR = TM::SPR, NACC = TM::NACC, EPS = TM::EPS;
   // gathers in flight per lane: the element policy's budget; the single-launch
   // GAT (in-kernel statistics, fp64 row state live) measured best at 4
-  constexpr int kUx = Row::kInStats ? (XE::kU < 4 ? XE::kU : 4) : XE::kU;
+  constexpr int kUx = Row::kInStats ? (XE::kU < 4 ? XE::kU : 4)
+                      : HasStagedHeads<Row>::value ? (XE::kU < GSP_HM_U ? XE::kU : GSP_HM_U)
+                                                   : XE::kU;
   constexpr int U = TM::U < kUx ? TM::U : kUx;
   using Raw = typename XE::Raw;
   static_assert(EPS % U == 0, "GSP_UNROLL must divide the edges per sub-group and segment (power of two)");
@@ -712,9 +717,23 @@ __device__ __forceinline__ void finish_row(float (&out)[V], int64_t d, int mean)
 #ifndef GSP_GATPRE_MIN_BLOCKS
 #define GSP_GATPRE_MIN_BLOCKS 3
 #endif
+// multi-head SpMM with stored alpha (WeightAlpha) and the fused GAT's staged
+// head-major alpha (WeightAlphaHM): 3 CTAs/SM (85 registers).  At 64 registers
+// the per-lane head offset and weight pointers spill inside the segment loop
+// (120 / 152 B of local stores / loads); measured on C3 (8 x 64): fused GAT
+// 0.532 -> 0.452 ms, multi-head SpMM 0.456 -> 0.427 ms (C2g 8 x 64: +-5%,
+// tools/c3_probe.py)
+#ifndef GSP_HM_MIN_BLOCKS
+#define GSP_HM_MIN_BLOCKS 3
+#endif
+#ifndef GSP_MH_MIN_BLOCKS
+#define GSP_MH_MIN_BLOCKS 3
+#endif
 template <class W, class XE>
 struct MinBlocksFor {  // measured on C3 (8 x 64): multi-head computed weights 0.74 -> 0.67 ms at 3 CTAs/SM
   static constexpr int value = XE::kMinBlocks ? XE::kMinBlocks
+                               : HasStagedHeads<typename W::Row>::value ? GSP_HM_MIN_BLOCKS
+                               : (W::Row::kMultiHead && !W::Row::kComputed) ? GSP_MH_MIN_BLOCKS
                                : !W::Row::kComputed ? kMinBlocks
                                : (W::Row::kMultiHead ? GSP_GATPRE_MIN_BLOCKS : GSP_GAT_MIN_BLOCKS);
 };
