@@ -36,6 +36,12 @@ for name, n, f_in, f_out in [("C4-l1", 232965, 602, 128), ("C5-l1", 716847, 300,
             ts.append(a.elapsed_time(b))
         ms = float(np.median(ts))
         row["tc_ms" if tc else "cublas_ms"] = ms
+        if tc:  # error vs fp64, scaled by |x||w| (the 3xTF32 bound is 2^-19 + F_in 2^-23)
+            fn()
+            torch.cuda.synchronize()
+            xs, ws_ = x[:4096].double(), w.double()
+            ref = xs @ ws_
+            row["tc_err_over_scale"] = float(((y[:4096].double() - ref).abs() / (xs.abs() @ ws_.abs())).max())
         row["tc_TFLOPs" if tc else "cublas_TFLOPs"] = 2 * n * f_in * f_out / ms / 1e9
     res.append(row)
     print(json.dumps(row), flush=True)
