@@ -32,6 +32,9 @@ namespace gsp {
 constexpr int kTcBM = 128, kTcBK = 16;  // K tile: 16 fp32 = 64-byte rows (SWIZZLE_64B)
 constexpr int kTcNT = 256;  // max output columns per CTA (wider outputs: several adjacent CTAs per row tile)
 constexpr int kTcThreads = 192;
+#ifndef GSP_TC_MC
+#define GSP_TC_MC 1
+#endif
 #ifndef GSP_TC_RAWHI
 #define GSP_TC_RAWHI 1
 #endif
@@ -111,6 +114,36 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+// TMA 2-D tile load multicast to the CTAs of ctamask (same smem offset and
+// mbarrier offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *tm, int c0, int c1, uint64_t *bar,
+                                               uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(ctamask)
+      : "memory");
+}
+
+// MMA completion arrives on the mbarrier at this offset in every CTA of ctamask
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t ctamask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(ctamask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -127,7 +160,11 @@ struct TcParams {
 // operand from TMEM; accumulator + 4 A stages = 256 columns, so two CTAs
 // still share an SM) and X's shared-memory slot is read once by the
 // converters instead of read + rewritten and then read by three MMAs
-template <bool kAT>
+// kMC = 2 (kAT only): CTA pairs (a cluster of two adjacent 128-row tiles)
+// share the W tiles -- CTA r loads W_hi (r = 0) or W_lo (r = 1) and the TMA
+// engine multicasts it into both CTAs, halving W's L2 traffic; a stage is
+// refilled only after both CTAs' MMAs released it (commits multicast to both).
+template <bool kAT, int kMC = 1>
 __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_constant__ CUtensorMap tm_x,
                                                                  const __grid_constant__ CUtensorMap tm_b,
                                                                  const TcParams p) {
@@ -147,17 +184,26 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
   const uint32_t stage_bytes = kAParts * a_bytes + 2 * b_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m0 = (int64_t)(blockIdx.x / ntiles) * kTcBM;
+  // a CTA pair's padding CTA (grid rounded up to even) loads the last real
+  // tile and stores nothing (its rows are >= n)
+  const int64_t m0_ld = m0 < p.n ? m0 : ((p.n - 1) / kTcBM) * kTcBM;
   const int S = p.stages, KT = p.kt_count;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&s_split[s], 128);
-      mbar_init(&s_empty[s], 1);
+      mbar_init(&s_empty[s], kMC);
     }
     mbar_init(&s_done, 1);
     fence_mbar_init();
   }
+  if constexpr (kMC > 1) {  // the peer's barriers must be initialised before anything is multicast to it
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    cluster_sync_all();
+  }
+  const uint32_t crank = kMC > 1 ? cluster_ctarank() : 0u;
+  constexpr uint16_t kMask = (uint16_t)((1u << kMC) - 1u);
   if (warp == 1) {  // TMEM accumulator: 128 lanes x tmem_cols fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(p.tmem_cols)
@@ -176,9 +222,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
         if (kt >= S) mbar_wait(&s_empty[s], (uint32_t)((kt / S - 1) & 1));
         uint8_t *st = base + (size_t)s * stage_bytes;
         mbar_arrive_expect_tx(&s_full[s], a_bytes + 2 * b_bytes);
-        tma_load_2d(st, &tm_x, kt * kTcBK, (int)m0, &s_full[s]);
-        tma_load_2d(st + kAParts * a_bytes, &tm_b, kt * kTcBK, n0, &s_full[s]);
-        tma_load_2d(st + kAParts * a_bytes + b_bytes, &tm_b, kt * kTcBK, p.n_pad + n0, &s_full[s]);
+        tma_load_2d(st, &tm_x, kt * kTcBK, (int)m0_ld, &s_full[s]);
+        if constexpr (kMC > 1) {  // this CTA's W part (hi or lo) into both CTAs of the pair
+          tma_load_2d_mc(st + kAParts * a_bytes + crank * b_bytes, &tm_b, kt * kTcBK, (int)crank * p.n_pad + n0,
+                         &s_full[s], kMask);
+        } else {
+          tma_load_2d(st + kAParts * a_bytes, &tm_b, kt * kTcBK, n0, &s_full[s]);
+          tma_load_2d(st + kAParts * a_bytes + b_bytes, &tm_b, kt * kTcBK, p.n_pad + n0, &s_full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -211,7 +262,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
           mma_tf32(tmem, ahi + o, bhi + o, idesc, 1u);
         }
         }
-        mma_commit(&s_empty[s]);  // stage reusable once these MMAs have read it
+        if constexpr (kMC > 1) mma_commit_mc(&s_empty[s], kMask);  // both CTAs' W slots
+        else mma_commit(&s_empty[s]);  // stage reusable once these MMAs have read it
       }
       mma_commit(&s_done);
     }
@@ -312,6 +364,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) linear_tc_kernel(const __grid_c
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  // no CTA of a pair exits while its peer may still multicast into it or
+  // arrive on its barriers (every MMA of both has completed past this point)
+  if constexpr (kMC > 1) cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
@@ -399,15 +454,38 @@ gsp_status linear_tc(int64_t n, int64_t f_in, const float *x, int64_t ldx, const
   while ((int)cols < nt + (at ? p.stages * 2 * kTcBK : 0)) cols *= 2;  // accumulator (+ A stages)
   p.tmem_cols = cols;
   const size_t smem = (size_t)p.stages * stage + 1024;
-  static std::atomic<int> granted[2][64];  // per kernel variant and device: largest dynamic smem already granted
+  // CTA pairs sharing W (linear_tc_kernel<true, 2>) for long K: C4 layer 1
+  // (F_in 602) 0.222 -> 0.211 ms, C3 layer 1 (500) 0.091 -> 0.089; shorter K
+  // measured slower (C5 layer 1, F_in 300: 0.371 -> 0.380; F_in 128: +15%)
+  const bool mc = at && GSP_TC_MC && f_in >= 384;
+  const int var = mc ? 2 : (at ? 1 : 0);
+  static std::atomic<int> granted[3][64];  // per kernel variant and device: largest dynamic smem already granted
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || granted[at][dev].load(std::memory_order_relaxed) < (int)smem) {
+  if (dev < 0 || dev >= 64 || granted[var][dev].load(std::memory_order_relaxed) < (int)smem) {
     const cudaError_t e =
-        at ? cudaFuncSetAttribute(linear_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-           : cudaFuncSetAttribute(linear_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        mc ? cudaFuncSetAttribute(linear_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        : at ? cudaFuncSetAttribute(linear_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+             : cudaFuncSetAttribute(linear_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return check_launch("cudaFuncSetAttribute(linear_tc_kernel)");
-    if (dev >= 0 && dev < 64) granted[at][dev].store((int)smem, std::memory_order_relaxed);
+    if (dev >= 0 && dev < 64) granted[var][dev].store((int)smem, std::memory_order_relaxed);
+  }
+  if (mc) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((ceil_div(n, kTcBM) + 1) / 2 * 2));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, linear_tc_kernel<true, 2>, tx, tb, p) != cudaSuccess)
+      return check_launch("cudaLaunchKernelEx(linear_tc_kernel<true, 2>)");
+    return check_launch("linear_tc_kernel<true, 2>");
   }
   const dim3 grid((unsigned)(ceil_div(n, kTcBM) * ntiles));
   if (at) linear_tc_kernel<true><<<grid, kTcThreads, smem, s>>>(tx, tb, p);

@@ -586,8 +586,12 @@ def _tc_rel(f_in):
 @pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cublas"])
 @pytest.mark.parametrize("n,f_in,f_out", [(5000, 3, 5), (5000, 33, 7), (5000, 128, 41), (5000, 602, 128),
                                           (1, 1, 1), (128, 32, 16), (129, 31, 17), (3000, 1433, 256),
-                                          (2000, 300, 128), (777, 500, 41), (1000, 64, 512), (500, 100, 300)])
+                                          (2000, 300, 128), (777, 500, 41), (1000, 64, 512), (500, 100, 300),
+                                          (100, 512, 128), (129, 400, 16)])
 def test_linear_parity(n, f_in, f_out, tc):
+    # f_in >= 384 with f_out <= 128 takes the CTA-pair (shared W) kernel; odd
+    # tile counts (777 -> 7, 100 -> 1, 129 -> 2 with a ragged tail) exercise
+    # its padding CTA
     x = uniform((n, f_in), seed=1)
     w = uniform((f_in, f_out), seed=2)
     y = host(G.gsp_linear(dev(x), dev(w), tensor_cores=tc))
