@@ -39,7 +39,7 @@ xin = torch.from_numpy(features(n, 50, 52)).to(dev)[:, :50]
 gcn_inference(gn, xin, GCNParams.init(50, 32, 7, dev))
 gat_inference(g, xin, GATParams.init(50, 32, 4, 7, dev))
 # tensor-core dense step (3xTF32 tcgen05, incl. a ragged row tail and two N tiles) and fp16-storage SpMM
-for (rows, fi, fo) in ((300, 37, 41), (129, 64, 300)):
+for (rows, fi, fo) in ((300, 37, 41), (129, 64, 300), (300, 400, 64)):  # 400: CTA pairs sharing W (3 tiles + pad)
     xl = torch.from_numpy(features(rows, fi, (fi + 3) // 4 * 4, seed=5)).to(dev)[:, :fi]
     G.gsp_linear(xl, torch.from_numpy(uniform((fi, fo), seed=6)).to(dev))
 for f in (5, 128, 300):
