@@ -434,42 +434,93 @@ __device__ __forceinline__ float norm_entry(double du, double dv, float w) {
   return __double2float_rn(r);
 }
 
-__global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                                        const float *val, int64_t n, const double *__restrict__ deg,
-                                                        float *val_out) {
-  // rows of at most kNormLong entries: one warp each (no CTA barrier);
-  // longer rows are left to normalize_long_kernel
-  const int lane = threadIdx.x & 31;
-  const int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (u >= n) return;
-  const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
-  if (e1 - b > kNormLong) return;
-  const double du = __ldg(deg + u);
-#pragma unroll 2
-  for (int64_t e = b + lane; e < e1; e += 32) val_out[e] = norm_entry(du, __ldg(deg + __ldg(col + e)), val[e]);
-}
-
-// entries of rows longer than kNormLong, edge-balanced: warp w takes entries
-// [256 w, 256 w + 256); each lane walks the rows its entries fall in (from
-// the warp's first row) and normalises the entries of long rows only
-constexpr int kNormChunk = 256;
-__global__ void __launch_bounds__(256) normalize_long_kernel(const int64_t *__restrict__ rp,
-                                                             const int32_t *__restrict__ col, const float *val,
-                                                             int64_t n, int64_t nnz, const double *__restrict__ deg,
-                                                             float *val_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t e0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kNormChunk;
-  if (e0 >= nnz) return;
-  const int64_t e1 = min(nnz, e0 + kNormChunk);
-  int64_t u = warp_lower_bound(rp, n, e0 + 1) - 1;  // row holding entry e0
-  int64_t ub = __ldg(rp + u), ue = __ldg(rp + u + 1);
-  for (int64_t e = e0 + lane; e < e1; e += 32) {
-    while (e >= ue) {
-      ++u;
-      ub = ue;
-      ue = __ldg(rp + u + 1);
+// One launch, two kinds of CTA (long ones first, so the power-law tail
+// overlaps the bulk):
+//  * LONG CTA c scans rows [256 c, 256 c + 256) (one coalesced load of their
+//    extents), collects the rows of more than kNormLong entries in shared
+//    memory and normalises each with the whole CTA, 4 entries per thread per
+//    round (every load of a round issued before the arithmetic);
+//  * SHORT CTA b owns rows [32 b, 32 b + 32): their entries are contiguous,
+//    so the CTA walks them edge-parallel (coalesced col / val loads, 4 per
+//    thread per round), finds each entry's row by a binary search of the 33
+//    staged row pointers and skips entries of long rows.
+// Each value depends on (d_u, d_v, w) only: bit-identical to any schedule.
+constexpr int kNormSlice = 256;  // rows scanned by a long CTA
+constexpr int kNormRows = 32;    // rows of a short CTA
+__global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restrict__ rp,
+                                                        const int32_t *__restrict__ col, const float *val,
+                                                        int64_t n, const double *__restrict__ deg, float *val_out,
+                                                        int n_long) {
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < n_long) {
+    __shared__ int s_long[kNormSlice];
+    __shared__ int s_n;
+    const int64_t r0 = (int64_t)blockIdx.x * kNormSlice;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    const int64_t r = r0 + tid;
+    if (r < n && __ldg(rp + r + 1) - __ldg(rp + r) > kNormLong) s_long[atomicAdd(&s_n, 1)] = tid;
+    __syncthreads();
+    const int nl = s_n;
+    for (int k = 0; k < nl; ++k) {
+      const int64_t u = r0 + s_long[k];
+      const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
+      const double du = __ldg(deg + u);
+      for (int64_t e0 = b + tid; e0 < e1; e0 += 4 * 256) {
+        int c[4];
+        float w[4];
+        double dv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t e = e0 + 256 * q;
+          c[q] = e < e1 ? __ldg(col + e) : 0;
+          w[q] = e < e1 ? val[e] : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dv[q] = e0 + 256 * q < e1 ? __ldg(deg + c[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t e = e0 + 256 * q;
+          if (e < e1) val_out[e] = norm_entry(du, dv[q], w[q]);
+        }
+      }
     }
-    if (ue - ub > kNormLong) val_out[e] = norm_entry(__ldg(deg + u), __ldg(deg + __ldg(col + e)), val[e]);
+    return;
+  }
+  __shared__ int64_t s_rp[kNormRows + 1];
+  __shared__ double s_du[kNormRows];
+  const int64_t r0 = (int64_t)(blockIdx.x - n_long) * kNormRows;
+  const int nr = (int)min((int64_t)kNormRows, n - r0);
+  if (tid <= nr) s_rp[tid] = __ldg(rp + r0 + tid);
+  if (tid < nr) s_du[tid] = __ldg(deg + r0 + tid);
+  __syncthreads();
+  const int64_t E0 = s_rp[0], E1 = s_rp[nr];
+  for (int64_t e0 = E0 + tid; e0 < E1; e0 += 4 * 256) {
+    int c[4], row[4];
+    float w[4];
+    double dv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t e = e0 + 256 * q;
+      int j = -1;
+      if (e < E1) {  // largest j with s_rp[j] <= e (the row holding entry e)
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_rp[mid] <= e) lo = mid;
+          else hi = mid - 1;
+        }
+        if (s_rp[lo + 1] - s_rp[lo] <= kNormLong) j = lo;
+      }
+      row[q] = j;
+      c[q] = j >= 0 ? __ldg(col + e) : 0;
+      w[q] = j >= 0 ? val[e] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dv[q] = row[q] >= 0 ? __ldg(deg + c[q]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (row[q] >= 0) val_out[e0 + 256 * q] = norm_entry(s_du[row[q]], dv[q], w[q]);
   }
 }
 
@@ -593,9 +644,8 @@ extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double
   degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, d);
   if ((st = check_launch("degree"))) return st;
   if (a->nnz == 0) return GSP_OK;
-  normalize_kernel<<<(unsigned)ceil_div(a->n_rows, 8), 256, 0, s>>>(a->row_ptr, a->col_idx, a->val, a->n_rows,
-                                                                   d, val_out);
-  normalize_long_kernel<<<(unsigned)ceil_div(a->nnz, 8 * kNormChunk), 256, 0, s>>>(
-      a->row_ptr, a->col_idx, a->val, a->n_rows, a->nnz, d, val_out);
+  const int64_t n_long = ceil_div(a->n_rows, kNormSlice);
+  normalize_kernel<<<(unsigned)(n_long + ceil_div(a->n_rows, kNormRows)), 256, 0, s>>>(
+      a->row_ptr, a->col_idx, a->val, a->n_rows, d, val_out, (int)n_long);
   return check_launch("normalize");
 }
