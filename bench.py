@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TF32_MMA_PEAK = 1035.7  # TFLOP/s, profiles/r2i_mma_peak_probe.txt (tcgen05 kind::tf32, 128x128x8, 148 SMs)
 L2_GATHER_PEAK_GBS = 20264.7  # profiles/r1_probes.txt: ldg U=8, x_MB=17 (random 512-B row gathers from L2)
 FALLBACK_HBM = 6650.0   # GB/s, B200_PROFILING.md fallback
 NOMINAL_HBM = 8000.0    # GB/s, B200 nominal
@@ -588,6 +589,29 @@ def secondaries(ctx, c4, c3):
                                     "softmax_backward_ms": float(np.median(t_sb)),
                                     "aggregate_backward_ms": float(np.median(t_gb))}
     del at3, perm3
+    # NEXT-1 dense step alone: C4 layer 1 (232,965 x 602 -> 128) on the tcgen05
+    # 3xTF32 GEMM, against the measured TF32 MMA rate (tools/mma_peak_probe.cu)
+    # and the HBM copy peak; the x_lo * w_hi, x_hi * w_lo, x_hi * w_hi products
+    # are the work the tensor pipe does
+    fin, fout = f, 128
+    xl = x[:, :fin]
+    wl = torch.from_numpy(features(fin, fout, fout, seed=3)).to(ctx.dev)
+    yl = G.empty_features(n, fout, ctx.dev)
+    import ctypes
+    nbl = ctypes.c_size_t(0)
+    G.lib().gsp_linear_workspace(fin, fout, ctypes.byref(nbl))
+    wsl = torch.empty(max(nbl.value, 16), dtype=torch.uint8, device=ctx.dev)
+    tl_ = ctx.timer.cold(lambda: G.gsp_linear(xl, wl, y=yl, ws=wsl), a.warmup, 20)
+    ml = float(np.median(tl_))
+    tf = 3 * 2.0 * n * fin * fout / (ml * 1e-3) / 1e12
+    bl = 4.0 * (n * fin + n * fout + 2 * fin * fout)
+    out["NEXT1_C4_layer1_dense_step"] = {
+        "ms": ml, "shape": [n, fin, fout], "TFLOPs_tf32_products": tf,
+        "tf32_peak_TFLOPs": TF32_MMA_PEAK, "tf32_frac": tf / TF32_MMA_PEAK,
+        "tf32_peak_kind": "measured tcgen05.mma kind::tf32 M=128 N=128 issue rate (profiles/r2i_mma_peak_probe.txt)",
+        "hbm_GB/s": bl / (ml * 1e-3) / 1e9, "hbm_frac": bl / (ml * 1e-3) / 1e9 / ctx.peak,
+        "kernel": "linear_tc_kernel<true, 2> (3xTF32, CTA pairs sharing W)"}
+    del xl, wl, yl, wsl
     # NEXT-1: the paper's Table spmm_time workload (2-layer GCN / GAT inference,
     # hidden 128, GAT 4 heads; both readings of A20: 4 x 32 and 4 x 128 per head)
     from paper_2103_00959_b200.inference import GATParams, GCNParams, gat_inference, gcn_inference
