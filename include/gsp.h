@@ -364,7 +364,10 @@ gsp_status gsp_attn_project_backward(int64_t n, int32_t heads, int64_t d, const 
  *   MMA's truncated read of the raw fp32 x, w = hi + lo pre-split by
  *   rounding; x w ~= lo.hi + hi.lo + hi.hi, fp32 accumulation in TMEM;
  *   per-product error <= 2^-19 |x||w|), operands staged by TMA (SWIZZLE_64B: 16-float K
- *   tiles), one CTA per (128 rows, <= 256 output columns).  Otherwise (ws
+ *   tiles), one CTA per (128 rows, <= 256 output columns); for f_out <= 128
+ *   and f_in >= 384 two adjacent row tiles run as a cluster (CTA pair) that
+ *   shares the W tiles by TMA multicast (needs cluster launch support, every
+ *   B200).  Results do not depend on the tiling.  Otherwise (ws
  *   NULL / too small, wider or unaligned operands) a
  *   cuBLAS SGEMM with fp32 compute (no TF32); one cuBLAS handle per (thread,
  *   device) is created on first use.
