@@ -382,38 +382,59 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
+// d_u = sum of row u's values in fp64.  A CTA owns 32 rows (4 per warp), their
+// extents staged in shared memory; a warp issues the first 32-entry batch of
+// all four rows before reducing any (lane l adds entries l, l + 32, ... of a
+// row in order, then an xor tree -- the per-row order of one warp per row);
+// rows of more than kNormLong entries are reduced afterwards by the whole CTA
+// (thread t adds entries t, t + 256, ..., xor tree per warp, warps in order).
+constexpr int kDegRows = 32;
 __global__ void __launch_bounds__(256) degree_kernel(const int64_t *__restrict__ rp, const float *__restrict__ val,
                                                      int64_t n, double *__restrict__ deg) {
-  __shared__ int s_long[8];
+  __shared__ int64_t s_rp[kDegRows + 1];
+  __shared__ int s_long[kDegRows];
   __shared__ int s_nlong;
   __shared__ double s_part[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_nlong = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * kDegRows;
+  const int nr = (int)min((int64_t)kDegRows, n - r0);
+  if (tid == 0) s_nlong = 0;
+  if (tid <= nr) s_rp[tid] = __ldg(rp + r0 + tid);
   __syncthreads();
-  const int64_t u = (int64_t)blockIdx.x * 8 + warp;
-  if (u < n) {
-    const int64_t b = __ldg(rp + u), e1 = __ldg(rp + u + 1);
+  float v0[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // first batch of the warp's four rows, all in flight
+    const int j = warp * 4 + q;
+    const int64_t b = j < nr ? s_rp[j] : 0, e1 = j < nr ? s_rp[j + 1] : 0;
+    v0[q] = (j < nr && e1 - b <= kNormLong && b + lane < e1) ? __ldg(val + b + lane) : 0.0f;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = warp * 4 + q;
+    if (j >= nr) break;
+    const int64_t b = s_rp[j], e1 = s_rp[j + 1];
     if (e1 - b > kNormLong) {
-      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = warp;
-    } else {
-      double s = 0.0;
-#pragma unroll 4
-      for (int64_t e = b + lane; e < e1; e += 32) s += (double)__ldg(val + e);
-      s = warp_sum_f64(s);
-      if (lane == 0) deg[u] = s;
+      if (lane == 0) s_long[atomicAdd(&s_nlong, 1)] = j;
+      continue;
     }
+    double sum = 0.0;
+    if (b + lane < e1) sum += (double)v0[q];
+#pragma unroll 4
+    for (int64_t e = b + lane + 32; e < e1; e += 32) sum += (double)__ldg(val + e);
+    sum = warp_sum_f64(sum);
+    if (lane == 0) deg[r0 + j] = sum;
   }
   __syncthreads();
   for (int k = 0; k < s_nlong; ++k) {
-    const int64_t r = (int64_t)blockIdx.x * 8 + s_long[k];
-    const int64_t b = __ldg(rp + r), e1 = __ldg(rp + r + 1);
-    double s = 0.0;
+    const int64_t r = r0 + s_long[k];
+    const int64_t b = s_rp[s_long[k]], e1 = s_rp[s_long[k] + 1];
+    double sum = 0.0;
 #pragma unroll 4
-    for (int64_t e = b + threadIdx.x; e < e1; e += 256) s += (double)__ldg(val + e);
-    s = warp_sum_f64(s);
-    if (lane == 0) s_part[warp] = s;
+    for (int64_t e = b + tid; e < e1; e += 256) sum += (double)__ldg(val + e);
+    sum = warp_sum_f64(sum);
+    if (lane == 0) s_part[warp] = sum;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       double t = s_part[0];
       for (int w = 1; w < 8; ++w) t += s_part[w];
       deg[r] = t;
@@ -640,7 +661,7 @@ extern "C" gsp_status gsp_sym_normalize(const gsp_csr *a, float *val_out, double
   if (val_out && overlaps(val_out, (size_t)a->nnz * 4, d, (size_t)a->n_rows * 8))
     return fail(GSP_ERR_ALIAS, "%s: val_out overlaps the degree array", fn);
   cudaStream_t s = cs(stream);
-  const unsigned gb = (unsigned)ceil_div(a->n_rows, 8);
+  const unsigned gb = (unsigned)ceil_div(a->n_rows, kDegRows);
   degree_kernel<<<gb, 256, 0, s>>>(a->row_ptr, a->val, a->n_rows, d);
   if ((st = check_launch("degree"))) return st;
   if (a->nnz == 0) return GSP_OK;
