@@ -516,22 +516,29 @@ __global__ void __launch_bounds__(256) normalize_kernel(const int64_t *__restric
   if (tid < nr) s_du[tid] = __ldg(deg + r0 + tid);
   __syncthreads();
   const int64_t E0 = s_rp[0], E1 = s_rp[nr];
-  for (int64_t e0 = E0 + tid; e0 < E1; e0 += 4 * 256) {
+  const int lane = tid & 31;
+  // lane l holds the start of row l + 1 (rows 1 .. nr - 1; later lanes: never
+  // <= an entry).  The row of entry e is #{j >= 1 : s_rp[j] <= e}: a warp's 32
+  // consecutive entries c .. c + 31 start from row(c) = one ballot, then each
+  // lane steps forward over the (few) rows starting inside the chunk
+  const int64_t start_l = lane + 1 < nr ? s_rp[lane + 1] : INT64_MAX;
+  // warp-uniform loop (every lane reaches the ballots): warp w takes the
+  // 32-entry chunks E0 + 32 w + 256 k
+  for (int64_t wb = E0 + (tid & ~31); wb < E1; wb += 4 * 256) {
+    const int64_t e0 = wb + lane;
     int c[4], row[4];
     float w[4];
     double dv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t e = e0 + 256 * q;
-      int j = -1;
-      if (e < E1) {  // largest j with s_rp[j] <= e (the row holding entry e)
-        int lo = 0, hi = nr - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s_rp[mid] <= e) lo = mid;
-          else hi = mid - 1;
-        }
-        if (s_rp[lo + 1] - s_rp[lo] <= kNormLong) j = lo;
+      const int64_t cw = wb + 256 * q;  // the chunk's first entry (warp-uniform)
+      int j = __popc(__ballot_sync(0xffffffffu, start_l <= cw));
+      if (e < E1) {
+        while (j + 1 < nr && s_rp[j + 1] <= e) ++j;
+        if (s_rp[j + 1] - s_rp[j] > kNormLong) j = -1;
+      } else {
+        j = -1;
       }
       row[q] = j;
       c[q] = j >= 0 ? __ldg(col + e) : 0;
