@@ -211,39 +211,60 @@ template <typename IT>
 __global__ void make_keys_kernel(int64_t n, int64_t m, const IT *__restrict__ src, const IT *__restrict__ dst,
                                  const float *__restrict__ w, int und, int with_loops, uint64_t *__restrict__ keys,
                                  uint32_t *__restrict__ vals, uint32_t *__restrict__ err) {
+  // one thread per input pair i (both slots 2i, 2i + 1 of an undirected pair
+  // in one 16-byte key store and one 8-byte value store), then one per loop
   const int64_t mm = und ? 2 * m : m;
-  const int64_t S = mm + (with_loops ? n : 0);
+  const int64_t T = m + (with_loops ? n : 0);
   const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < S; t += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t key;
-    if (t < mm) {
-      const int64_t i = und ? (t >> 1) : t;
-      const bool rev = und && (t & 1);
-      const int64_t u = (int64_t)src[i], v = (int64_t)dst[i];
-      uint32_t e = 0;
-      if (u < 0 || u >= n || v < 0 || v >= n) e |= kErrRange;
-      if (w && !rev) {
-        const float wi = w[i];
-        if (!isfinite(wi)) e |= kErrNonfinite;
-        else if (wi < 0.0f) e |= kErrNeg;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < m) {
+      const int64_t u = (int64_t)src[t], v = (int64_t)dst[t];
+      const uint32_t er = (u < 0 || u >= n || v < 0 || v >= n) ? kErrRange : 0u;
+      uint32_t ef = er;  // the forward slot also validates the weight
+      if (w) {
+        const float wi = w[t];
+        if (!isfinite(wi)) ef |= kErrNonfinite;
+        else if (wi < 0.0f) ef |= kErrNeg;
       }
-      if (e) atomicOr(err, e);
-      if (e || (rev && u == v)) key = EMPTY;
-      else key = rev ? (uint64_t)v * n + u : (uint64_t)u * n + v;
+      if (ef) atomicOr(err, ef);
+      const uint64_t kf = ef ? EMPTY : (uint64_t)u * n + v;
+      if (und) {
+        const uint64_t kr = (er || u == v) ? EMPTY : (uint64_t)v * n + u;  // reverse of a self pair: none
+        *reinterpret_cast<ulonglong2 *>(keys + 2 * t) = make_ulonglong2(kf, kr);
+        *reinterpret_cast<uint2 *>(vals + 2 * t) = make_uint2((uint32_t)(2 * t), (uint32_t)(2 * t + 1));
+      } else {
+        keys[t] = kf;
+        vals[t] = (uint32_t)t;
+      }
     } else {
-      const uint64_t u = (uint64_t)(t - mm);
-      key = u * n + u;
+      const uint64_t u = (uint64_t)(t - m);
+      keys[mm + (int64_t)u] = u * n + u;
+      vals[mm + (int64_t)u] = (uint32_t)(mm + (int64_t)u);
     }
-    keys[t] = key;
-    vals[t] = (uint32_t)t;
   }
 }
 
 __global__ void head_flags_kernel(const uint64_t *__restrict__ keys, int64_t S, uint64_t EMPTY,
                                   uint32_t *__restrict__ head) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = keys[k];
-    head[k] = (key < EMPTY && (k == 0 || keys[k - 1] != key)) ? 1u : 0u;
+  // 4 keys per thread (two 16-byte loads, one 16-byte store of the flags)
+  for (int64_t k = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); k < S;
+       k += 4 * (int64_t)gridDim.x * blockDim.x) {
+    if (k + 4 <= S) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(keys + k);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(keys + k + 2);
+      const uint64_t p = k ? keys[k - 1] : ~0ull;
+      uint4 f;
+      f.x = (a.x < EMPTY && (k == 0 || p != a.x)) ? 1u : 0u;
+      f.y = (a.y < EMPTY && a.x != a.y) ? 1u : 0u;
+      f.z = (b.x < EMPTY && a.y != b.x) ? 1u : 0u;
+      f.w = (b.y < EMPTY && b.x != b.y) ? 1u : 0u;
+      *reinterpret_cast<uint4 *>(head + k) = f;
+    } else {
+      for (int64_t j = k; j < S; ++j) {
+        const uint64_t key = keys[j];
+        head[j] = (key < EMPTY && (j == 0 || keys[j - 1] != key)) ? 1u : 0u;
+      }
+    }
   }
 }
 
@@ -607,11 +628,13 @@ extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, cons
 
   if (cudaMemsetAsync(W + Lw.scalars, 0, 16, s) != cudaSuccess) return check_launch("memset");
   const unsigned gb = (unsigned)std::min<int64_t>(ceil_div(S, 256), 65535 * 4);
+  const unsigned gk = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m + n, 256), 65535 * 4));
+  const unsigned gh = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(S, 4 * 256), 65535 * 4));
   if (it == GSP_I32)
-    make_keys_kernel<int32_t><<<gb, 256, 0, s>>>(n, m, (const int32_t *)src, (const int32_t *)dst, w, und,
+    make_keys_kernel<int32_t><<<gk, 256, 0, s>>>(n, m, (const int32_t *)src, (const int32_t *)dst, w, und,
                                                  fill != 0.0f, ka, va, d_err);
   else
-    make_keys_kernel<int64_t><<<gb, 256, 0, s>>>(n, m, (const int64_t *)src, (const int64_t *)dst, w, und,
+    make_keys_kernel<int64_t><<<gk, 256, 0, s>>>(n, m, (const int64_t *)src, (const int64_t *)dst, w, und,
                                                  fill != 0.0f, ka, va, d_err);
   gsp_status st = check_launch("make_keys");
   if (st) return st;
@@ -619,7 +642,7 @@ extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, cons
   // stable LSD radix sort over the bits of EMPTY = n*n
   if ((st = radix_sort_pairs(ka, va, kb, vb, S, key_bits(n), counts, scan_ws, s))) return st;
   const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
-  head_flags_kernel<<<gb, 256, 0, s>>>(ka, S, EMPTY, head);
+  head_flags_kernel<<<gh, 256, 0, s>>>(ka, S, EMPTY, head);
   if ((st = check_launch("head_flags"))) return st;
   if ((st = scan_exclusive(head, idx, S, scan_ws, s))) return st;
   fill_i64_kernel<<<1, 256, 0, s>>>(row_ptr, 1, 0);  // row_ptr[0] = 0 even if row 0 is empty
