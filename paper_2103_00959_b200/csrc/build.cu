@@ -284,37 +284,64 @@ __global__ void coalesce_kernel(const uint64_t *__restrict__ keys, const uint32_
                                 const uint32_t *__restrict__ head, const uint32_t *__restrict__ idx,
                                 int64_t *__restrict__ row_ptr, int32_t *__restrict__ col, float *__restrict__ val,
                                 int64_t *__restrict__ nnz_out) {
+  // 4 consecutive sorted slots per thread: keys / head / idx / pos by 16-byte
+  // loads, each key's row computed once (the previous slot's row carried)
   const uint64_t EMPTY = (uint64_t)n * (uint64_t)n;
   const int64_t mm = und ? 2 * m : m;
   const double inv_n = 1.0 / (double)n;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < S; k += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = keys[k];
-    if (key >= EMPTY) continue;
-    const bool last_valid = (k + 1 == S) || keys[k + 1] >= EMPTY;
-    const int64_t r = (int64_t)div_by_n(key, (uint64_t)n, inv_n);
-    if (head[k]) {
-      double s = 0.0;
-      for (int64_t j = k; j < S && keys[j] == key; ++j) {
-        const int64_t p = pos[j];
-        double wj;
-        if (p < mm) {
-          const int64_t i = und ? (p >> 1) : p;
-          wj = w ? (double)w[i] : 1.0;
-        } else {
-          wj = (double)fill;
-        }
-        s = __dadd_rn(s, wj);
+  for (int64_t k0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); k0 < S;
+       k0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    uint64_t kk[5];  // keys k0 .. k0 + 3 and k0 + 4 (EMPTY past the end)
+    uint32_t hd[4], ix[4];
+    if (k0 + 4 <= S) {
+      const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(keys + k0);
+      const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(keys + k0 + 2);
+      kk[0] = a.x, kk[1] = a.y, kk[2] = b.x, kk[3] = b.y;
+      const uint4 h = *reinterpret_cast<const uint4 *>(head + k0);
+      const uint4 x = *reinterpret_cast<const uint4 *>(idx + k0);
+      hd[0] = h.x, hd[1] = h.y, hd[2] = h.z, hd[3] = h.w;
+      ix[0] = x.x, ix[1] = x.y, ix[2] = x.z, ix[3] = x.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        kk[q] = k0 + q < S ? keys[k0 + q] : EMPTY;
+        hd[q] = k0 + q < S ? head[k0 + q] : 0u;
+        ix[q] = k0 + q < S ? idx[k0 + q] : 0u;
       }
-      const int64_t o = idx[k];
-      col[o] = (int32_t)(key - (uint64_t)r * n);
-      val[o] = __double2float_rn(s);
-      const int64_t prev_r = (k == 0) ? -1 : (int64_t)div_by_n(keys[k - 1], (uint64_t)n, inv_n);
-      for (int64_t rr = prev_r + 1; rr <= r; ++rr) row_ptr[rr] = o;
     }
-    if (last_valid) {
-      const int64_t total = (int64_t)idx[k] + head[k];
-      for (int64_t rr = r + 1; rr <= n; ++rr) row_ptr[rr] = total;
-      *nnz_out = total;
+    kk[4] = k0 + 4 < S ? keys[k0 + 4] : EMPTY;
+    int64_t prev_r = (k0 == 0) ? -1 : (int64_t)div_by_n(keys[k0 - 1], (uint64_t)n, inv_n);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = k0 + q;
+      const uint64_t key = kk[q];
+      if (k >= S || key >= EMPTY) break;  // sorted: EMPTY keys only at the end
+      const bool last_valid = kk[q + 1] >= EMPTY;
+      const int64_t r = (int64_t)div_by_n(key, (uint64_t)n, inv_n);
+      if (hd[q]) {
+        double sum = 0.0;
+        for (int64_t j = k; j < S && keys[j] == key; ++j) {
+          const int64_t p = pos[j];
+          double wj;
+          if (p < mm) {
+            const int64_t i = und ? (p >> 1) : p;
+            wj = w ? (double)w[i] : 1.0;
+          } else {
+            wj = (double)fill;
+          }
+          sum = __dadd_rn(sum, wj);
+        }
+        const int64_t o = ix[q];
+        col[o] = (int32_t)(key - (uint64_t)r * n);
+        val[o] = __double2float_rn(sum);
+        for (int64_t rr = prev_r + 1; rr <= r; ++rr) row_ptr[rr] = o;
+      }
+      if (last_valid) {
+        const int64_t total = (int64_t)ix[q] + hd[q];
+        for (int64_t rr = r + 1; rr <= n; ++rr) row_ptr[rr] = total;
+        *nnz_out = total;
+      }
+      prev_r = r;
     }
   }
 }
@@ -646,7 +673,7 @@ extern "C" gsp_status gsp_coo_to_csr(int64_t n, int64_t m, const void *src, cons
   if ((st = check_launch("head_flags"))) return st;
   if ((st = scan_exclusive(head, idx, S, scan_ws, s))) return st;
   fill_i64_kernel<<<1, 256, 0, s>>>(row_ptr, 1, 0);  // row_ptr[0] = 0 even if row 0 is empty
-  coalesce_kernel<<<gb, 256, 0, s>>>(ka, va, S, n, m, und, w, fill, head, idx, row_ptr, col_idx, val, d_nnz);
+  coalesce_kernel<<<gh, 256, 0, s>>>(ka, va, S, n, m, und, w, fill, head, idx, row_ptr, col_idx, val, d_nnz);
   if ((st = check_launch("coalesce"))) return st;
 
   struct {
