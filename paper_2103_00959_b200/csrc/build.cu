@@ -115,10 +115,22 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const uint64_
   h[tid] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  if (base + kRadixTile <= N) {  // full tile: 16-byte loads (2 keys), all issued before the atomics
+    ulonglong2 kv[kRadixItems / 2];
 #pragma unroll
-  for (int i = 0; i < kRadixItems; ++i) {
-    const int64_t k = base + (int64_t)i * kRadixThreads + tid;
-    if (k < N) atomicAdd(&h[(unsigned)(keys[k] >> shift) & 255u], 1u);
+    for (int i = 0; i < kRadixItems / 2; ++i)
+      kv[i] = *reinterpret_cast<const ulonglong2 *>(keys + base + 2 * ((int64_t)i * kRadixThreads + tid));
+#pragma unroll
+    for (int i = 0; i < kRadixItems / 2; ++i) {
+      atomicAdd(&h[(unsigned)(kv[i].x >> shift) & 255u], 1u);
+      atomicAdd(&h[(unsigned)(kv[i].y >> shift) & 255u], 1u);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kRadixItems; ++i) {
+      const int64_t k = base + (int64_t)i * kRadixThreads + tid;
+      if (k < N) atomicAdd(&h[(unsigned)(keys[k] >> shift) & 255u], 1u);
+    }
   }
   __syncthreads();
   counts[(int64_t)tid * ntiles + blockIdx.x] = h[tid];
